@@ -1,0 +1,160 @@
+/*
+ * abftlp_b200.h -- device-pointer operator entry points of the B200 ABFT library.
+ *
+ * These are the hot-path operators the reference keeps as C++ functions
+ * (P:src/gemm_abft.hpp:23-74, P:src/embedding_abft.hpp:38-52, P:src/fault_lab.hpp:98-106),
+ * exposed in the same C conventions as abftlp.h: plain pointers and sizes, status codes,
+ * thread-local abftlp_last_error(), explicit _free for every handle.
+ *
+ * All d_* pointers are device pointers; `stream` is a cudaStream_t (NULL = legacy default
+ * stream). Calls are asynchronous on `stream` unless documented otherwise. Encoded weights
+ * and tables are immutable after creation and may be shared by concurrent calls on different
+ * streams; per-call scratch lives in a per-stream workspace inside the library.
+ */
+#ifndef ABFTLP_B200_H
+#define ABFTLP_B200_H
+
+#include "abftlp.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef void* abftlp_stream;
+
+/* ------------------------------------------------------------------ int8 ABFT GEMM */
+typedef struct abftlp_gemm_weight_s abftlp_gemm_weight;
+
+/* Encode B (s8, k x n, row-major, leading dimension ldb >= n) once: mod-127 row checksums
+ * cs[k] (each in [0,126]) plus B' in the GEMM's K-major TMA layout.
+ * Replaces compute_row_checksums (P:src/gemm_abft.cpp:60-71) + PackedEncodedWeight
+ * (P:src/gemm_abft.cpp:73-85). Empty B -> ABFTLP_ERR_INVALID_ARGUMENT. */
+abftlp_status abftlp_gemm_encode(const int8_t* d_b, uint64_t k, uint64_t n, uint64_t ldb,
+                                 abftlp_stream stream, abftlp_gemm_weight** out);
+void abftlp_gemm_weight_free(abftlp_gemm_weight* w);
+/* PackedEncodedWeight::k()/n() (P:src/gemm_abft.hpp:37-38). */
+abftlp_status abftlp_gemm_weight_dims(const abftlp_gemm_weight* w, uint64_t* k, uint64_t* n);
+/* Copies WeightChecksum::values (k int8) to d_cs. */
+abftlp_status abftlp_gemm_weight_checksums(const abftlp_gemm_weight* w, int8_t* d_cs, abftlp_stream stream);
+/* Replaces the stored checksum column with d_cs (k int8): PackedEncodedWeight(b, cs) with a
+ * caller-supplied WeightChecksum (P:src/gemm_abft.cpp:73-85) -- e.g. checksums of the pristine
+ * B packed next to a B corrupted after encoding (P:src/fault_lab.cpp:186-189). */
+abftlp_status abftlp_gemm_weight_set_checksums(abftlp_gemm_weight* w, const int8_t* d_cs,
+                                               abftlp_stream stream);
+/* Reads the logical k x (n+1) encoded matrix [B | cs] to d_out (row-major, ld = n+1):
+ * the PackedEncodedWeight::at(i, j) contract (P:src/gemm_abft.cpp:87-91). */
+abftlp_status abftlp_gemm_weight_read(const abftlp_gemm_weight* w, int8_t* d_out, abftlp_stream stream);
+
+/* In-epilogue fault hook: flip `bit` (0..31) of C'(row, col), col <= n (col == n hits the
+ * checksum column), after the product and before verification -- the reference's
+ * inject_intermediate_C point (P:src/fault_lab.cpp:192-195). */
+typedef struct {
+    int32_t active;
+    uint64_t row;
+    uint64_t col;
+    uint32_t bit;
+} abftlp_fault;
+
+/* Checked GEMM: C = A x B (int32, m x n, ld ldc), csum[i] = C'[i][n] = sum_p A[i][p]*cs[p]
+ * (stride csum_ld), row_flags[i] = mod127(sum_j C[i][j]) != mod127(csum[i]),
+ * *d_err_count = number of flagged rows. A is u8 m x k (ld lda >= k).
+ * Replaces abft_gemm + verify_checksums (P:src/gemm_abft.cpp:93-100, 113-124). The result is
+ * returned even when rows are flagged. Pass d_c = C' and d_csum = C' + n, ldc = csum_ld = n+1
+ * to obtain the reference's m x (n+1) cTemp layout directly. */
+abftlp_status abftlp_gemm_checked(const uint8_t* d_a, uint64_t m, uint64_t lda,
+                                  const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
+                                  int32_t* d_csum, uint64_t csum_ld, uint8_t* d_row_flags,
+                                  uint32_t* d_err_count, const abftlp_fault* fault,
+                                  abftlp_stream stream);
+/* Same kernel with checking compiled out (no checksum MMA, no residue epilogue): the
+ * apples-to-apples baseline. Replaces plain_gemm (P:src/gemm_abft.cpp:102-111). */
+abftlp_status abftlp_gemm_unchecked(const uint8_t* d_a, uint64_t m, uint64_t lda,
+                                    const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
+                                    abftlp_stream stream);
+/* Standalone row check over an existing C and checksum column (faults injected after the
+ * product). Replaces verify_checksums (P:src/gemm_abft.cpp:113-124). */
+abftlp_status abftlp_gemm_verify(const int32_t* d_c, uint64_t ldc, const int32_t* d_csum,
+                                 uint64_t csum_ld, uint64_t m, uint64_t n, uint8_t* d_row_flags,
+                                 uint32_t* d_err_count, abftlp_stream stream);
+/* Host-buffer convenience (the "e2e" path): copies A in, runs the checked GEMM, copies
+ * C, csum, flags and the count out; synchronous. Any output pointer may be NULL. */
+abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t lda,
+                                       const abftlp_gemm_weight* w, int32_t* c, uint64_t ldc,
+                                       int32_t* csum, uint8_t* row_flags, uint32_t* err_count,
+                                       abftlp_stream stream);
+
+/* ------------------------------------------------------------------ EmbeddingBag */
+typedef struct abftlp_eb_table_s abftlp_eb_table;
+
+#define ABFTLP_EB_S8 0  /* int8 rows (the reference's QuantEmbeddingTable) */
+#define ABFTLP_EB_U8 1  /* uint8 rows */
+#define ABFTLP_EB_U4 2  /* packed 4-bit rows: element j = (byte[j/2] >> 4*(j&1)) & 0xF */
+#define ABFTLP_EB_SCALE_F32 0
+#define ABFTLP_EB_SCALE_F16 1
+
+/* Build a checked table over device rows (borrowed: the caller keeps them alive and
+ * immutable) plus per-row scale/bias (f32 or f16). Row sums (int32) are computed on the
+ * device -- precompute_row_sums (P:src/embedding_abft.cpp:39-45) -- unless d_row_sums is
+ * given, in which case those are stored as-is (load_table(validate=false) semantics). */
+abftlp_status abftlp_eb_table_create(int32_t elem_type, const void* d_rows, uint64_t rows,
+                                     uint64_t dim, uint64_t row_stride_bytes, int32_t scale_type,
+                                     const void* d_scales, const void* d_biases,
+                                     const int32_t* d_row_sums, abftlp_stream stream,
+                                     abftlp_eb_table** out);
+void abftlp_eb_table_free(abftlp_eb_table* t);
+/* Synchronous: number of rows whose d_row_sums entry differs from the recomputed sum
+ * (load_table validation, P:src/embedding_abft.cpp:139-143). */
+abftlp_status abftlp_eb_table_validate(const abftlp_eb_table* t, const int32_t* d_row_sums,
+                                       abftlp_stream stream, uint64_t* mismatched_rows);
+/* Device row sums of the table (int32[rows]). */
+abftlp_status abftlp_eb_table_row_sums(const abftlp_eb_table* t, int32_t* d_out, abftlp_stream stream);
+
+/* Checked pooled lookups over CSR bags: bag b = indices[offsets[b] .. offsets[b+1]),
+ * optional per-lookup weights (NULL = unweighted). out[b][0..dim) (ld_out), flags[b],
+ * rsum[b], csum[b] (nullable), *d_flag_count (nullable) = flagged bags. Indices >= rows set
+ * bit 0 of *d_status (nullable) -- the reference's out_of_range (P:src/embedding_abft.cpp:16-22).
+ * Replaces abft_embedding_bag / batch_abft_eb (P:src/embedding_abft.cpp:62-91). */
+abftlp_status abftlp_eb_checked(const abftlp_eb_table* t, const int64_t* d_offsets,
+                                const int64_t* d_indices, uint64_t num_bags,
+                                const float* d_weights, float* d_out, uint64_t ld_out,
+                                uint8_t* d_flags, double* d_rsum, double* d_csum,
+                                uint32_t* d_flag_count, int32_t* d_status, abftlp_stream stream);
+/* Same lookups without the check. Replaces embedding_bag (P:src/embedding_abft.cpp:47-60). */
+abftlp_status abftlp_eb_unchecked(const abftlp_eb_table* t, const int64_t* d_offsets,
+                                  const int64_t* d_indices, uint64_t num_bags,
+                                  const float* d_weights, float* d_out, uint64_t ld_out,
+                                  int32_t* d_status, abftlp_stream stream);
+
+/* ------------------------------------------------------------------ fault injection */
+/* XOR bit `bit` of element `index` of an array of `elem_bytes`-wide integers
+ * (flip_bit, P:src/fault_lab.hpp:87-93). */
+abftlp_status abftlp_flip_bit(void* d_ptr, uint32_t elem_bytes, uint64_t index, uint32_t bit,
+                              abftlp_stream stream);
+/* Flip bit of encoded weight element B'(i, j), j < n (inject_weight_B after encoding,
+ * P:src/fault_lab.cpp:98-115); j == n hits the checksum column. */
+abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uint64_t j,
+                                          uint32_t bit, abftlp_stream stream);
+/* Flip bit (< element width) of table element (row, col) after row sums were computed
+ * (inject_eb_table, P:src/fault_lab.cpp:139-166). Mutates the caller's row buffer. */
+abftlp_status abftlp_eb_table_flip_bit(abftlp_eb_table* t, uint64_t row, uint64_t col,
+                                       uint32_t bit, abftlp_stream stream);
+/* Seeded generators reproducing SplitMix64(seed, stream) draws off .. off+count-1
+ * (P:src/rng.hpp:10-43): kind 0 = u8 next_below(256), 1 = s8 next_int(-128,127),
+ * 2 = f32 (float)next_real(lo, hi), 3 = i64 next_below(bound). */
+abftlp_status abftlp_generate(void* d_out, uint64_t count, uint64_t seed, uint64_t rng_stream,
+                              uint64_t off, int32_t kind, double lo, double hi, uint64_t bound,
+                              abftlp_stream stream);
+/* Writes a buffer larger than L2 (benchmark cache flush). */
+abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ABFTLP_B200_H */

@@ -1,0 +1,511 @@
+// C ABI of libabftlp_b200.so: the reference-compatible surface (include/abftlp.h) and the
+// device-pointer operator entry points (include/abftlp_b200.h).
+//
+// Error model mirrors the reference's `guarded` (P:src/capi.cpp:28-41): invalid_argument and
+// out_of_range -> ABFTLP_ERR_INVALID_ARGUMENT, runtime_error -> ABFTLP_ERR_IO, anything else
+// (including CUDA failures) -> ABFTLP_ERR_INTERNAL; the message goes to a thread-local string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iomanip>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/abftlp_b200.h"
+#include "campaign.h"
+#include "runtime.h"
+
+struct abftlp_campaign_s {
+    abftk::CampaignConfig cfg;
+};
+struct abftlp_report_s {
+    abftk::CampaignReport report;
+};
+struct abftlp_gemm_weight_s {
+    abftk::GemmWeight* w;
+};
+struct abftlp_eb_table_s {
+    abftk::EbTable* t;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+abftlp_status fail(abftlp_status code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename Fn>
+abftlp_status guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const std::invalid_argument& e) {
+        return fail(ABFTLP_ERR_INVALID_ARGUMENT, e.what());
+    } catch (const std::out_of_range& e) {
+        return fail(ABFTLP_ERR_INVALID_ARGUMENT, e.what());
+    } catch (const abftk::CudaError& e) {
+        return fail(ABFTLP_ERR_INTERNAL, e.what());
+    } catch (const std::runtime_error& e) {
+        return fail(ABFTLP_ERR_IO, e.what());
+    } catch (const std::exception& e) {
+        return fail(ABFTLP_ERR_INTERNAL, e.what());
+    }
+}
+
+char* dup_string(const std::string& s) {
+    char* out = new char[s.size() + 1];
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return out;
+}
+
+cudaStream_t as_stream(abftlp_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Per-stream device staging for the host-buffer entry points.
+struct HostStage {
+    uint8_t* a = nullptr;
+    size_t a_cap = 0;
+    int32_t* c = nullptr;
+    size_t c_cap = 0;
+    int32_t* csum = nullptr;
+    size_t csum_cap = 0;
+    uint8_t* flags = nullptr;
+    size_t flags_cap = 0;
+    uint32_t* err = nullptr;
+};
+std::mutex g_stage_mu;
+std::unordered_map<uint64_t, HostStage> g_stage;
+
+template <typename T>
+void ensure(T*& p, size_t& cap, size_t need) {
+    if (need <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    ABFT_CUDA(cudaMalloc(&p, need * sizeof(T)));
+    cap = need;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ============================================================ status
+const char* abftlp_status_str(abftlp_status status) {
+    switch (status) {
+        case ABFTLP_OK: return "ok";
+        case ABFTLP_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case ABFTLP_ERR_IO: return "i/o error";
+        case ABFTLP_ERR_PARSE: return "parse error";
+        case ABFTLP_ERR_INTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+const char* abftlp_last_error(void) { return g_last_error.c_str(); }
+
+// ============================================================ campaigns
+abftlp_status abftlp_campaign_load(const char* config_path, abftlp_campaign** out) {
+    if (!config_path || !out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        std::ifstream in(config_path);
+        if (!in) return fail(ABFTLP_ERR_IO, std::string("config not found: ") + config_path);
+        std::ostringstream buf;
+        buf << in.rdbuf();
+        try {
+            *out = new abftlp_campaign_s{abftk::parse_campaign_config(buf.str())};
+        } catch (const std::invalid_argument& e) {
+            return fail(ABFTLP_ERR_PARSE, e.what());
+        }
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_campaign_parse(const char* config_text, abftlp_campaign** out) {
+    if (!config_text || !out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        try {
+            *out = new abftlp_campaign_s{abftk::parse_campaign_config(config_text)};
+        } catch (const std::invalid_argument& e) {
+            return fail(ABFTLP_ERR_PARSE, e.what());
+        }
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_campaign_free(abftlp_campaign* campaign) { delete campaign; }
+
+abftlp_status abftlp_campaign_run(const abftlp_campaign* campaign, abftlp_report** out) {
+    if (!campaign || !out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        *out = new abftlp_report_s{abftk::run_campaign(campaign->cfg)};
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_report_free(abftlp_report* report) { delete report; }
+uint64_t abftlp_report_trials(const abftlp_report* report) { return report->report.trials; }
+uint64_t abftlp_report_detected(const abftlp_report* report) { return report->report.detected; }
+uint64_t abftlp_report_false_positives(const abftlp_report* report) { return report->report.falsePositives; }
+double abftlp_report_detection_rate(const abftlp_report* report) { return report->report.detectionRate(); }
+
+abftlp_status abftlp_report_write_csv(const abftlp_report* report, const char* path) {
+    if (!report || !path) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        std::ofstream out(path);
+        if (!out) return fail(ABFTLP_ERR_IO, std::string("cannot write: ") + path);
+        out << abftk::report_to_csv(report->report);
+        return out ? ABFTLP_OK : fail(ABFTLP_ERR_IO, std::string("write failed: ") + path);
+    });
+}
+
+abftlp_status abftlp_report_render(const abftlp_report* report, char** out) {
+    if (!report || !out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        *out = dup_string(abftk::report_to_table(report->report));
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_string_free(char* s) { delete[] s; }
+
+// ============================================================ analysis (closed forms)
+abftlp_status abftlp_analyze(uint64_t m, uint64_t n, uint64_t k, uint64_t d, uint64_t pool, abftlp_analysis* out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("encode_overhead: zero dimension");
+        if (pool < 1 || d < 1) throw std::invalid_argument("eb_overhead: zero argument");
+        const double dm = double(m), dn = double(n), dk = double(k);
+        abftlp_analysis a{};
+        a.encode_overhead_a = 1.0 / (2.0 * dn) + 1.0 / dm + 1.0 / (2.0 * dk);
+        a.encode_overhead_b = 1.0 / (2.0 * dm) + 1.0 / dn + 1.0 / (2.0 * dk);
+        a.p_detect_b_bitflip = 1.0 - std::pow(3.0 / 256.0, dm);
+        a.p_detect_b_random = 1.0 - std::pow(1018.0 / 32640.0, dm);
+        a.p_detect_c_bitflip = 1.0;
+        a.p_detect_c_random = 1.0 - 1.0 / 127.0;
+        a.eb_overhead = 1.0 / double(d) + 1.0 / (3.0 * double(pool));
+        a.eb_memory_overhead = 32.0 / (8.0 * double(d));
+        *out = a;
+        return ABFTLP_OK;
+    });
+}
+
+// ============================================================ benches (GPU)
+abftlp_status abftlp_bench_gemm(uint64_t m, uint64_t n, uint64_t k, uint32_t repetitions, uint64_t seed,
+                                abftlp_bench_result* out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::BenchTimes r = abftk::bench_gemm(m, n, k, repetitions, seed);
+        *out = {r.baseline_ns, r.abft_ns, (r.abft_ns - r.baseline_ns) / r.baseline_ns};
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_bench_eb(uint64_t table_rows, uint64_t dim, uint64_t pooling, uint64_t batch,
+                              uint32_t repetitions, uint64_t seed, abftlp_bench_result* out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::BenchTimes r = abftk::bench_eb(table_rows, dim, pooling, batch, repetitions, seed);
+        *out = {r.baseline_ns, r.abft_ns, (r.abft_ns - r.baseline_ns) / r.baseline_ns};
+        return ABFTLP_OK;
+    });
+}
+
+// ============================================================ eb-check over files
+abftlp_status abftlp_eb_check_files(const char* table_path, const char* indices_path, int skip_validation,
+                                    uint64_t* bags_out, uint64_t* flagged_out, char** render_out) {
+    if (!table_path || !indices_path) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::HostTable table = abftk::load_table_file(table_path);
+        std::ifstream in(indices_path);
+        if (!in) return fail(ABFTLP_ERR_IO, std::string("indices file not found: ") + indices_path);
+        abftk::HostBags bags;
+        std::string perr;
+        if (!abftk::parse_bag_lines(in, bags, perr)) return fail(ABFTLP_ERR_PARSE, perr);
+        std::vector<abftk::EbResultHost> res = abftk::check_bags_on_device(table, bags, skip_validation == 0);
+        uint64_t flagged = 0;
+        std::ostringstream render;
+        for (size_t i = 0; i < res.size(); ++i) {
+            flagged += res[i].err ? 1 : 0;
+            render << "bag " << i << ": " << (res[i].err ? "ERROR" : "ok") << " rsum=" << res[i].rsum
+                   << " csum=" << res[i].csum << "\n";
+        }
+        if (bags_out) *bags_out = res.size();
+        if (flagged_out) *flagged_out = flagged;
+        if (render_out) *render_out = dup_string(render.str());
+        return ABFTLP_OK;
+    });
+}
+
+// ============================================================ device operators: GEMM
+abftlp_status abftlp_gemm_encode(const int8_t* d_b, uint64_t k, uint64_t n, uint64_t ldb, abftlp_stream stream,
+                                 abftlp_gemm_weight** out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::GemmWeight* w = abftk::encode_weight(d_b, static_cast<int64_t>(k), static_cast<int64_t>(n),
+                                                    static_cast<int64_t>(ldb), as_stream(stream));
+        *out = new abftlp_gemm_weight_s{w};
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_gemm_weight_free(abftlp_gemm_weight* w) {
+    if (!w) return;
+    abftk::free_weight(w->w);
+    delete w;
+}
+
+abftlp_status abftlp_gemm_weight_dims(const abftlp_gemm_weight* w, uint64_t* k, uint64_t* n) {
+    if (!w || !k || !n) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    *k = static_cast<uint64_t>(w->w->k);
+    *n = static_cast<uint64_t>(w->w->n);
+    return ABFTLP_OK;
+}
+
+abftlp_status abftlp_gemm_weight_checksums(const abftlp_gemm_weight* w, int8_t* d_cs, abftlp_stream stream) {
+    if (!w || !d_cs) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        ABFT_CUDA(cudaMemcpyAsync(d_cs, w->w->cs, static_cast<size_t>(w->w->k), cudaMemcpyDeviceToDevice,
+                                  as_stream(stream)));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_weight_set_checksums(abftlp_gemm_weight* w, const int8_t* d_cs, abftlp_stream stream) {
+    if (!w || !d_cs) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const size_t k = static_cast<size_t>(w->w->k);
+        ABFT_CUDA(cudaMemcpyAsync(w->w->cs, d_cs, k, cudaMemcpyDeviceToDevice, as_stream(stream)));
+        ABFT_CUDA(cudaMemcpyAsync(w->w->cs_tile, d_cs, k, cudaMemcpyDeviceToDevice, as_stream(stream)));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_weight_read(const abftlp_gemm_weight* w, int8_t* d_out, abftlp_stream stream) {
+    if (!w || !d_out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::read_encoded(*w->w, d_out, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_checked(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w,
+                                  int32_t* d_c, uint64_t ldc, int32_t* d_csum, uint64_t csum_ld,
+                                  uint8_t* d_row_flags, uint32_t* d_err_count, const abftlp_fault* fault,
+                                  abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::Fault f;
+        if (fault && fault->active) {
+            f.active = true;
+            f.row = static_cast<int64_t>(fault->row);
+            f.col = static_cast<int64_t>(fault->col);
+            f.bit = fault->bit;
+        }
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    true, d_csum, static_cast<int64_t>(csum_ld), d_row_flags, d_err_count, &f, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_unchecked(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w,
+                                    int32_t* d_c, uint64_t ldc, abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    false, nullptr, 0, nullptr, nullptr, nullptr, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_verify(const int32_t* d_c, uint64_t ldc, const int32_t* d_csum, uint64_t csum_ld, uint64_t m,
+                                 uint64_t n, uint8_t* d_row_flags, uint32_t* d_err_count, abftlp_stream stream) {
+    return guarded([&] {
+        abftk::verify(d_c, static_cast<int64_t>(ldc), d_csum, static_cast<int64_t>(csum_ld), static_cast<int64_t>(m),
+                      static_cast<int64_t>(n), d_row_flags, d_err_count, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w,
+                                       int32_t* c, uint64_t ldc, int32_t* csum, uint8_t* row_flags,
+                                       uint32_t* err_count, abftlp_stream stream) {
+    if (!w || (m && !a)) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::GemmWeight& W = *w->w;
+        if (lda < static_cast<uint64_t>(W.k)) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
+        if (c && ldc < static_cast<uint64_t>(W.n)) throw std::invalid_argument("abft_gemm: ldc < n");
+        cudaStream_t st = as_stream(stream);
+        int dev = 0;
+        ABFT_CUDA(cudaGetDevice(&dev));
+        const uint64_t key = (reinterpret_cast<uint64_t>(st) << 8) ^ static_cast<uint64_t>(dev);
+        std::lock_guard<std::mutex> g(g_stage_mu);
+        HostStage& s = g_stage[key];
+        const size_t n = static_cast<size_t>(W.n), k = static_cast<size_t>(W.k);
+        const size_t dldc = (n + 3) / 4 * 4;
+        ensure(s.a, s.a_cap, m * ((k + 15) / 16 * 16));
+        ensure(s.c, s.c_cap, m * dldc);
+        ensure(s.csum, s.csum_cap, m);
+        ensure(s.flags, s.flags_cap, m);
+        if (!s.err) ABFT_CUDA(cudaMalloc(&s.err, sizeof(uint32_t)));
+        const size_t dlda = (k + 15) / 16 * 16;
+        ABFT_CUDA(cudaMemcpy2DAsync(s.a, dlda, a, lda, k, m, cudaMemcpyHostToDevice, st));
+        abftk::gemm(s.a, static_cast<int64_t>(m), static_cast<int64_t>(dlda), W, s.c, static_cast<int64_t>(dldc), true,
+                    s.csum, 1, s.flags, s.err, nullptr, st);
+        if (c) ABFT_CUDA(cudaMemcpy2DAsync(c, ldc * 4, s.c, dldc * 4, n * 4, m, cudaMemcpyDeviceToHost, st));
+        if (csum) ABFT_CUDA(cudaMemcpyAsync(csum, s.csum, m * 4, cudaMemcpyDeviceToHost, st));
+        if (row_flags) ABFT_CUDA(cudaMemcpyAsync(row_flags, s.flags, m, cudaMemcpyDeviceToHost, st));
+        if (err_count) ABFT_CUDA(cudaMemcpyAsync(err_count, s.err, 4, cudaMemcpyDeviceToHost, st));
+        ABFT_CUDA(cudaStreamSynchronize(st));
+        return ABFTLP_OK;
+    });
+}
+
+// ============================================================ device operators: EmbeddingBag
+abftlp_status abftlp_eb_table_create(int32_t elem_type, const void* d_rows, uint64_t rows, uint64_t dim,
+                                     uint64_t row_stride_bytes, int32_t scale_type, const void* d_scales,
+                                     const void* d_biases, const int32_t* d_row_sums, abftlp_stream stream,
+                                     abftlp_eb_table** out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::EbTable* t = abftk::eb_table_create(elem_type, d_rows, static_cast<int64_t>(rows),
+                                                   static_cast<int64_t>(dim), static_cast<int64_t>(row_stride_bytes),
+                                                   scale_type, d_scales, d_biases, d_row_sums, as_stream(stream));
+        *out = new abftlp_eb_table_s{t};
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_eb_table_free(abftlp_eb_table* t) {
+    if (!t) return;
+    abftk::eb_table_free(t->t);
+    delete t;
+}
+
+abftlp_status abftlp_eb_table_validate(const abftlp_eb_table* t, const int32_t* d_row_sums, abftlp_stream stream,
+                                       uint64_t* mismatched_rows) {
+    if (!t || !d_row_sums || !mismatched_rows) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        *mismatched_rows = abftk::eb_table_validate(*t->t, d_row_sums, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_table_row_sums(const abftlp_eb_table* t, int32_t* d_out, abftlp_stream stream) {
+    if (!t || !d_out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_row_sums(*t->t, d_out, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_checked(const abftlp_eb_table* t, const int64_t* d_offsets, const int64_t* d_indices,
+                                uint64_t num_bags, const float* d_weights, float* d_out, uint64_t ld_out,
+                                uint8_t* d_flags, double* d_rsum, double* d_csum, uint32_t* d_flag_count,
+                                int32_t* d_status, abftlp_stream stream) {
+    if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        if (num_bags && !d_flags) throw std::invalid_argument("null argument");
+        abftk::eb_run(*t->t, d_offsets, d_indices, static_cast<int64_t>(num_bags), d_weights, d_out,
+                      static_cast<int64_t>(ld_out), true, d_flags, d_rsum, d_csum, d_flag_count, d_status,
+                      as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_unchecked(const abftlp_eb_table* t, const int64_t* d_offsets, const int64_t* d_indices,
+                                  uint64_t num_bags, const float* d_weights, float* d_out, uint64_t ld_out,
+                                  int32_t* d_status, abftlp_stream stream) {
+    if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_run(*t->t, d_offsets, d_indices, static_cast<int64_t>(num_bags), d_weights, d_out,
+                      static_cast<int64_t>(ld_out), false, nullptr, nullptr, nullptr, nullptr, d_status,
+                      as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+// ============================================================ fault injection
+abftlp_status abftlp_flip_bit(void* d_ptr, uint32_t elem_bytes, uint64_t index, uint32_t bit, abftlp_stream stream) {
+    if (!d_ptr) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        if (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4 && elem_bytes != 8)
+            throw std::invalid_argument("flip_bit: element width must be 1, 2, 4 or 8 bytes");
+        if (bit >= elem_bytes * 8) throw std::out_of_range("flip_bit: bit index out of range");
+        abftk::flip_bit(d_ptr, index * elem_bytes, bit, as_stream(stream));  // little-endian element
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uint64_t j, uint32_t bit,
+                                          abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::GemmWeight& W = *w->w;
+        if (i >= static_cast<uint64_t>(W.k) || j > static_cast<uint64_t>(W.n))
+            throw std::out_of_range("inject_weight_B: coordinates out of range");
+        if (bit >= 8) throw std::out_of_range("flip_bit: bit index out of range");
+        if (j < static_cast<uint64_t>(W.n)) {
+            abftk::flip_bit(W.bt, j * static_cast<uint64_t>(W.k_pad) + i, bit, as_stream(stream));
+        } else {  // checksum column: both the stored vector and the MMA operand
+            abftk::flip_bit(W.cs, i, bit, as_stream(stream));
+            abftk::flip_bit(W.cs_tile, i, bit, as_stream(stream));
+        }
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_table_flip_bit(abftlp_eb_table* t, uint64_t row, uint64_t col, uint32_t bit,
+                                       abftlp_stream stream) {
+    if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::EbTable& T = *t->t;
+        if (row >= static_cast<uint64_t>(T.rows) || col >= static_cast<uint64_t>(T.dim))
+            throw std::out_of_range("inject_eb_table: coordinates out of range");
+        const uint32_t width = T.elem == abftk::kEbU4 ? 4u : 8u;
+        if (bit >= width) throw std::out_of_range("flip_bit: bit index out of range");
+        uint64_t byte = row * static_cast<uint64_t>(T.row_stride);
+        uint32_t b = bit;
+        if (T.elem == abftk::kEbU4) {
+            byte += col / 2;
+            b += 4u * static_cast<uint32_t>(col & 1);
+        } else {
+            byte += col;
+        }
+        abftk::flip_bit(const_cast<uint8_t*>(T.data), byte, b, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_generate(void* d_out, uint64_t count, uint64_t seed, uint64_t rng_stream, uint64_t off,
+                              int32_t kind, double lo, double hi, uint64_t bound, abftlp_stream stream) {
+    if (!d_out && count) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        if (kind < 0 || kind > 3) throw std::invalid_argument("generate: unknown kind");
+        if (kind == 3 && bound == 0) throw std::invalid_argument("generate: bound must be > 0");
+        abftk::gen(d_out, static_cast<int64_t>(count), seed, rng_stream, off, kind, lo, hi, bound, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream) {
+    if (!d_buf) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::l2_flush(d_buf, static_cast<int64_t>(bytes), salt, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+}  // extern "C"

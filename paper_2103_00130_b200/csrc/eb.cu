@@ -1,0 +1,432 @@
+// ABFT EmbeddingBag for sm_100a: warp-per-bag checked / unchecked pooled lookups and the
+// row-sum encoder.
+//
+//   eb_meta_kernel  replaces precompute_row_sums (P:src/embedding_abft.cpp:39-45) and packs the
+//                   per-row (scale, bias, rowSum) into one 16-B (fp32) or 8-B (fp16) record so a
+//                   lookup touches one metadata sector.
+//   eb_bag_kernel   replaces embedding_bag / abft_embedding_bag / batch_abft_eb
+//                   (P:src/embedding_abft.cpp:47-91). Lane l owns a fixed column slice, so every
+//                   output column is accumulated sequentially in bag order with the reference's
+//                   exact fp32 operation order (scale*q, +bias, *w, +=; no FMA contraction).
+//                   The row loads of up to 32 lookups are issued before any is consumed, so each
+//                   warp keeps 32 row-gathers in flight. cSum is the reference's sequential fp64
+//                   chain; rSum is computed by a warp tree when every partial sum is provably
+//                   exact in fp64 (then the order cannot matter) and by the reference's sequential
+//                   order otherwise -- bit-identical either way.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "abft_internal.h"
+#include "ptx.cuh"
+
+namespace abftk {
+
+namespace {
+
+template <int BPL>
+struct LaneWord {
+    using T = uint32_t;
+};
+template <>
+struct LaneWord<8> {
+    using T = uint64_t;
+};
+
+template <int BPL>
+__device__ __forceinline__ typename LaneWord<BPL>::T load_row_word(const uint8_t* ptr) {
+    if constexpr (BPL == 1) {
+        uint16_t v;
+        asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(v) : "l"(ptr));
+        return v;
+    } else if constexpr (BPL == 2) {
+        uint16_t v;
+        asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(ptr));
+        return v;
+    } else if constexpr (BPL == 4) {
+        uint32_t v;
+        asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(ptr));
+        return v;
+    } else {
+        uint64_t v;
+        asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(ptr));
+        return v;
+    }
+}
+
+// Decode element c (0-based within the lane's slice) of a lane word.
+template <int ELEM, typename W>
+__device__ __forceinline__ float decode(W w, int c) {
+    if constexpr (ELEM == kEbS8) {
+        return static_cast<float>(static_cast<int8_t>(static_cast<uint8_t>(w >> (8 * c))));
+    } else if constexpr (ELEM == kEbU8) {
+        return static_cast<float>(static_cast<uint8_t>(w >> (8 * c)));
+    } else {  // u4: element j = (byte[j/2] >> 4*(j&1)) & 0xF, low nibble = even column
+        return static_cast<float>(static_cast<uint32_t>(w >> (4 * c)) & 0xFu);
+    }
+}
+
+template <int SCALE>
+__device__ __forceinline__ void load_meta(const void* meta, int64_t i, float& s, float& b, int32_t& rs) {
+    if constexpr (SCALE == kEbF32) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(meta) + i);
+        s = __uint_as_float(v.x);
+        b = __uint_as_float(v.y);
+        rs = static_cast<int32_t>(v.z);
+    } else {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(meta) + i);
+        s = __half2float(__ushort_as_half(static_cast<unsigned short>(v.x & 0xFFFFu)));
+        b = __half2float(__ushort_as_half(static_cast<unsigned short>(v.x >> 16)));
+        rs = static_cast<int32_t>(v.y);
+    }
+}
+
+// Exponent range of a float's set bits: msb/lsb exponents (value = sum of 2^e over set bits).
+__device__ __forceinline__ void bit_span(float v, int& emax, int& umin) {
+    const uint32_t bits = __float_as_uint(v) & 0x7FFFFFFFu;
+    if (!bits) return;
+    const int ex = static_cast<int>(bits >> 23);
+    const uint32_t mant = bits & 0x7FFFFFu;
+    int lo, hi;
+    if (ex == 0) {
+        lo = -149 + (__ffs(static_cast<int>(mant)) - 1);
+        hi = -149 + (31 - __clz(static_cast<int>(mant)));
+    } else {
+        const uint32_t sig = mant | 0x800000u;
+        lo = ex - 150 + (__ffs(static_cast<int>(sig)) - 1);
+        hi = ex - 127;
+    }
+    emax = max(emax, hi);
+    umin = min(umin, lo);
+}
+
+}  // namespace
+
+// CPL > 0: lane owns columns [lane*CPL, lane*CPL+CPL) (d == 32*CPL).
+// CPL == 0: generic layout, lane owns columns lane + 32*c (c < kGenericSlots), byte loads.
+constexpr int kGenericSlots = 8;
+
+template <int ELEM, int SCALE, int CPL, bool WEIGHTED, bool CHECKED>
+__global__ void __launch_bounds__(256) eb_bag_kernel(const EbParams p, int log2d) {
+    constexpr bool kGeneric = CPL == 0;
+    constexpr int NC = kGeneric ? kGenericSlots : CPL;
+    constexpr int BPL = kGeneric ? 1 : (ELEM == kEbU4 ? CPL / 2 : CPL);
+    constexpr int R = kGeneric ? 8 : 32;  // lookups gathered per round
+    using Word = typename LaneWord<BPL>::T;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t bag = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    __shared__ uint32_t blk_flags;
+    __shared__ uint32_t is_last;
+    if (threadIdx.x == 0) blk_flags = 0;
+    __syncthreads();
+
+    if (bag < p.num_bags) {
+        const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
+        float acc[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = 0.0f;
+        double csum = 0.0;
+        bool oob = false;
+        const double dd = static_cast<double>(p.dim);
+        for (int64_t base = beg; base < end; base += R) {
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(R), end - base));
+            int64_t my_idx = -1;
+            float my_s = 0.f, my_b = 0.f, my_w = 1.f;
+            int32_t my_rs = 0;
+            if (lane < cnt) {
+                const int64_t ix = p.indices[base + lane];
+                if (static_cast<uint64_t>(ix) >= static_cast<uint64_t>(p.rows)) {
+                    oob = true;
+                } else {
+                    my_idx = ix;
+                    load_meta<SCALE>(p.meta, ix, my_s, my_b, my_rs);
+                }
+                if constexpr (WEIGHTED) my_w = p.weights[base + lane];
+            }
+            if constexpr (!kGeneric) {
+                Word data[R];
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
+                    data[t] = (t < cnt && it >= 0) ? load_row_word<BPL>(p.data + it * p.row_stride + lane * BPL) : Word(0);
+                }
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    if (t < cnt) {
+                        const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
+                        const float s = __shfl_sync(0xffffffffu, my_s, t);
+                        const float b = __shfl_sync(0xffffffffu, my_b, t);
+                        const float w = WEIGHTED ? __shfl_sync(0xffffffffu, my_w, t) : 1.0f;
+                        const int32_t rs = __shfl_sync(0xffffffffu, my_rs, t);
+                        if (it >= 0) {
+#pragma unroll
+                            for (int c = 0; c < NC; ++c) {
+                                float x = __fadd_rn(__fmul_rn(s, decode<ELEM>(data[t], c)), b);
+                                if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                                acc[c] = __fadd_rn(acc[c], x);
+                            }
+                            if constexpr (CHECKED) {
+                                double term = __dadd_rn(__dmul_rn(static_cast<double>(s), static_cast<double>(rs)),
+                                                        __dmul_rn(dd, static_cast<double>(b)));
+                                if constexpr (WEIGHTED) term = __dmul_rn(static_cast<double>(w), term);
+                                csum = __dadd_rn(csum, term);
+                            }
+                        }
+                    }
+                }
+            } else {
+                uint32_t data[R][NC];
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        const int64_t j = lane + 32 * c;
+                        uint32_t v = 0;
+                        if (t < cnt && it >= 0 && j < p.dim) {
+                            const int64_t byte = ELEM == kEbU4 ? (j >> 1) : j;
+                            v = p.data[it * p.row_stride + byte];
+                            if (ELEM == kEbU4) v = (v >> (4 * (j & 1))) & 0xFu;
+                        }
+                        data[t][c] = v;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < R; ++t) {
+                    if (t < cnt) {
+                        const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
+                        const float s = __shfl_sync(0xffffffffu, my_s, t);
+                        const float b = __shfl_sync(0xffffffffu, my_b, t);
+                        const float w = WEIGHTED ? __shfl_sync(0xffffffffu, my_w, t) : 1.0f;
+                        const int32_t rs = __shfl_sync(0xffffffffu, my_rs, t);
+                        if (it >= 0) {
+#pragma unroll
+                            for (int c = 0; c < NC; ++c) {
+                                const float q = ELEM == kEbS8 ? static_cast<float>(static_cast<int8_t>(data[t][c]))
+                                                              : static_cast<float>(data[t][c]);
+                                float x = __fadd_rn(__fmul_rn(s, q), b);
+                                if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                                if (lane + 32 * c < p.dim) acc[c] = __fadd_rn(acc[c], x);
+                            }
+                            if constexpr (CHECKED) {
+                                double term = __dadd_rn(__dmul_rn(static_cast<double>(s), static_cast<double>(rs)),
+                                                        __dmul_rn(dd, static_cast<double>(b)));
+                                if constexpr (WEIGHTED) term = __dmul_rn(static_cast<double>(w), term);
+                                csum = __dadd_rn(csum, term);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
+
+        // ---- pooled output
+        float* dst = p.out + bag * p.ld_out;
+        if constexpr (!kGeneric) {
+            if constexpr (NC % 4 == 0) {
+                float* d0 = dst + lane * NC;
+                if ((reinterpret_cast<uintptr_t>(d0) & 15) == 0) {
+#pragma unroll
+                    for (int c = 0; c < NC; c += 4)
+                        *reinterpret_cast<float4*>(d0 + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) d0[c] = acc[c];
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) dst[lane * NC + c] = acc[c];
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (lane + 32 * c < p.dim) dst[lane + 32 * c] = acc[c];
+        }
+
+        if constexpr (CHECKED) {
+            // ---- rSum = sum_j double(r[j]) in the reference's order (P:src/embedding_abft.cpp:66-67)
+            int emax = -100000, umin = 100000;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) bit_span(acc[c], emax, umin);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+                umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+            }
+            double rsum = 0.0;
+            if (emax == -100000) {
+                rsum = 0.0;
+            } else if (emax + 1 + log2d - umin <= 53) {
+                // every partial sum is an exactly representable multiple of 2^umin: order-free
+                double s = 0.0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) s = __dadd_rn(s, static_cast<double>(acc[c]));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+                rsum = s;
+            } else if constexpr (!kGeneric) {
+                for (int l = 0; l < 32; ++l)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, acc[c], l)));
+            } else {
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    for (int l = 0; l < 32; ++l) {
+                        const float v = __shfl_sync(0xffffffffu, acc[c], l);
+                        if (l + 32 * c < p.dim) rsum = __dadd_rn(rsum, static_cast<double>(v));
+                    }
+            }
+            // ---- err = |rSum - cSum| > 1e-5 * max(|rSum|, |cSum|, 1)   (P:src/embedding_abft.cpp:80-81)
+            const double diff = fabs(__dsub_rn(rsum, csum));
+            const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
+            const int flag = diff > __dmul_rn(1e-5, mx);
+            if (lane == 0) {
+                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (p.rsum) p.rsum[bag] = rsum;
+                if (p.csum) p.csum[bag] = csum;
+                if (flag) atomicAdd(&blk_flags, 1u);
+            }
+        }
+    }
+    if constexpr (CHECKED) {
+        if (p.flag_count) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
+                __threadfence();
+                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
+            }
+            __syncthreads();
+            if (is_last && threadIdx.x == 0) {
+                __threadfence();
+                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
+                atomicExch(p.ws_block_cnt, 0u);
+            }
+        }
+    }
+}
+
+// Row sums + metadata packing. One warp per row. If `given_sums` is non-null the stored sums are
+// taken from it (stale sums survive, as load_table(validate=false)); `mismatch` counts rows whose
+// given sum differs from the recomputed one (load_table validation, P:src/embedding_abft.cpp:139-143).
+template <int ELEM, int SCALE>
+__global__ void __launch_bounds__(256) eb_meta_kernel(const uint8_t* __restrict__ data, int64_t rows, int64_t dim,
+                                                      int64_t row_stride, const void* __restrict__ scales,
+                                                      const void* __restrict__ biases,
+                                                      const int32_t* __restrict__ given_sums, void* __restrict__ meta,
+                                                      int32_t* __restrict__ sums_out, uint32_t* mismatch) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x) >> 5; r < rows;
+         r += (static_cast<int64_t>(gridDim.x) * 256) >> 5) {
+        const uint8_t* row = data + r * row_stride;
+        int32_t s = 0;
+        for (int64_t j = lane; j < dim; j += 32) {
+            if (ELEM == kEbS8)
+                s += static_cast<int8_t>(row[j]);
+            else if (ELEM == kEbU8)
+                s += row[j];
+            else
+                s += (row[j >> 1] >> (4 * (j & 1))) & 0xF;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            int32_t stored = s;
+            if (given_sums) {
+                stored = given_sums[r];
+                if (mismatch && stored != s) atomicAdd(mismatch, 1u);
+            }
+            if (sums_out) sums_out[r] = s;
+            if (meta) {
+                if constexpr (SCALE == kEbF32) {
+                    EbMetaF32 mrec;
+                    mrec.scale = reinterpret_cast<const float*>(scales)[r];
+                    mrec.bias = reinterpret_cast<const float*>(biases)[r];
+                    mrec.row_sum = stored;
+                    mrec.pad = 0;
+                    reinterpret_cast<EbMetaF32*>(meta)[r] = mrec;
+                } else {
+                    EbMetaF16 mrec;
+                    mrec.scale = reinterpret_cast<const uint16_t*>(scales)[r];
+                    mrec.bias = reinterpret_cast<const uint16_t*>(biases)[r];
+                    mrec.row_sum = stored;
+                    reinterpret_cast<EbMetaF16*>(meta)[r] = mrec;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host launchers
+template <int ELEM, int SCALE, int CPL>
+static cudaError_t launch_bag_cpl(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((p.num_bags + 7) / 8);
+    const bool w = p.weights != nullptr;
+    if (checked) {
+        if (w)
+            eb_bag_kernel<ELEM, SCALE, CPL, true, true><<<blocks, 256, 0, st>>>(p, log2d);
+        else
+            eb_bag_kernel<ELEM, SCALE, CPL, false, true><<<blocks, 256, 0, st>>>(p, log2d);
+    } else {
+        if (w)
+            eb_bag_kernel<ELEM, SCALE, CPL, true, false><<<blocks, 256, 0, st>>>(p, log2d);
+        else
+            eb_bag_kernel<ELEM, SCALE, CPL, false, false><<<blocks, 256, 0, st>>>(p, log2d);
+    }
+    return cudaGetLastError();
+}
+
+template <int ELEM, int SCALE>
+static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
+    const int64_t d = p.dim;
+    const bool aligned_rows = (p.row_stride % 8) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 8) == 0;
+    if (aligned_rows && d % 32 == 0) {
+        const int64_t cpl = d / 32;
+        if (ELEM != kEbU4 && cpl == 1) return launch_bag_cpl<ELEM, SCALE, 1>(p, checked, log2d, st);
+        if (cpl == 2) return launch_bag_cpl<ELEM, SCALE, 2>(p, checked, log2d, st);
+        if (cpl == 4) return launch_bag_cpl<ELEM, SCALE, 4>(p, checked, log2d, st);
+        if (cpl == 8) return launch_bag_cpl<ELEM, SCALE, 8>(p, checked, log2d, st);
+    }
+    if (d > 32 * kGenericSlots) return cudaErrorInvalidValue;
+    return launch_bag_cpl<ELEM, SCALE, 0>(p, checked, log2d, st);
+}
+
+cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st) {
+    if (p.num_bags <= 0) return cudaSuccess;
+    int log2d = 0;
+    while ((int64_t{1} << log2d) < p.dim) ++log2d;
+    if (scale == kEbF32) {
+        if (elem == kEbS8) return launch_bag_elem<kEbS8, kEbF32>(p, checked, log2d, st);
+        if (elem == kEbU8) return launch_bag_elem<kEbU8, kEbF32>(p, checked, log2d, st);
+        return launch_bag_elem<kEbU4, kEbF32>(p, checked, log2d, st);
+    }
+    if (elem == kEbS8) return launch_bag_elem<kEbS8, kEbF16>(p, checked, log2d, st);
+    if (elem == kEbU8) return launch_bag_elem<kEbU8, kEbF16>(p, checked, log2d, st);
+    return launch_bag_elem<kEbU4, kEbF16>(p, checked, log2d, st);
+}
+
+cudaError_t launch_eb_meta(int elem, int scale, const uint8_t* data, int64_t rows, int64_t dim, int64_t row_stride,
+                           const void* scales, const void* biases, const int32_t* given_sums, void* meta,
+                           int32_t* sums_out, uint32_t* mismatch, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    int64_t blocks = (rows + 7) / 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    const unsigned g = static_cast<unsigned>(blocks);
+#define ABFT_META(E, S) \
+    eb_meta_kernel<E, S><<<g, 256, 0, st>>>(data, rows, dim, row_stride, scales, biases, given_sums, meta, sums_out, mismatch)
+    if (scale == kEbF32) {
+        if (elem == kEbS8) ABFT_META(kEbS8, kEbF32);
+        else if (elem == kEbU8) ABFT_META(kEbU8, kEbF32);
+        else ABFT_META(kEbU4, kEbF32);
+    } else {
+        if (elem == kEbS8) ABFT_META(kEbS8, kEbF16);
+        else if (elem == kEbU8) ABFT_META(kEbU8, kEbF16);
+        else ABFT_META(kEbU4, kEbF16);
+    }
+#undef ABFT_META
+    return cudaGetLastError();
+}
+
+}  // namespace abftk

@@ -1,0 +1,470 @@
+// Host runtime: device buffers, TMA tensor maps, per-stream workspace, launch decisions.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+
+#include "runtime.h"
+
+namespace abftk {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear sticky-free errors
+        throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+
+static int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int device_sm_count() {
+    static int sms = [] {
+        int dev = 0, n = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+        return n;
+    }();
+    return sms;
+}
+
+// ------------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2D row-major tensor: `inner` elements per row (contiguous), `outer` rows, `row_bytes` pitch.
+static CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {row_bytes};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
+    return map;
+}
+
+// ------------------------------------------------------------------ per-stream workspace
+// Scratch that must not live in the shared immutable weight/table handles: kernels
+// leave every counter at zero on exit, so one workspace serves any number of ordered calls.
+struct Workspace {
+    int device = 0;
+    uint32_t* row_res = nullptr;
+    int32_t* csum_acc = nullptr;
+    int64_t rows_cap = 0;
+    uint32_t* mtile_cnt = nullptr;
+    int64_t mtiles_cap = 0;
+    uint32_t* tile_flag = nullptr;
+    int64_t tiles_cap = 0;
+    uint32_t* small = nullptr;  // [0] err_acc [1] done_cnt [2] verify acc [3] verify blocks [4] eb acc [5] eb blocks
+    uint32_t epoch = 0;
+    uint8_t* scratch = nullptr;  // A repack buffer
+    size_t scratch_cap = 0;
+    std::mutex mu;
+};
+
+static std::mutex g_ws_mu;
+static std::unordered_map<uint64_t, Workspace*> g_ws;
+
+static Workspace& ws_for(cudaStream_t st) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const uint64_t key = (reinterpret_cast<uint64_t>(st) << 8) ^ static_cast<uint64_t>(dev);
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) return *it->second;
+    auto* w = new Workspace();
+    w->device = dev;
+    cuda_check(cudaMalloc(&w->small, 64 * sizeof(uint32_t)), "cudaMalloc(workspace)");
+    cuda_check(cudaMemset(w->small, 0, 64 * sizeof(uint32_t)), "cudaMemset(workspace)");
+    g_ws[key] = w;
+    return *w;
+}
+
+template <typename T>
+static void grow(T*& ptr, int64_t& cap, int64_t need, cudaStream_t st) {
+    if (need <= cap) return;
+    const int64_t ncap = std::max<int64_t>(need, std::max<int64_t>(cap * 2, 256));
+    if (ptr) {
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        cuda_check(cudaFree(ptr), "cudaFree");
+    }
+    cuda_check(cudaMalloc(&ptr, ncap * sizeof(T)), "cudaMalloc(workspace)");
+    cuda_check(cudaMemset(ptr, 0, ncap * sizeof(T)), "cudaMemset(workspace)");
+    cap = ncap;
+}
+
+// ------------------------------------------------------------------ GEMM
+static CUtensorMap weight_map(const GemmWeight& w, int bn) {
+    return w.map_b[bn == 64 ? 0 : bn == 128 ? 1 : 2];
+}
+
+void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
+    if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
+    if (!d_b) throw std::invalid_argument("null argument");
+    if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
+    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, 256);
+    const size_t need_bt = static_cast<size_t>(n_pad * k_pad);
+    if (!w.bt || need_bt > w.bt_cap || static_cast<size_t>(k_pad) > w.kpad_cap) {
+        if (w.bt) {
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            cudaFree(w.bt);
+            cudaFree(w.cs_tile);
+            cudaFree(w.cs);
+            w.bt = nullptr;
+            w.cs_tile = nullptr;
+            w.cs = nullptr;
+        }
+        cuda_check(cudaMalloc(&w.bt, static_cast<size_t>(n_pad * k_pad)), "cudaMalloc(B')");
+        cuda_check(cudaMalloc(&w.cs_tile, static_cast<size_t>(kCsRows * k_pad)), "cudaMalloc(cs tile)");
+        cuda_check(cudaMalloc(&w.cs, static_cast<size_t>(k_pad)), "cudaMalloc(cs)");
+        w.bt_cap = need_bt;
+        w.kpad_cap = static_cast<size_t>(k_pad);
+    }
+    w.k = k;
+    w.n = n;
+    w.k_pad = k_pad;
+    w.n_pad = n_pad;
+    cuda_check(cudaMemsetAsync(w.cs_tile, 0, static_cast<size_t>(kCsRows * k_pad), st), "cudaMemsetAsync");
+    cuda_check(launch_encode_weight(d_b, k, n, ldb, w, st), "encode_weight_kernel");
+    const int bns[3] = {64, 128, 256};
+    for (int i = 0; i < 3; ++i)
+        w.map_b[i] = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, w.bt, k_pad, n_pad, k_pad, kBK, bns[i],
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+    w.map_cs = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, w.cs_tile, k_pad, kCsRows, k_pad, kBK, kCsRows,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
+    if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
+    auto* w = new GemmWeight();
+    try {
+        encode_weight_into(*w, d_b, k, n, ldb, st);
+    } catch (...) {
+        free_weight(w);
+        throw;
+    }
+    return w;
+}
+
+void read_encoded(const GemmWeight& w, int8_t* d_out, cudaStream_t st) {
+    cuda_check(launch_read_encoded(w, d_out, st), "read_encoded_kernel");
+}
+
+void free_weight(GemmWeight* w) {
+    if (!w) return;
+    if (w->owns) {
+        cudaFree(w->bt);
+        cudaFree(w->cs_tile);
+        cudaFree(w->cs);
+    }
+    delete w;
+}
+
+// Pick the N tile and the split-K factor. Small-m GEMMs re-read A once per N tile and every CTA
+// must ingest its A and B' slabs through L2 -> SMEM, so the model minimises the bytes the busiest
+// SM moves (A slab + B' slab + partial C tile) times the number of waves, plus the L2 total.
+GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault) {
+    (void)checked;
+    const int sms = device_sm_count();
+    const int64_t m_tiles = (m + kBM - 1) / kBM;
+    const int64_t kb = k_pad / kBK;
+    if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn,splits" tuning override
+        int bn = 0, sp = 0;
+        if (std::sscanf(env, "%d,%d", &bn, &sp) == 2 && (bn == 64 || bn == 128 || bn == 256) && sp >= 1) {
+            if (!c_tma_ok || fault) sp = 1;
+            sp = static_cast<int>(std::min<int64_t>(sp, kb));
+            return {bn, sp, !c_tma_ok ? kEpiDirect : (sp > 1 ? kEpiTmaReduce : kEpiTmaStore)};
+        }
+    }
+    GemmTiling best{64, 1, c_tma_ok ? kEpiTmaStore : kEpiDirect};
+    double best_cost = 1e300;
+    for (int bn : {256, 128, 64}) {
+        const int64_t n_tiles = (n + bn - 1) / bn;
+        const int64_t tiles = m_tiles * n_tiles;
+        int64_t splits = 1;
+        if (c_tma_ok && !fault && (n % 4) == 0) {
+            splits = std::max<int64_t>(1, std::min<int64_t>(kb / 4, sms / std::max<int64_t>(tiles, 1)));
+        }
+        const int64_t kbps = (kb + splits - 1) / splits;
+        splits = (kb + kbps - 1) / kbps;
+        const int64_t ctas = tiles * splits;
+        const int64_t waves = (ctas + sms - 1) / sms;
+        const double per_cta = double(kBM) * kbps * kBK + double(bn) * kbps * kBK + double(kBM) * bn * 4.0;
+        const double l2_total = double(ctas) * per_cta;
+        const double cost = waves * per_cta / 100.0 + l2_total / 10000.0 + (bn < 256 ? 1.0 : 0.0);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best.bn = bn;
+            best.splits = static_cast<int>(splits);
+            best.epi = !c_tma_ok ? kEpiDirect : (splits > 1 ? kEpiTmaReduce : kEpiTmaStore);
+        }
+    }
+    return best;
+}
+
+void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
+          int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
+          cudaStream_t st, const GemmTiling* force) {
+    if (m < 0) throw std::invalid_argument("abft_gemm: negative m");
+    if (m > 0 && (!d_a || !d_c)) throw std::invalid_argument("null argument");
+    if (lda < w.k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
+    if (ldc < w.n) throw std::invalid_argument("abft_gemm: ldc < n");
+    if (checked && (!d_csum || !d_flags || !d_err_count)) throw std::invalid_argument("null argument");
+    if (m > (int64_t{1} << 31) - 1 || w.n > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too large");
+    const bool has_fault = fault && fault->active;
+    if (has_fault) {
+        if (!checked) throw std::invalid_argument("abft_gemm: fault hook needs the checked kernel");
+        if (fault->row < 0 || fault->row >= m || fault->col < 0 || fault->col > w.n || fault->bit > 31)
+            throw std::out_of_range("abft_gemm: fault coordinates out of range");
+    }
+    if (m == 0) {
+        if (checked) cuda_check(cudaMemsetAsync(d_err_count, 0, sizeof(uint32_t), st), "cudaMemsetAsync");
+        return;
+    }
+    Workspace& ws = ws_for(st);
+    std::lock_guard<std::mutex> g(ws.mu);
+
+    // A must be a TMA-legal 2D tensor: 16-byte aligned base and pitch. Otherwise repack once.
+    const uint8_t* a = d_a;
+    int64_t a_ld = lda;
+    if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0) {
+        a_ld = round_up(w.k, 16);
+        const size_t need = static_cast<size_t>(a_ld * m);
+        if (need > ws.scratch_cap) {
+            if (ws.scratch) {
+                cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+                cuda_check(cudaFree(ws.scratch), "cudaFree");
+            }
+            cuda_check(cudaMalloc(&ws.scratch, need), "cudaMalloc(A scratch)");
+            ws.scratch_cap = need;
+        }
+        cuda_check(cudaMemcpy2DAsync(ws.scratch, a_ld, d_a, lda, w.k, m, cudaMemcpyDeviceToDevice, st),
+                   "cudaMemcpy2DAsync(A repack)");
+        a = ws.scratch;
+    }
+    const bool c_tma_ok = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0;
+    GemmTiling t = force ? *force : choose_tiling(m, w.n, w.k_pad, checked, c_tma_ok, has_fault);
+    if (!c_tma_ok) t.epi = kEpiDirect;
+    if (t.epi == kEpiDirect || has_fault || (w.n % 4) != 0) t.splits = 1;
+    if (t.splits == 1 && t.epi == kEpiTmaReduce) t.epi = kEpiTmaStore;
+    if (t.splits > 1) t.epi = kEpiTmaReduce;
+
+    const int64_t m_tiles = (m + kBM - 1) / kBM;
+    const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
+    const int64_t kb = w.k_pad / kBK;
+    const int64_t kbps = (kb + t.splits - 1) / t.splits;
+    const int64_t splits = (kb + kbps - 1) / kbps;
+
+    if (checked && m > ws.rows_cap) {
+        int64_t cap_a = ws.rows_cap, cap_b = ws.rows_cap;  // row_res and csum_acc share one capacity
+        grow(ws.row_res, cap_a, m, st);
+        grow(ws.csum_acc, cap_b, m, st);
+        ws.rows_cap = std::min(cap_a, cap_b);
+    }
+    grow(ws.mtile_cnt, ws.mtiles_cap, m_tiles, st);
+    if (t.splits > 1) grow(ws.tile_flag, ws.tiles_cap, m_tiles * n_tiles, st);
+
+    GemmParams p{};
+    p.m = static_cast<int>(m);
+    p.n = static_cast<int>(w.n);
+    p.k_blocks = static_cast<int>(kb);
+    p.kb_per_split = static_cast<int>(kbps);
+    p.n_tiles = static_cast<int>(n_tiles);
+    p.m_tiles = static_cast<int>(m_tiles);
+    p.splits = static_cast<int>(splits);
+    p.c = d_c;
+    p.ldc = ldc;
+    p.csum = d_csum;
+    p.csum_ld = csum_ld;
+    p.flags = d_flags;
+    p.err_count = d_err_count;
+    p.row_res = ws.row_res;
+    p.csum_acc = ws.csum_acc;
+    p.mtile_cnt = ws.mtile_cnt;
+    p.err_acc = ws.small + 0;
+    p.done_cnt = ws.small + 1;
+    p.tile_flag = ws.tile_flag;
+    p.epoch = ++ws.epoch;
+    if (has_fault) {
+        p.fault_active = 1;
+        p.fault_row = static_cast<int>(fault->row);
+        p.fault_col = static_cast<int>(fault->col);
+        p.fault_bit = static_cast<int>(fault->bit);
+    }
+    const CUtensorMap map_a =
+        make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, a, w.k, m, a_ld, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+    CUtensorMap map_c;
+    std::memset(&map_c, 0, sizeof(map_c));
+    if (t.epi != kEpiDirect)
+        map_c = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_INT32, d_c, w.n, m, ldc * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    const dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(m_tiles), static_cast<unsigned>(splits));
+    cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, grid, map_a, weight_map(w, t.bn), w.map_cs, map_c, p, st),
+               "gemm_u8s8_kernel");
+}
+
+void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum_ld, int64_t m, int64_t n,
+            uint8_t* d_flags, uint32_t* d_err_count, cudaStream_t st) {
+    if (m < 0 || n < 0) throw std::invalid_argument("verify_checksums: negative size");
+    if (m > 0 && (!d_c || !d_csum)) throw std::invalid_argument("null argument");
+    Workspace& ws = ws_for(st);
+    std::lock_guard<std::mutex> g(ws.mu);
+    cuda_check(launch_verify(d_c, ldc, d_csum, csum_ld, m, n, d_flags, d_err_count, ws.small + 2, ws.small + 3, st),
+               "verify_kernel");
+}
+
+// ------------------------------------------------------------------ EmbeddingBag
+int64_t eb_elem_row_bytes(int elem, int64_t dim) { return elem == kEbU4 ? (dim + 1) / 2 : dim; }
+
+EbTable* eb_table_create(int elem, const void* d_rows, int64_t rows, int64_t dim, int64_t row_stride, int scale_type,
+                         const void* d_scales, const void* d_biases, const int32_t* d_given_sums, cudaStream_t st) {
+    if (elem < kEbS8 || elem > kEbU4) throw std::invalid_argument("eb_table_create: unknown element type");
+    if (scale_type != kEbF32 && scale_type != kEbF16) throw std::invalid_argument("eb_table_create: unknown scale type");
+    if (rows <= 0 || dim <= 0) throw std::invalid_argument("eb_table_create: empty table");
+    if (!d_rows || !d_scales || !d_biases) throw std::invalid_argument("null argument");
+    if (row_stride < eb_elem_row_bytes(elem, dim)) throw std::invalid_argument("eb_table_create: row stride too small");
+    auto* t = new EbTable();
+    t->elem = elem;
+    t->scale_type = scale_type;
+    t->rows = rows;
+    t->dim = dim;
+    t->row_stride = row_stride;
+    t->data = reinterpret_cast<const uint8_t*>(d_rows);
+    const size_t rec = scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16);
+    try {
+        cuda_check(cudaMalloc(&t->meta, rec * static_cast<size_t>(rows)), "cudaMalloc(eb meta)");
+        cuda_check(launch_eb_meta(elem, scale_type, t->data, rows, dim, row_stride, d_scales, d_biases, d_given_sums,
+                                  t->meta, nullptr, nullptr, st),
+                   "eb_meta_kernel");
+    } catch (...) {
+        eb_table_free(t);
+        throw;
+    }
+    return t;
+}
+
+void eb_table_rebuild(EbTable& t, int elem, const void* d_rows, int64_t rows, int64_t dim, int64_t row_stride,
+                      int scale_type, const void* d_scales, const void* d_biases, const int32_t* d_given_sums,
+                      cudaStream_t st) {
+    const size_t rec = scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16);
+    const size_t old = (t.scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16)) * static_cast<size_t>(t.rows);
+    if (!t.meta || rec * static_cast<size_t>(rows) > old) {
+        if (t.meta) {
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            cudaFree(t.meta);
+            t.meta = nullptr;
+        }
+        cuda_check(cudaMalloc(&t.meta, rec * static_cast<size_t>(rows)), "cudaMalloc(eb meta)");
+    }
+    t.elem = elem;
+    t.scale_type = scale_type;
+    t.rows = rows;
+    t.dim = dim;
+    t.row_stride = row_stride;
+    t.data = reinterpret_cast<const uint8_t*>(d_rows);
+    cuda_check(launch_eb_meta(elem, scale_type, t.data, rows, dim, row_stride, d_scales, d_biases, d_given_sums,
+                              t.meta, nullptr, nullptr, st),
+               "eb_meta_kernel");
+}
+
+void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st) {
+    cuda_check(launch_eb_meta(t.elem, t.scale_type, t.data, t.rows, t.dim, t.row_stride, nullptr, nullptr, nullptr,
+                              nullptr, d_out, nullptr, st),
+               "eb_meta_kernel(row sums)");
+}
+
+void eb_table_free(EbTable* t) {
+    if (!t) return;
+    cudaFree(t->meta);
+    delete t;
+}
+
+uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaStream_t st) {
+    if (!d_given_sums) return 0;
+    Workspace& ws = ws_for(st);
+    std::lock_guard<std::mutex> g(ws.mu);
+    uint32_t* cnt = ws.small + 8;
+    cuda_check(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st), "cudaMemsetAsync");
+    cuda_check(launch_eb_meta(t.elem, t.scale_type, t.data, t.rows, t.dim, t.row_stride, nullptr, nullptr, d_given_sums,
+                              nullptr, nullptr, cnt, st),
+               "eb_meta_kernel(validate)");
+    uint32_t h = 0;
+    cuda_check(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    return h;
+}
+
+void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices, int64_t num_bags,
+            const float* d_weights, float* d_out, int64_t ld_out, bool checked, uint8_t* d_flags, double* d_rsum,
+            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st) {
+    if (num_bags < 0) throw std::invalid_argument("embedding_bag: negative bag count");
+    if (num_bags == 0) {
+        if (checked && d_flag_count) cuda_check(cudaMemsetAsync(d_flag_count, 0, 4, st), "cudaMemsetAsync");
+        return;
+    }
+    if (!d_offsets || !d_indices || !d_out) throw std::invalid_argument("null argument");
+    if (ld_out < t.dim) throw std::invalid_argument("embedding_bag: ld_out < dim");
+    Workspace& ws = ws_for(st);
+    std::lock_guard<std::mutex> g(ws.mu);
+    EbParams p{};
+    p.data = t.data;
+    p.meta = t.meta;
+    p.rows = t.rows;
+    p.dim = t.dim;
+    p.row_stride = t.row_stride;
+    p.offsets = d_offsets;
+    p.indices = d_indices;
+    p.weights = d_weights;
+    p.num_bags = num_bags;
+    p.out = d_out;
+    p.ld_out = ld_out;
+    p.flags = checked ? d_flags : nullptr;
+    p.rsum = checked ? d_rsum : nullptr;
+    p.csum = checked ? d_csum : nullptr;
+    p.flag_count = checked ? d_flag_count : nullptr;
+    p.status = d_status;
+    p.ws_flag_acc = ws.small + 4;
+    p.ws_block_cnt = ws.small + 5;
+    const cudaError_t e = launch_eb_bags(t.elem, t.scale_type, p, checked, st);
+    if (e == cudaErrorInvalidValue) throw std::invalid_argument("embedding_bag: unsupported dimension");
+    cuda_check(e, "eb_bag_kernel");
+}
+
+// ------------------------------------------------------------------ fault lab
+void flip_bit(void* d_base, uint64_t byte_offset, uint32_t bit, cudaStream_t st) {
+    cuda_check(launch_flip_bit(d_base, byte_offset, bit, st), "flip_bit_kernel");
+}
+void set_random(void* d_cell, int width, uint64_t rng_state, cudaStream_t st) {
+    cuda_check(launch_set_random(d_cell, width, rng_state, st), "set_random_kernel");
+}
+void gen(void* d_out, int64_t count, uint64_t seed, uint64_t stream, uint64_t off, int kind, double lo, double hi,
+         uint64_t bound, cudaStream_t st) {
+    cuda_check(launch_gen(d_out, count, seed, stream, off, kind, lo, hi, bound, st), "gen_kernel");
+}
+void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st) {
+    cuda_check(launch_flush(d_buf, bytes, salt, st), "flush_kernel");
+}
+
+}  // namespace abftk

@@ -1,0 +1,99 @@
+// Host runtime of the B200 ABFT library: owns device buffers, tensor maps, the per-stream
+// workspace and the launch decisions. The C ABI (capi.cpp) is a thin layer over this.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "abft_internal.h"
+
+namespace abftk {
+
+struct Fault {
+    bool active = false;
+    int64_t row = 0, col = 0;
+    uint32_t bit = 0;
+};
+
+// ---- GEMM (replaces P:src/gemm_abft.hpp:23-74)
+GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st);
+// Re-encode into an existing handle, growing its buffers only when needed (campaign scratch).
+void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st);
+// Logical k x (n+1) [B | cs] matrix, row-major (PackedEncodedWeight::at contract).
+void read_encoded(const GemmWeight& w, int8_t* d_out, cudaStream_t st);
+void free_weight(GemmWeight* w);
+GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault);
+// checked == false: plain GEMM (csum/flags/err_count ignored).
+void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
+          int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
+          cudaStream_t st, const GemmTiling* force = nullptr);
+void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum_ld, int64_t m, int64_t n,
+            uint8_t* d_flags, uint32_t* d_err_count, cudaStream_t st);
+
+// ---- EmbeddingBag (replaces P:src/embedding_abft.hpp:38-47)
+EbTable* eb_table_create(int elem, const void* d_rows, int64_t rows, int64_t dim, int64_t row_stride, int scale_type,
+                         const void* d_scales, const void* d_biases, const int32_t* d_given_sums, cudaStream_t st);
+void eb_table_free(EbTable* t);
+// Re-point an existing table at new rows/scales (reuses the metadata buffer when large enough).
+void eb_table_rebuild(EbTable& t, int elem, const void* d_rows, int64_t rows, int64_t dim, int64_t row_stride,
+                      int scale_type, const void* d_scales, const void* d_biases, const int32_t* d_given_sums,
+                      cudaStream_t st);
+void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st);
+// Number of rows whose stored sum differs from the recomputed one (synchronizes `st`).
+uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaStream_t st);
+void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices, int64_t num_bags,
+            const float* d_weights, float* d_out, int64_t ld_out, bool checked, uint8_t* d_flags, double* d_rsum,
+            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st);
+int64_t eb_elem_row_bytes(int elem, int64_t dim);
+
+// ---- fault lab
+void flip_bit(void* d_base, uint64_t byte_offset, uint32_t bit, cudaStream_t st);
+void set_random(void* d_cell, int width, uint64_t rng_state, cudaStream_t st);
+void gen(void* d_out, int64_t count, uint64_t seed, uint64_t stream, uint64_t off, int kind, double lo, double hi,
+         uint64_t bound, cudaStream_t st);
+void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
+
+// ---- launchers implemented in the .cu files
+cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, dim3 grid, const CUtensorMap& a, const CUtensorMap& b,
+                               const CUtensorMap& cs, const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
+int gemm_stages(int bn, bool checked);
+cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st);
+cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st);
+cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,
+                          uint8_t* flags, uint32_t* err_count, uint32_t* ws_acc, uint32_t* ws_blocks, cudaStream_t st);
+cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st);
+cudaError_t launch_eb_meta(int elem, int scale, const uint8_t* data, int64_t rows, int64_t dim, int64_t row_stride,
+                           const void* scales, const void* biases, const int32_t* given_sums, void* meta,
+                           int32_t* sums_out, uint32_t* mismatch, cudaStream_t st);
+cudaError_t launch_gen(void* out, int64_t count, uint64_t seed, uint64_t stream, uint64_t off, int kind, double lo,
+                       double hi, uint64_t bound, cudaStream_t st);
+cudaError_t launch_flip_bit(void* base, uint64_t byte_offset, uint32_t bit, cudaStream_t st);
+cudaError_t launch_set_random(void* cell, int width, uint64_t state, cudaStream_t st);
+cudaError_t launch_nonzero(const uint32_t* value, uint8_t* out, int64_t slot, cudaStream_t st);
+cudaError_t launch_any_flag(const uint8_t* flags, int64_t n, uint8_t* out, int64_t slot, cudaStream_t st);
+cudaError_t launch_flush(void* buf, int64_t bytes, int salt, cudaStream_t st);
+
+// Host SplitMix64, identical to P:src/rng.hpp:10-43 (drives fault placement on the host).
+struct SplitMix64 {
+    uint64_t state;
+    static uint64_t mix(uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    }
+    SplitMix64(uint64_t seed, uint64_t stream) : state(mix(seed ^ mix(stream + 0x9e3779b97f4a7c15ULL))) {}
+    uint64_t next() {
+        state += 0x9e3779b97f4a7c15ULL;
+        return mix(state);
+    }
+    uint64_t next_below(uint64_t bound) { return next() % bound; }
+    // Value of draw `e` (0-based) of this stream without advancing (counter-based).
+    static uint64_t draw_at(uint64_t seed, uint64_t stream, uint64_t e) {
+        SplitMix64 r(seed, stream);
+        return mix(r.state + (e + 1) * 0x9e3779b97f4a7c15ULL);
+    }
+};
+
+int device_sm_count();
+
+}  // namespace abftk
