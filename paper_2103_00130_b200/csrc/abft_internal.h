@@ -21,30 +21,36 @@ void cuda_check(cudaError_t e, const char* what);
 #define ABFT_CUDA(call) ::abftk::cuda_check((call), #call)
 
 // ------------------------------------------------------------------ GEMM
-constexpr int kBM = 128;  // rows of A per CTA tile (one UMMA M=128 accumulator)
-constexpr int kBK = 128;  // K bytes per pipeline stage = one 128-byte swizzle span
-constexpr int kCsRows = 16;  // checksum operand: row 0 = cs, rows 1..15 zero (UMMA N=16)
+constexpr int kBM = 128;      // rows of A per CTA; a CTA pair covers 256 rows (tcgen05 cta_group::2, M=256)
+constexpr int kPairM = 256;
+constexpr int kBK = 128;      // K bytes per k-block = one 128-byte swizzle span
+constexpr int kRowAlign = 256;  // B' rows are padded to a multiple of this
 
-// Encoded weight B' = [B | cs] stored K-major: Bt[j][p] = B[p][j] for j < n,
-// zero for n <= j < n_pad and p >= k. The checksum column lives in its own
-// 16-row operand `cs_tile` so the MMA of the main tile never sees it.
+// Encoded weight B' = [B | cs]^T stored K-block-major:
+//   bt[kb][j][kk] = B[kb*128 + kk][j]   for j < n
+//   bt[kb][n][kk] = cs[kb*128 + kk]      (the checksum column lives in row n of B')
+//   zero for n < j < n_pad and for kb*128 + kk >= k.
+// One k-block slab of a tile (rows j0..j0+R) is contiguous (R*128 bytes), so each TMA request is
+// one long burst, and the checksum column is produced by the main MMA of the tile that holds row n.
 struct GemmWeight {
-    int64_t k = 0, n = 0;          // logical sizes (reference PackedEncodedWeight::k()/n())
-    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0
-    int8_t* bt = nullptr;          // n_pad x k_pad
-    int8_t* cs_tile = nullptr;     // 16 x k_pad
-    int8_t* cs = nullptr;          // k  (WeightChecksum::values, each in [0,126])
+    int64_t k = 0, n = 0;          // logical sizes (PackedEncodedWeight::k()/n())
+    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad >= n + 1
+    int8_t* bt = nullptr;          // k_pad/128 x n_pad x 128
+    int8_t* cs = nullptr;          // k (WeightChecksum::values, each in [0,126])
     bool owns = true;
-    size_t bt_cap = 0, kpad_cap = 0;  // allocation capacities (campaign scratch re-encodes in place)
-    CUtensorMap map_b[3]{};        // box {128, BN} for BN = 64, 128, 256
-    CUtensorMap map_cs{};          // box {128, 16}
+    size_t bt_cap = 0, cs_cap = 0;  // allocation capacities (campaign scratch re-encodes in place)
+    CUtensorMap map_b[3]{};         // 3D box {128, BN/2, KS} for BN = 64, 128, 256
+    uint64_t offset(int64_t i, int64_t j) const {  // byte offset of logical element (i, j), j <= n
+        return static_cast<uint64_t>((i / kBK) * n_pad * kBK + j * kBK + (i % kBK));
+    }
 };
 
 struct GemmParams {
     int m, n;          // logical output size (n excludes the checksum column)
-    int k_blocks;      // total 128-byte K blocks
-    int kb_per_split;  // K blocks handled by one CTA
-    int n_tiles, m_tiles, splits;
+    int k_blocks;      // 128-byte K blocks
+    int n_tiles;       // N tiles covered by the MMA (includes the tile holding row n when CHECKED)
+    int m_tiles;       // 256-row pair tiles
+    int num_tiles;     // m_tiles * n_tiles
     int32_t* c;
     int64_t ldc;
     int32_t* csum;  // checksum column C'[:, n] (checked only)
@@ -53,20 +59,19 @@ struct GemmParams {
     uint32_t* err_count; // number of flagged rows (checked only)
     // self-resetting per-stream workspace
     uint32_t* row_res;    // [m] sum of per-tile row residues (each < 127)
-    int32_t* csum_acc;    // [m] split-K partial checksum column
-    uint32_t* mtile_cnt;  // [m_tiles] arrival counters
+    int32_t* csum_acc;    // [m] checksum column value
+    uint32_t* half_cnt;   // [m_tiles*2] arrivals per 128-row half
     uint32_t* err_acc;    // [1]
     uint32_t* done_cnt;   // [1]
-    uint32_t* tile_flag;  // [m_tiles * n_tiles] split-K zero-init epochs
-    uint32_t epoch;
     // in-epilogue fault hook (P:src/fault_lab.cpp:192-195 semantics): flip `bit` of C'(row, col)
     int fault_active, fault_row, fault_col, fault_bit;
+    unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
 };
 
-enum EpiMode { kEpiTmaStore = 0, kEpiTmaReduce = 1, kEpiDirect = 2 };
+enum EpiMode { kEpiTmaStore = 0, kEpiDirect = 2, kEpiNone = 4 };
 
 struct GemmTiling {
-    int bn, splits, epi;
+    int bn, epi;
 };
 
 // ------------------------------------------------------------------ EmbeddingBag

@@ -286,9 +286,7 @@ abftlp_status abftlp_gemm_weight_checksums(const abftlp_gemm_weight* w, int8_t* 
 abftlp_status abftlp_gemm_weight_set_checksums(abftlp_gemm_weight* w, const int8_t* d_cs, abftlp_stream stream) {
     if (!w || !d_cs) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
-        const size_t k = static_cast<size_t>(w->w->k);
-        ABFT_CUDA(cudaMemcpyAsync(w->w->cs, d_cs, k, cudaMemcpyDeviceToDevice, as_stream(stream)));
-        ABFT_CUDA(cudaMemcpyAsync(w->w->cs_tile, d_cs, k, cudaMemcpyDeviceToDevice, as_stream(stream)));
+        abftk::set_checksums(*w->w, d_cs, as_stream(stream));
         return ABFTLP_OK;
     });
 }
@@ -457,12 +455,8 @@ abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uin
         if (i >= static_cast<uint64_t>(W.k) || j > static_cast<uint64_t>(W.n))
             throw std::out_of_range("inject_weight_B: coordinates out of range");
         if (bit >= 8) throw std::out_of_range("flip_bit: bit index out of range");
-        if (j < static_cast<uint64_t>(W.n)) {
-            abftk::flip_bit(W.bt, j * static_cast<uint64_t>(W.k_pad) + i, bit, as_stream(stream));
-        } else {  // checksum column: both the stored vector and the MMA operand
-            abftk::flip_bit(W.cs, i, bit, as_stream(stream));
-            abftk::flip_bit(W.cs_tile, i, bit, as_stream(stream));
-        }
+        abftk::flip_bit(W.bt, W.offset(static_cast<int64_t>(i), static_cast<int64_t>(j)), bit, as_stream(stream));
+        if (j == static_cast<uint64_t>(W.n)) abftk::flip_bit(W.cs, i, bit, as_stream(stream));  // keep the vector in sync
         return ABFTLP_OK;
     });
 }
@@ -498,6 +492,11 @@ abftlp_status abftlp_generate(void* d_out, uint64_t count, uint64_t seed, uint64
         abftk::gen(d_out, static_cast<int64_t>(count), seed, rng_stream, off, kind, lo, hi, bound, as_stream(stream));
         return ABFTLP_OK;
     });
+}
+
+// Debug: record 8 globaltimer stamps per GEMM CTA into d_trace (NULL disables). Not in the headers.
+__attribute__((visibility("default"))) void abftlp_debug_gemm_trace(unsigned long long* d_trace) {
+    abftk::set_gemm_trace(d_trace);
 }
 
 abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream) {

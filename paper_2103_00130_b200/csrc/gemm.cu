@@ -1,18 +1,23 @@
 // ABFT int8 GEMM for sm_100a.
 //
 //   encode_weight_kernel  replaces compute_row_checksums + PackedEncodedWeight
-//                         (P:src/gemm_abft.cpp:60-91): one pass over B producing the
-//                         mod-127 row checksums and B' in the K-major, zero-padded layout
-//                         the TMA/UMMA mainloop streams.
-//   gemm_u8s8_kernel      replaces abft_gemm + verify_checksums / plain_gemm
-//                         (P:src/gemm_abft.cpp:30-56, 93-124): TMA -> 128B-swizzled smem ring
-//                         -> tcgen05.mma.kind::i8 (A u8 x B s8 -> s32 in TMEM) -> epilogue that
-//                         stores C (TMA store, or TMA reduce-add for split-K) and, when CHECKED,
-//                         reduces every output row mod 127 and compares it with the checksum
-//                         column A*cs (an extra N=16 MMA on the checksum operand) -- per-row
-//                         flags without a second pass over C.
-//   verify_kernel         replaces verify_checksums (P:src/gemm_abft.cpp:113-124) for
-//                         post-hoc checks (faults injected into C after the product).
+//                         (P:src/gemm_abft.cpp:60-91): one pass over B producing the mod-127 row
+//                         checksums cs and B' = [B | cs]^T in the K-block-major layout the mainloop
+//                         streams (abft_internal.h: GemmWeight). The checksum is row n of B', so the
+//                         tile that holds row n computes C'[:, n] = A*cs with the same MMAs.
+//   gemm_pair_kernel      replaces abft_gemm + verify_checksums / plain_gemm
+//                         (P:src/gemm_abft.cpp:30-56, 93-124). Persistent CTA pairs
+//                         (cluster of 2, tcgen05.mma.cta_group::2 kind::i8, M=256 x N=BN, A u8 x
+//                         B s8 -> s32 in TMEM). Each CTA loads its 128 rows of A and half of the
+//                         B' tile; one 3-D TMA request per operand brings KS k-blocks (few, large
+//                         requests: the per-SM TMA engine completes requests ~serially, so bytes per
+//                         request set the ingest rate). Two TMEM accumulators let the epilogue of
+//                         tile i overlap the mainloop of tile i+1. The CHECKED epilogue reduces
+//                         every output row mod 127 straight from TMEM, takes the checksum column
+//                         from the tile that holds it, and the last CTA of each 128-row half
+//                         compares and publishes flags -- no second pass over C.
+//   verify_kernel         replaces verify_checksums (P:src/gemm_abft.cpp:113-124) for post-hoc
+//                         checks (faults injected into C after the product).
 #include <cuda_runtime.h>
 
 #include "abft_internal.h"
@@ -21,17 +26,17 @@
 namespace abftk {
 
 // ============================================================ encoder
-// Block handles a 64-row slab of B (k rows) and walks all n columns in 64-wide chunks, so the
-// row sums stay block-local (int64, as the reference). Writes Bt[j][p] = B[p][j] (zero padded to
-// n_pad x k_pad), cs[p] = mod127(sum_j B[p][j]) and row 0 of the 16-row checksum operand.
+// Block handles a 64-row slab of B (64 consecutive p, inside one k-block) and walks all n_pad
+// columns in 64-wide chunks, so the int64 row sums stay block-local (as the reference). Writes
+// B'[kb][j][p % 128] (64 contiguous bytes per j), then the checksum row j = n.
 __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __restrict__ b, int64_t k, int64_t n,
-                                                            int64_t ldb, int8_t* __restrict__ bt, int64_t k_pad,
-                                                            int64_t n_pad, int8_t* __restrict__ cs_tile,
+                                                            int64_t ldb, int8_t* __restrict__ bt, int64_t n_pad,
                                                             int8_t* __restrict__ cs) {
     __shared__ int8_t tile[64][64 + 4];
     __shared__ long long part[4][64];
     const int tid = threadIdx.x;
     const int64_t p0 = static_cast<int64_t>(blockIdx.x) * 64;
+    int8_t* slab = bt + (p0 / kBK) * n_pad * kBK + (p0 % kBK);
     long long acc = 0;  // thread (tid & 63) accumulates row (tid & 63) for column quarter (tid >> 6)
     for (int64_t j0 = 0; j0 < n_pad; j0 += 64) {
         for (int idx = tid; idx < 64 * 64; idx += 256) {
@@ -47,7 +52,7 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
         }
         for (int idx = tid; idx < 64 * 64; idx += 256) {
             const int c = idx >> 6, r = idx & 63;
-            bt[(j0 + c) * k_pad + p0 + r] = tile[r][c];
+            slab[(j0 + c) * kBK + r] = tile[r][c];
         }
         __syncthreads();
     }
@@ -57,262 +62,313 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
         const long long s = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
         const int64_t p = p0 + tid;
         const int8_t v = p < k ? static_cast<int8_t>(mod127(s)) : static_cast<int8_t>(0);
-        cs_tile[p] = v;  // row 0 of the checksum operand; rows 1..15 stay zero
+        slab[n * kBK + tid] = v;  // checksum row of B'
         if (p < k) cs[p] = v;
     }
 }
 
+// Replace the checksum row of B' (and the cs vector) with caller-supplied values.
+__global__ void set_checksums_kernel(int8_t* __restrict__ bt, int8_t* __restrict__ cs, const int8_t* __restrict__ src,
+                                     int64_t k, int64_t n, int64_t n_pad) {
+    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < k;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int8_t v = src[p];
+        bt[(p / kBK) * n_pad * kBK + n * kBK + (p % kBK)] = v;
+        cs[p] = v;
+    }
+}
+
 // Logical k x (n+1) view [B | cs] of an encoded weight (PackedEncodedWeight::at contract).
-__global__ void read_encoded_kernel(const int8_t* __restrict__ bt, const int8_t* __restrict__ cs, int64_t k, int64_t n,
-                                    int64_t k_pad, int8_t* __restrict__ out) {
+__global__ void read_encoded_kernel(const int8_t* __restrict__ bt, int64_t k, int64_t n, int64_t n_pad,
+                                    int8_t* __restrict__ out) {
     const int64_t total = k * (n + 1);
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / (n + 1), j = e - i * (n + 1);
-        out[e] = j < n ? bt[j * k_pad + i] : cs[i];
+        out[e] = bt[(i / kBK) * n_pad * kBK + j * kBK + (i % kBK)];
     }
 }
 
-// ============================================================ GEMM
-template <int BN, bool CHECKED>
-struct GemmCfg {
-    static constexpr int kABytes = kBM * kBK;
-    static constexpr int kBBytes = BN * kBK;
-    static constexpr int kCsBytes = CHECKED ? kCsRows * kBK : 0;
-    static constexpr int kStageBytes = kABytes + kBBytes + kCsBytes;
-    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-    static constexpr int kTmemNeed = BN + (CHECKED ? 16 : 0);
-    static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128
-                                                                : kTmemNeed <= 256 ? 256 : 512;
-    static constexpr int kBarBytes = 256;
-    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kBarBytes;
-    static_assert(kStageBytes % 1024 == 0, "stage buffers must keep 1024-byte alignment");
-    static_assert(kStages * kStageBytes >= 4 * 2 * 4096, "epilogue staging reuses the stage ring");
+// ============================================================ GEMM (CTA pairs)
+template <int BN>
+struct PairCfg {
+    static constexpr int KS = BN == 64 ? 4 : 2;             // k-blocks per pipeline stage
+    static constexpr int kABytes = kBM * kBK;                // per CTA per k-block (its 128 rows of A)
+    static constexpr int kBBytes = (BN / 2) * kBK;           // per CTA per k-block (its half of the B' tile)
+    static constexpr int kStageBytes = KS * (kABytes + kBBytes);
+    static constexpr int kStaging = 4 * 2 * 4096;            // epilogue: 4 warps x 2 x (32 rows x 32 int32)
+    static constexpr int kBarBytes = 512;
+    static constexpr int kRawStages = (220 * 1024 - 1024 - kStaging - kBarBytes) / kStageBytes;
+    static constexpr int kStages = kRawStages > 8 ? 8 : kRawStages;
+    static constexpr uint32_t kTmemCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStaging + kBarBytes;
+    static_assert(kStages >= 2, "need a double-buffered ring");
+    static_assert(kBBytes % 1024 == 0 && kABytes % 1024 == 0, "SW128 tiles must stay 1024-byte aligned");
 };
 
 template <int BN, bool CHECKED, int EPI>
-__global__ void __launch_bounds__(192, 1)
-    gemm_u8s8_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmCS, const __grid_constant__ CUtensorMap tmC,
-                     const GemmParams p) {
-    using Cfg = GemmCfg<BN, CHECKED>;
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
+    using Cfg = PairCfg<BN>;
     constexpr int STAGES = Cfg::kStages;
+    constexpr int KS = Cfg::KS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
+    uint8_t* staging = smem + STAGES * Cfg::kStageBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(staging + Cfg::kStaging);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     uint32_t* bcast = tmem_holder + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nt = blockIdx.x, mt = blockIdx.y, sp = blockIdx.z;
-    const int kb0 = sp * p.kb_per_split;
-    const int kb1 = min(kb0 + p.kb_per_split, p.k_blocks);
-    const int nkb = kb1 - kb0;
-    const bool has_cs = CHECKED && nt == 0;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = static_cast<int>(cluster_id_x()), npairs = static_cast<int>(nclusters_x());
+    const int kb_steps = (p.k_blocks + KS - 1) / KS;
+    unsigned long long* trace = p.trace ? p.trace + 16ull * blockIdx.x : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+        }
         fence_mbar_init();
     }
-    if (warp == 0) tmem_alloc<Cfg::kTmemCols>(tmem_holder);
-    if (warp == 4 && lane == 0) {
+    if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
-        if (has_cs) tma_prefetch(&tmCS);
-        if (EPI != kEpiDirect) tma_prefetch(&tmC);
+        if (EPI == kEpiTmaStore) tma_prefetch(&tmC);
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_holder;
+    // Barriers must be visible to the peer before any TMA / commit targets them; TMEM is allocated
+    // afterwards by the MMA warp so the producer's first loads overlap the allocation.
+    cluster_sync();
+    if (trace && threadIdx.x == 0) trace[1] = globaltimer();
+    uint32_t tmem = 0;
+    if (warp >= 1) {
+        if (warp == 1) {
+            tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
+            tc_fence_before();
+        }
+        named_bar_sync(2, 160);  // MMA warp + 4 epilogue warps
+        tc_fence_after();
+        tmem = *tmem_holder;
+    }
 
-    if (warp == 4) {
-        // ---------------- TMA producer (one elected lane)
+    if (warp == 0) {
+        // ---------------- TMA producer (both CTAs; completion counted on the leader's barrier)
         if (lane == 0) {
-            const uint64_t pol_a = policy_evict_last();   // A is re-read by every N tile
-            const uint64_t pol_b = policy_evict_first();  // B' is streamed once per call
-            const uint32_t bytes = Cfg::kABytes + Cfg::kBBytes + (has_cs ? Cfg::kCsBytes : 0);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = smem + s * Cfg::kStageBytes;
-                mbar_arrive_expect_tx(&full[s], bytes);
-                const int kx = (kb0 + i) * kBK;
-                tma_load_2d(st, &tmA, &full[s], kx, mt * kBM, pol_a);
-                tma_load_2d(st + Cfg::kABytes, &tmB, &full[s], kx, nt * BN, pol_b);
-                if (has_cs) tma_load_2d(st + Cfg::kABytes + Cfg::kBBytes, &tmCS, &full[s], kx, 0, pol_a);
+            const uint64_t pol_b = policy_evict_last();  // weights are re-used across calls
+            const uint64_t pol_a = policy_evict_last();  // A is re-read by every N tile of the call
+            int it = 0;
+            for (int t = pair; t < p.num_tiles; t += npairs) {
+                const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+                for (int ks = 0; ks < kb_steps; ++ks, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * Cfg::kStageBytes;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+                    tma_load_3d_pair(st, &tmA, &full[s], 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS, pol_a);
+                    tma_load_3d_pair(st + KS * Cfg::kABytes, &tmB, &full[s], 0,
+                                     nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS, pol_b);
+                }
             }
         }
-    } else if (warp == 5) {
-        // ---------------- MMA issuer (one thread issues for the whole CTA)
-        if (lane == 0) {
-            constexpr uint32_t id_main = idesc_u8s8(kBM, BN);
-            constexpr uint32_t id_cs = idesc_u8s8(kBM, kCsRows);
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+    } else if (warp == 1) {
+        // ---------------- MMA issuer: leader CTA, one thread, for the whole pair
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = idesc_u8s8(kPairM, BN);
+            int it = 0, local = 0;
+            for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+                const int acc = local & 1;
+                const uint32_t aph = (local >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
-                const uint32_t a_addr = smem_u32(smem + s * Cfg::kStageBytes);
-                const uint64_t da = umma_desc_sw128(a_addr);
-                const uint64_t db = umma_desc_sw128(a_addr + Cfg::kABytes);
-                const uint64_t dc = umma_desc_sw128(a_addr + Cfg::kABytes + Cfg::kBBytes);
+                const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
+                for (int ks = 0; ks < kb_steps; ++ks, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    if (trace && local == 0 && ks == 0) trace[2] = globaltimer();
+                    const uint32_t a0 = smem_u32(smem + s * Cfg::kStageBytes);
+                    const uint32_t b0 = a0 + KS * Cfg::kABytes;
 #pragma unroll
-                for (int kk = 0; kk < kBK / 32; ++kk) {  // UMMA K = 32 bytes for 8-bit operands
-                    const uint32_t acc = (i | kk) != 0;
-                    mma_i8(tmem, da + 2 * kk, db + 2 * kk, id_main, acc);
-                    if (has_cs) mma_i8(tmem + BN, da + 2 * kk, dc + 2 * kk, id_cs, acc);
+                    for (int j = 0; j < KS; ++j) {
+                        const uint64_t da = umma_desc_sw128(a0 + j * Cfg::kABytes);
+                        const uint64_t db = umma_desc_sw128(b0 + j * Cfg::kBBytes);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; ++kk)  // UMMA K = 32 bytes for 8-bit operands
+                            mma_i8_pair(d, da + 2 * kk, db + 2 * kk, idesc, (ks | j | kk) != 0 ? 1u : 0u);
+                    }
+                    mma_commit_pair(&empty[s]);  // frees the slot in both CTAs once these MMAs read it
                 }
-                mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
+                mma_commit_pair(&tfull[acc]);  // accumulator complete, both CTAs' epilogues may read
+                if (trace && local == 0) trace[3] = globaltimer();
             }
-            mma_commit(tmem_full);  // accumulator complete
         }
     } else {
-        // ---------------- epilogue: warps 0..3, thread <-> output row (TMEM lane)
-        const int row = mt * kBM + warp * 32 + lane;
-        const int n0 = nt * BN;
-        uint32_t* my_flag = p.tile_flag + (mt * p.n_tiles + nt);
-        if constexpr (EPI == kEpiTmaReduce) {
-            if (sp == 0) {
-                // Split 0 zero-fills this CTA's C tile while the mainloop runs; every split then
-                // reduce-adds its partial product into it (int32 addition is exact).
-                const int rows_here = min(kBM, p.m - mt * kBM);
-                const int v4_per_row = min(BN, p.n - n0) >> 2;
-                const int total = rows_here * v4_per_row;
-                for (int idx = threadIdx.x; idx < total; idx += 128) {
-                    const int r = idx / v4_per_row, q = idx - r * v4_per_row;
-                    *reinterpret_cast<int4*>(p.c + static_cast<int64_t>(mt * kBM + r) * p.ldc + n0 + 4 * q) =
-                        make_int4(0, 0, 0, 0);
-                }
-                __threadfence();
-                named_bar_sync(1, 128);
-                if (threadIdx.x == 0) st_release_gpu(my_flag, p.epoch);
-            }
-        }
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        if constexpr (EPI == kEpiTmaReduce) {
-            if (lane == 0) {
-                while (static_cast<int32_t>(ld_acquire_gpu(my_flag) - p.epoch) < 0) {
-                }
-                fence_proxy_async_global();
-            }
-            __syncwarp();
-        }
-        fence_proxy_async_smem();
-        const uint32_t t_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-        const int fault_here = p.fault_active && row == p.fault_row;
-        long long rsum = 0;
+        // ---------------- epilogue: warps 2..5, thread <-> one row of this CTA's 128-row half
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int ncols = CHECKED ? p.n + 1 : p.n;
+        const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+        int local = 0, chunk_ctr = 0;
+        for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+            const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+            const int acc = local & 1;
+            const uint32_t aph = (local >> 1) & 1;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
+            const int row0 = mt * kPairM + static_cast<int>(rank) * kBM + q * 32;  // first row of this warp
+            const int row = row0 + lane;
+            const int n0 = nt * BN;
+            const uint32_t t_row = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+            const bool fault_here = p.fault_active && row == p.fault_row;
+            long long rsum = 0;
+            int32_t csv = 0;
+            bool has_cs = false;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-            const int col0 = n0 + c * 32;
-            if (col0 >= p.n) break;  // warp-uniform
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(t_row + c * 32, v);
-            tmem_wait_ld();
-            if (fault_here) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (p.fault_col == col0 + j) v[j] ^= 1u << p.fault_bit;
-            }
-            if constexpr (CHECKED) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) rsum += static_cast<int32_t>(v[j]);
-            }
-            if constexpr (EPI == kEpiDirect) {
-                if (row < p.m) {
-                    int32_t* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+            for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = n0 + c * 32;
+                if (col0 >= ncols) break;  // warp-uniform
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t_row + c * 32, v);
+                tmem_wait_ld();
+                if (fault_here) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (col0 + j < p.n) crow[col0 + j] = static_cast<int32_t>(v[j]);
+                        if (p.fault_col == col0 + j) v[j] ^= 1u << p.fault_bit;
                 }
-            } else {
-                uint8_t* buf = smem + (warp * 2 + (c & 1)) * 4096;
-                if (c >= 2) {
-                    if (lane == 0) bulk_wait_read<1>();
-                    __syncwarp();
-                }
+                if constexpr (CHECKED) {
+                    if (col0 + 32 <= p.n) {
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    if (mt * kBM + warp * 32 < p.m) {
-                        if constexpr (EPI == kEpiTmaStore)
-                            tma_store_2d(&tmC, buf, col0, mt * kBM + warp * 32);
-                        else
-                            tma_reduce_add_2d(&tmC, buf, col0, mt * kBM + warp * 32);
+                        for (int j = 0; j < 32; ++j) rsum += static_cast<int32_t>(v[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if (col0 + j < p.n) rsum += static_cast<int32_t>(v[j]);
+                            if (col0 + j == p.n) {
+                                csv = static_cast<int32_t>(v[j]);
+                                has_cs = true;
+                            }
+                        }
                     }
-                    bulk_commit();
+                }
+                if (col0 >= p.n) continue;  // the checksum column is not part of C
+                if constexpr (EPI == kEpiTmaStore) {
+                    uint8_t* buf = staging + (q * 2 + (chunk_ctr & 1)) * 4096;
+                    if (chunk_ctr >= 2) {
+                        if (lane == 0) bulk_wait_read<1>();
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq)
+                        *reinterpret_cast<uint4*>(buf + lane * 128 + ((qq ^ (lane & 7)) << 4)) =
+                            make_uint4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (row0 < p.m) tma_store_2d(&tmC, buf, col0, row0);
+                        bulk_commit();
+                    }
+                    ++chunk_ctr;
+                } else if constexpr (EPI == kEpiDirect) {
+                    if (row < p.m) {
+                        int32_t* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.n) crow[col0 + j] = static_cast<int32_t>(v[j]);
+                    }
+                }
+            }
+            if (trace && local == 0 && threadIdx.x == 64) trace[7] = globaltimer();
+            // accumulator drained: let the MMA warp reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0)
+                    mbar_arrive_local(&tempty[acc]);
+                else
+                    mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc * 8));
+            }
+            if constexpr (CHECKED) {
+                if (row < p.m) {
+                    // mod is a ring homomorphism: the residue of the int64 row sum equals the sum of the
+                    // per-tile residues mod 127 (P:src/gemm_abft.cpp:119-122 reduces the row sum once).
+                    atomicAdd(&p.row_res[row], static_cast<uint32_t>(mod127(rsum)));
+                    if (has_cs) p.csum_acc[row] = csv;
+                }
+                // All 128 threads' contributions are issued; one release by one thread publishes them
+                // (release is cumulative over the barrier), and only warp (threadIdx 64..95) waits for
+                // the arrival count -- the other epilogue warps move on to the next tile.
+                named_bar_sync(1, 128);
+                if (warp == 2) {
+                    const int half = mt * 2 + static_cast<int>(rank);
+                    uint32_t prev = 0;
+                    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.half_cnt[half], 1u);
+                    prev = __shfl_sync(0xffffffffu, prev, 0);
+                    if (trace && local == 0 && lane == 0) trace[8] = globaltimer();
+                    if (prev == static_cast<uint32_t>(p.n_tiles - 1)) {
+                        // Last tile of this 128-row half: every contribution is visible. Finalize the 128
+                        // rows (4 per lane) and leave the workspace zeroed for the next call.
+                        __threadfence();  // every lane acquires (lane 0's acquire is not warp-cumulative)
+                        const int hrow0 = mt * kPairM + static_cast<int>(rank) * kBM;
+                        uint32_t accs[4];
+                        int32_t css[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int rr = hrow0 + r * 32 + lane;
+                            accs[r] = rr < p.m ? ld_relaxed_gpu(&p.row_res[rr]) : 0u;
+                            css[r] = rr < p.m ? static_cast<int32_t>(ld_relaxed_gpu(
+                                                    reinterpret_cast<uint32_t*>(&p.csum_acc[rr])))
+                                              : 0;
+                        }
+                        uint32_t cnt = 0;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) {
+                            const int rr = hrow0 + r * 32 + lane;
+                            int flag = 0;
+                            if (rr < p.m) {
+                                flag = static_cast<int32_t>(accs[r] % 127u) != mod127(css[r]);
+                                p.flags[rr] = static_cast<uint8_t>(flag);
+                                p.csum[static_cast<int64_t>(rr) * p.csum_ld] = css[r];
+                                p.row_res[rr] = 0u;
+                            }
+                            cnt += __popc(__ballot_sync(0xffffffffu, flag));
+                        }
+                        if (lane == 0) {
+                            p.half_cnt[half] = 0u;
+                            if (cnt) atomicAdd(p.err_acc, cnt);
+                            const uint32_t done = atom_add_acq_rel_gpu(p.done_cnt, 1u);
+                            if (done == static_cast<uint32_t>(2 * p.m_tiles - 1)) {
+                                *p.err_count = atomicExch(p.err_acc, 0u);
+                                *p.done_cnt = 0u;
+                            }
+                        }
+                    }
                 }
             }
         }
-        if constexpr (EPI != kEpiDirect) {
+        if constexpr (EPI == kEpiTmaStore) {
             if (lane == 0) bulk_wait<0>();
             __syncwarp();
         }
-        if constexpr (CHECKED) {
-            int32_t csv = 0;
-            if (has_cs) {
-                csv = static_cast<int32_t>(tmem_ld_32x32b_x1(t_row + BN));
-                tmem_wait_ld();
-                if (fault_here && p.fault_col == p.n) csv ^= static_cast<int32_t>(1u << p.fault_bit);
-            }
-            if (row < p.m) {
-                // mod is a ring homomorphism: the residue of the full int64 row sum equals the sum of
-                // per-tile residues mod 127 (P:src/gemm_abft.cpp:119-122 reduces the int64 sum once).
-                atomicAdd(&p.row_res[row], static_cast<uint32_t>(mod127(rsum)));
-                if (has_cs) atomicAdd(&p.csum_acc[row], csv);
-            }
-            __threadfence();
-            named_bar_sync(1, 128);
-            if (threadIdx.x == 0) {
-                const uint32_t prev = atomicAdd(&p.mtile_cnt[mt], 1u);
-                *bcast = prev == static_cast<uint32_t>(p.n_tiles * p.splits - 1) ? 1u : 0u;
-            }
-            named_bar_sync(1, 128);
-            if (*bcast) {
-                // Last CTA of this M tile: every contribution is in; finalize the rows and clean the
-                // workspace for the next call on this stream.
-                __threadfence();
-                int flag = 0;
-                if (row < p.m) {
-                    const uint32_t acc = atomicExch(&p.row_res[row], 0u);
-                    const int32_t cs = atomicExch(&p.csum_acc[row], 0);
-                    flag = static_cast<int32_t>(acc % 127u) != mod127(cs);
-                    p.flags[row] = static_cast<uint8_t>(flag);
-                    p.csum[static_cast<int64_t>(row) * p.csum_ld] = cs;
-                }
-                const uint32_t wcount = __popc(__ballot_sync(0xffffffffu, flag));
-                if (lane == 0 && wcount) atomicAdd(p.err_acc, wcount);
-                __threadfence();
-                named_bar_sync(1, 128);
-                if (threadIdx.x == 0) {
-                    atomicExch(&p.mtile_cnt[mt], 0u);
-                    const uint32_t prev = atomicAdd(p.done_cnt, 1u);
-                    if (prev == static_cast<uint32_t>(p.m_tiles - 1)) {
-                        __threadfence();
-                        *p.err_count = atomicExch(p.err_acc, 0u);
-                        atomicExch(p.done_cnt, 0u);
-                    }
-                }
-            }
-        }
+        if (trace && threadIdx.x == 64) trace[5] = globaltimer();
     }
     tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
+    cluster_sync();
+    if (trace && threadIdx.x == 0) trace[6] = globaltimer();
+    if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<Cfg::kTmemCols>(tmem);
+        tmem_dealloc_pair<Cfg::kTmemCols>(tmem);
     }
 }
 
@@ -357,59 +413,58 @@ __global__ void __launch_bounds__(256) verify_kernel(const int32_t* __restrict__
 
 // ============================================================ host launchers
 template <int BN, bool CHECKED, int EPI>
-static cudaError_t launch_one(dim3 grid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cs,
-                              const CUtensorMap& c, const GemmParams& p, cudaStream_t st) {
-    using Cfg = GemmCfg<BN, CHECKED>;
-    auto kern = gemm_u8s8_kernel<BN, CHECKED, EPI>;
+static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                              const GemmParams& p, cudaStream_t st) {
+    using Cfg = PairCfg<BN>;
+    auto kern = gemm_pair_kernel<BN, CHECKED, EPI>;
     static bool attr_done = false;  // benign race: idempotent attribute set
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    kern<<<grid, 192, Cfg::kSmemBytes, st>>>(a, b, cs, c, p);
+    kern<<<2 * pairs, 192, Cfg::kSmemBytes, st>>>(a, b, c, p);
     return cudaGetLastError();
 }
 
 template <int BN, bool CHECKED>
-static cudaError_t launch_epi(int epi, dim3 grid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& cs,
-                              const CUtensorMap& c, const GemmParams& p, cudaStream_t st) {
+static cudaError_t launch_epi(int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                              const GemmParams& p, cudaStream_t st) {
     switch (epi) {
-        case kEpiTmaStore: return launch_one<BN, CHECKED, kEpiTmaStore>(grid, a, b, cs, c, p, st);
-        case kEpiTmaReduce: return launch_one<BN, CHECKED, kEpiTmaReduce>(grid, a, b, cs, c, p, st);
-        default: return launch_one<BN, CHECKED, kEpiDirect>(grid, a, b, cs, c, p, st);
+        case kEpiTmaStore: return launch_one<BN, CHECKED, kEpiTmaStore>(pairs, a, b, c, p, st);
+        case kEpiNone: return launch_one<BN, CHECKED, kEpiNone>(pairs, a, b, c, p, st);
+        default: return launch_one<BN, CHECKED, kEpiDirect>(pairs, a, b, c, p, st);
     }
 }
 
-cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, dim3 grid, const CUtensorMap& a, const CUtensorMap& b,
-                               const CUtensorMap& cs, const CUtensorMap& c, const GemmParams& p, cudaStream_t st) {
+cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b,
+                               const CUtensorMap& c, const GemmParams& p, cudaStream_t st) {
     if (checked) {
-        if (bn == 256) return launch_epi<256, true>(epi, grid, a, b, cs, c, p, st);
-        if (bn == 128) return launch_epi<128, true>(epi, grid, a, b, cs, c, p, st);
-        return launch_epi<64, true>(epi, grid, a, b, cs, c, p, st);
+        if (bn == 256) return launch_epi<256, true>(epi, pairs, a, b, c, p, st);
+        if (bn == 128) return launch_epi<128, true>(epi, pairs, a, b, c, p, st);
+        return launch_epi<64, true>(epi, pairs, a, b, c, p, st);
     }
-    if (bn == 256) return launch_epi<256, false>(epi, grid, a, b, cs, c, p, st);
-    if (bn == 128) return launch_epi<128, false>(epi, grid, a, b, cs, c, p, st);
-    return launch_epi<64, false>(epi, grid, a, b, cs, c, p, st);
+    if (bn == 256) return launch_epi<256, false>(epi, pairs, a, b, c, p, st);
+    if (bn == 128) return launch_epi<128, false>(epi, pairs, a, b, c, p, st);
+    return launch_epi<64, false>(epi, pairs, a, b, c, p, st);
 }
 
-int gemm_stages(int bn, bool checked) {
-    if (checked) return bn == 256 ? GemmCfg<256, true>::kStages : bn == 128 ? GemmCfg<128, true>::kStages
-                                                                            : GemmCfg<64, true>::kStages;
-    return bn == 256 ? GemmCfg<256, false>::kStages : bn == 128 ? GemmCfg<128, false>::kStages
-                                                                : GemmCfg<64, false>::kStages;
-}
+int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }
 
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st) {
     int64_t blocks = (w.k * (w.n + 1) + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    read_encoded_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(w.bt, w.cs, w.k, w.n, w.k_pad, out);
+    read_encoded_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(w.bt, w.k, w.n, w.n_pad, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st) {
+    set_checksums_kernel<<<static_cast<unsigned>((w.k + 255) / 256), 256, 0, st>>>(w.bt, w.cs, src, w.k, w.n, w.n_pad);
     return cudaGetLastError();
 }
 
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st) {
-    encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.k_pad, w.n_pad,
-                                                                             w.cs_tile, w.cs);
+    encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs);
     return cudaGetLastError();
 }
 

@@ -74,12 +74,9 @@ struct Workspace {
     uint32_t* row_res = nullptr;
     int32_t* csum_acc = nullptr;
     int64_t rows_cap = 0;
-    uint32_t* mtile_cnt = nullptr;
-    int64_t mtiles_cap = 0;
-    uint32_t* tile_flag = nullptr;
-    int64_t tiles_cap = 0;
+    uint32_t* half_cnt = nullptr;
+    int64_t halves_cap = 0;
     uint32_t* small = nullptr;  // [0] err_acc [1] done_cnt [2] verify acc [3] verify blocks [4] eb acc [5] eb blocks
-    uint32_t epoch = 0;
     uint8_t* scratch = nullptr;  // A repack buffer
     size_t scratch_cap = 0;
     std::mutex mu;
@@ -117,44 +114,58 @@ static void grow(T*& ptr, int64_t& cap, int64_t need, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ GEMM
-static CUtensorMap weight_map(const GemmWeight& w, int bn) {
-    return w.map_b[bn == 64 ? 0 : bn == 128 ? 1 : 2];
+static unsigned long long* g_trace = nullptr;  // debug: per-CTA phase timestamps
+void set_gemm_trace(unsigned long long* d_trace) { g_trace = d_trace; }
+
+int gemm_ks(int bn);
+cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
+
+// 3D view {128 bytes of a k-block, rows, k-blocks} of a K-contiguous byte matrix. `row_bytes` is
+// the row pitch, `kb_bytes` the step between k-blocks (128 for row-major A; n_pad*128 for B').
+static CUtensorMap make_map_kblocks(const void* base, uint64_t rows, uint64_t kblocks, uint64_t row_bytes,
+                                    uint64_t kb_bytes, uint32_t box_rows, uint32_t box_kb) {
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBK), rows, kblocks};
+    const cuuint64_t strides[2] = {row_bytes, kb_bytes};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), box_rows, box_kb};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(3d) failed (code " + std::to_string(int(r)) + ")");
+    return map;
 }
+
+static int bn_index(int bn) { return bn == 64 ? 0 : bn == 128 ? 1 : 2; }
 
 void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
     if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
     if (!d_b) throw std::invalid_argument("null argument");
     if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
-    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, 256);
+    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n + 1, kRowAlign);
     const size_t need_bt = static_cast<size_t>(n_pad * k_pad);
-    if (!w.bt || need_bt > w.bt_cap || static_cast<size_t>(k_pad) > w.kpad_cap) {
+    if (!w.bt || need_bt > w.bt_cap || static_cast<size_t>(k_pad) > w.cs_cap) {
         if (w.bt) {
             cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
             cudaFree(w.bt);
-            cudaFree(w.cs_tile);
             cudaFree(w.cs);
             w.bt = nullptr;
-            w.cs_tile = nullptr;
             w.cs = nullptr;
         }
-        cuda_check(cudaMalloc(&w.bt, static_cast<size_t>(n_pad * k_pad)), "cudaMalloc(B')");
-        cuda_check(cudaMalloc(&w.cs_tile, static_cast<size_t>(kCsRows * k_pad)), "cudaMalloc(cs tile)");
+        cuda_check(cudaMalloc(&w.bt, need_bt), "cudaMalloc(B')");
         cuda_check(cudaMalloc(&w.cs, static_cast<size_t>(k_pad)), "cudaMalloc(cs)");
         w.bt_cap = need_bt;
-        w.kpad_cap = static_cast<size_t>(k_pad);
+        w.cs_cap = static_cast<size_t>(k_pad);
     }
     w.k = k;
     w.n = n;
     w.k_pad = k_pad;
     w.n_pad = n_pad;
-    cuda_check(cudaMemsetAsync(w.cs_tile, 0, static_cast<size_t>(kCsRows * k_pad), st), "cudaMemsetAsync");
     cuda_check(launch_encode_weight(d_b, k, n, ldb, w, st), "encode_weight_kernel");
-    const int bns[3] = {64, 128, 256};
-    for (int i = 0; i < 3; ++i)
-        w.map_b[i] = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, w.bt, k_pad, n_pad, k_pad, kBK, bns[i],
-                                 CU_TENSOR_MAP_SWIZZLE_128B);
-    w.map_cs = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, w.cs_tile, k_pad, kCsRows, k_pad, kBK, kCsRows,
-                           CU_TENSOR_MAP_SWIZZLE_128B);
+    for (int bn : {64, 128, 256})
+        w.map_b[bn_index(bn)] = make_map_kblocks(w.bt, static_cast<uint64_t>(n_pad), static_cast<uint64_t>(k_pad / kBK),
+                                                 kBK, static_cast<uint64_t>(n_pad * kBK), bn / 2, gemm_ks(bn));
 }
 
 GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
@@ -173,53 +184,48 @@ void read_encoded(const GemmWeight& w, int8_t* d_out, cudaStream_t st) {
     cuda_check(launch_read_encoded(w, d_out, st), "read_encoded_kernel");
 }
 
+void set_checksums(GemmWeight& w, const int8_t* d_cs, cudaStream_t st) {
+    cuda_check(launch_set_checksums(w, d_cs, st), "set_checksums_kernel");
+}
+
 void free_weight(GemmWeight* w) {
     if (!w) return;
     if (w->owns) {
         cudaFree(w->bt);
-        cudaFree(w->cs_tile);
         cudaFree(w->cs);
     }
     delete w;
 }
 
-// Pick the N tile and the split-K factor. Small-m GEMMs re-read A once per N tile and every CTA
-// must ingest its A and B' slabs through L2 -> SMEM, so the model minimises the bytes the busiest
-// SM moves (A slab + B' slab + partial C tile) times the number of waves, plus the L2 total.
+// Pick the N tile of the CTA pair. Cost model (cycles, per pair): waves x max(MMA issue, per-SM
+// operand ingest) with MMA issue floors measured on B200 for cta_group::2 kind::i8 (N=64: 46 cycles,
+// N=128: 64, N=256: 128 per K=32 step) and ~128 B/clk of TMA ingest per SM; plus the epilogue drain
+// of the last tile (TMA store ~31 B/clk/SM).
 GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault) {
-    (void)checked;
-    const int sms = device_sm_count();
-    const int64_t m_tiles = (m + kBM - 1) / kBM;
+    (void)fault;
+    const int pairs = std::max(1, device_sm_count() / 2);
+    const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t kb = k_pad / kBK;
-    if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn,splits" tuning override
-        int bn = 0, sp = 0;
-        if (std::sscanf(env, "%d,%d", &bn, &sp) == 2 && (bn == 64 || bn == 128 || bn == 256) && sp >= 1) {
-            if (!c_tma_ok || fault) sp = 1;
-            sp = static_cast<int>(std::min<int64_t>(sp, kb));
-            return {bn, sp, !c_tma_ok ? kEpiDirect : (sp > 1 ? kEpiTmaReduce : kEpiTmaStore)};
-        }
+    const int64_t ncols = checked ? n + 1 : n;
+    const int epi = c_tma_ok ? kEpiTmaStore : kEpiDirect;
+    if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn[,epi]" tuning override
+        int bn = 0, e = -1;
+        const int got = std::sscanf(env, "%d,%d", &bn, &e);
+        if (got >= 1 && (bn == 64 || bn == 128 || bn == 256))
+            return {bn, (got == 2 && e == kEpiNone) ? kEpiNone : epi};
     }
-    GemmTiling best{64, 1, c_tma_ok ? kEpiTmaStore : kEpiDirect};
+    GemmTiling best{64, epi};
     double best_cost = 1e300;
     for (int bn : {256, 128, 64}) {
-        const int64_t n_tiles = (n + bn - 1) / bn;
-        const int64_t tiles = m_tiles * n_tiles;
-        int64_t splits = 1;
-        if (c_tma_ok && !fault && (n % 4) == 0) {
-            splits = std::max<int64_t>(1, std::min<int64_t>(kb / 4, sms / std::max<int64_t>(tiles, 1)));
-        }
-        const int64_t kbps = (kb + splits - 1) / splits;
-        splits = (kb + kbps - 1) / kbps;
-        const int64_t ctas = tiles * splits;
-        const int64_t waves = (ctas + sms - 1) / sms;
-        const double per_cta = double(kBM) * kbps * kBK + double(bn) * kbps * kBK + double(kBM) * bn * 4.0;
-        const double l2_total = double(ctas) * per_cta;
-        const double cost = waves * per_cta / 100.0 + l2_total / 10000.0 + (bn < 256 ? 1.0 : 0.0);
-        if (cost < best_cost) {
+        const int64_t tiles = m_tiles * ((ncols + bn - 1) / bn);
+        const int64_t waves = (tiles + pairs - 1) / pairs;
+        const double mma = double(kb) * 4 * (bn == 64 ? 46 : bn == 128 ? 64 : 128);
+        const double ingest = double(kb) * (kBM * kBK + (bn / 2) * kBK) / 128.0;
+        const double epi_drain = double(kBM) * bn * 4 / 31.0;
+        const double cost = waves * std::max(mma, ingest) + epi_drain;
+        if (cost < best_cost * 0.97) {
             best_cost = cost;
             best.bn = bn;
-            best.splits = static_cast<int>(splits);
-            best.epi = !c_tma_ok ? kEpiDirect : (splits > 1 ? kEpiTmaReduce : kEpiTmaStore);
         }
     }
     return best;
@@ -232,8 +238,8 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (m > 0 && (!d_a || !d_c)) throw std::invalid_argument("null argument");
     if (lda < w.k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
     if (ldc < w.n) throw std::invalid_argument("abft_gemm: ldc < n");
-    if (checked && (!d_csum || !d_flags || !d_err_count)) throw std::invalid_argument("null argument");
-    if (m > (int64_t{1} << 31) - 1 || w.n > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too large");
+    if (checked && (!d_err_count || (m > 0 && (!d_csum || !d_flags)))) throw std::invalid_argument("null argument");
+    if (m > (int64_t{1} << 31) - 1 || w.n > (int64_t{1} << 31) - 2) throw std::invalid_argument("abft_gemm: too large");
     const bool has_fault = fault && fault->active;
     if (has_fault) {
         if (!checked) throw std::invalid_argument("abft_gemm: fault hook needs the checked kernel");
@@ -247,11 +253,12 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
 
-    // A must be a TMA-legal 2D tensor: 16-byte aligned base and pitch. Otherwise repack once.
+    // A is read through a 3D view {128 B, rows, k-blocks}: base and pitch must be 16-byte aligned and
+    // the last (partial) k-block must stay inside the allocation. Otherwise repack into scratch.
     const uint8_t* a = d_a;
     int64_t a_ld = lda;
-    if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0) {
-        a_ld = round_up(w.k, 16);
+    if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0 || (w.k % kBK != 0 && lda < w.k_pad)) {
+        a_ld = w.k_pad;
         const size_t need = static_cast<size_t>(a_ld * m);
         if (need > ws.scratch_cap) {
             if (ws.scratch) {
@@ -267,16 +274,13 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     }
     const bool c_tma_ok = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0;
     GemmTiling t = force ? *force : choose_tiling(m, w.n, w.k_pad, checked, c_tma_ok, has_fault);
-    if (!c_tma_ok) t.epi = kEpiDirect;
-    if (t.epi == kEpiDirect || has_fault || (w.n % 4) != 0) t.splits = 1;
-    if (t.splits == 1 && t.epi == kEpiTmaReduce) t.epi = kEpiTmaStore;
-    if (t.splits > 1) t.epi = kEpiTmaReduce;
+    if (!c_tma_ok && t.epi != kEpiNone) t.epi = kEpiDirect;
 
-    const int64_t m_tiles = (m + kBM - 1) / kBM;
-    const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
+    const int64_t m_tiles = (m + kPairM - 1) / kPairM;
+    const int64_t ncols = checked ? w.n + 1 : w.n;
+    const int64_t n_tiles = (ncols + t.bn - 1) / t.bn;
     const int64_t kb = w.k_pad / kBK;
-    const int64_t kbps = (kb + t.splits - 1) / t.splits;
-    const int64_t splits = (kb + kbps - 1) / kbps;
+    if (m_tiles * n_tiles > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
 
     if (checked && m > ws.rows_cap) {
         int64_t cap_a = ws.rows_cap, cap_b = ws.rows_cap;  // row_res and csum_acc share one capacity
@@ -284,17 +288,15 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         grow(ws.csum_acc, cap_b, m, st);
         ws.rows_cap = std::min(cap_a, cap_b);
     }
-    grow(ws.mtile_cnt, ws.mtiles_cap, m_tiles, st);
-    if (t.splits > 1) grow(ws.tile_flag, ws.tiles_cap, m_tiles * n_tiles, st);
+    if (checked) grow(ws.half_cnt, ws.halves_cap, 2 * m_tiles, st);
 
     GemmParams p{};
     p.m = static_cast<int>(m);
     p.n = static_cast<int>(w.n);
     p.k_blocks = static_cast<int>(kb);
-    p.kb_per_split = static_cast<int>(kbps);
     p.n_tiles = static_cast<int>(n_tiles);
     p.m_tiles = static_cast<int>(m_tiles);
-    p.splits = static_cast<int>(splits);
+    p.num_tiles = static_cast<int>(m_tiles * n_tiles);
     p.c = d_c;
     p.ldc = ldc;
     p.csum = d_csum;
@@ -303,26 +305,25 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.err_count = d_err_count;
     p.row_res = ws.row_res;
     p.csum_acc = ws.csum_acc;
-    p.mtile_cnt = ws.mtile_cnt;
+    p.half_cnt = ws.half_cnt;
     p.err_acc = ws.small + 0;
     p.done_cnt = ws.small + 1;
-    p.tile_flag = ws.tile_flag;
-    p.epoch = ++ws.epoch;
+    p.trace = g_trace;
     if (has_fault) {
         p.fault_active = 1;
         p.fault_row = static_cast<int>(fault->row);
         p.fault_col = static_cast<int>(fault->col);
         p.fault_bit = static_cast<int>(fault->bit);
     }
-    const CUtensorMap map_a =
-        make_map_2d(CU_TENSOR_MAP_DATA_TYPE_UINT8, a, w.k, m, a_ld, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap map_a = make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
+                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_ks(t.bn));
     CUtensorMap map_c;
     std::memset(&map_c, 0, sizeof(map_c));
-    if (t.epi != kEpiDirect)
+    if (t.epi == kEpiTmaStore)
         map_c = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_INT32, d_c, w.n, m, ldc * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    const dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(m_tiles), static_cast<unsigned>(splits));
-    cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, grid, map_a, weight_map(w, t.bn), w.map_cs, map_c, p, st),
-               "gemm_u8s8_kernel");
+    const int pairs = static_cast<int>(std::min<int64_t>(p.num_tiles, std::max(1, device_sm_count() / 2)));
+    cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
+               "gemm_pair_kernel");
 }
 
 void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum_ld, int64_t m, int64_t n,

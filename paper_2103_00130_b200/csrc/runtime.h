@@ -21,6 +21,7 @@ GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, 
 void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st);
 // Logical k x (n+1) [B | cs] matrix, row-major (PackedEncodedWeight::at contract).
 void read_encoded(const GemmWeight& w, int8_t* d_out, cudaStream_t st);
+void set_checksums(GemmWeight& w, const int8_t* d_cs, cudaStream_t st);
 void free_weight(GemmWeight* w);
 GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault);
 // checked == false: plain GEMM (csum/flags/err_count ignored).
@@ -54,9 +55,8 @@ void gen(void* d_out, int64_t count, uint64_t seed, uint64_t stream, uint64_t of
 void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
 
 // ---- launchers implemented in the .cu files
-cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, dim3 grid, const CUtensorMap& a, const CUtensorMap& b,
-                               const CUtensorMap& cs, const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
-int gemm_stages(int bn, bool checked);
+cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b,
+                               const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st);
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st);
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,
@@ -95,5 +95,6 @@ struct SplitMix64 {
 };
 
 int device_sm_count();
+void set_gemm_trace(unsigned long long* d_trace);  // debug instrumentation (nullptr = off)
 
 }  // namespace abftk

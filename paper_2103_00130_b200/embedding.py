@@ -1,0 +1,246 @@
+"""Host mirror of the reference's checked EmbeddingBag API (P:src/embedding_abft.hpp:12-52).
+
+Tables live on the GPU: 8-bit signed rows (the reference's type), plus the BASELINE variants
+uint8 and packed 4-bit rows, with fp32 or fp16 per-row scale/bias. Lookups run in the
+warp-per-bag kernel through the C ABI; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import device, ptr, stream_handle, to_device
+
+kEbRelativeBound = 1e-5
+ELEM = {"s8": 0, "u8": 1, "u4": 2}
+SCALE = {"f32": 0, "f16": 1}
+
+
+@dataclass
+class IndexBag:
+    """Multiset of row indices with optional per-lookup weights (P:src/embedding_abft.hpp:24-27)."""
+    indices: Sequence[int] = field(default_factory=list)
+    weights: Optional[Sequence[float]] = None
+
+
+@dataclass
+class EbCheckedResult:
+    """Pooled vector (fp32), the fp64 sums used by the check, and the verdict (P:src/embedding_abft.hpp:29-34)."""
+    r: torch.Tensor
+    rSum: float
+    cSum: float
+    err: bool
+
+
+class QuantEmbeddingTable:
+    """Row-wise quantized table with per-row scale/bias and device-computed int32 row sums.
+
+    ``rows``: R x row_bytes (row_bytes = d for s8/u8, d/2 for u4; element j of a u4 row is
+    (byte[j/2] >> 4*(j&1)) & 0xF). The rows are kept alive by this object (the C ABI borrows
+    them). ``row_sums`` overrides the computed sums (stale-sum experiments,
+    load_table(validate=False) semantics).
+    """
+
+    def __init__(self, rows, scales, biases, elem: str = "s8", dim: int | None = None, row_sums=None,
+                 scale_dtype: str | None = None, stream=None):
+        if elem not in ELEM:
+            raise ValueError(f"unknown element type {elem!r}")
+        rt = to_device(rows, torch.int8 if elem == "s8" else torch.uint8, ndim=2)
+        R, row_bytes = (int(s) for s in rt.shape)
+        if dim is None:
+            dim = row_bytes * 2 if elem == "u4" else row_bytes
+        if scale_dtype is None:
+            scale_dtype = "f16" if (isinstance(scales, torch.Tensor) and scales.dtype == torch.float16) or \
+                (isinstance(scales, np.ndarray) and scales.dtype == np.float16) else "f32"
+        sdt = torch.float16 if scale_dtype == "f16" else torch.float32
+        st = to_device(scales, sdt)
+        bt = to_device(biases, sdt)
+        if st.numel() != R or bt.numel() != R:
+            raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "table: scale/bias length mismatch")
+        rs = None
+        if row_sums is not None:
+            rs = to_device(row_sums, torch.int32)
+            if rs.numel() != R:
+                raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "table: row-sum length mismatch")
+        h = C.c_void_p()
+        _lib.call("abftlp_eb_table_create", ELEM[elem], ptr(rt) if rt.numel() else C.c_void_p(1), R, dim, row_bytes,
+                  SCALE[scale_dtype], ptr(st) if R else C.c_void_p(1), ptr(bt) if R else C.c_void_p(1), ptr(rs),
+                  stream_handle(stream), C.byref(h))
+        self._h = h
+        self.rows, self.scales, self.biases, self._given_sums = rt, st, bt, rs
+        self.elem, self.scale_dtype = elem, scale_dtype
+        self._R, self._d = R, int(dim)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib.abftlp_eb_table_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def numRows(self) -> int:
+        return self._R
+
+    def dim(self) -> int:
+        return self._d
+
+    @property
+    def rowSums(self) -> torch.Tensor:
+        """Stored row sums (the given ones if supplied, else the device-computed ones)."""
+        if self._given_sums is not None:
+            return self._given_sums
+        out = torch.empty(self._R, dtype=torch.int32, device=device())
+        _lib.call("abftlp_eb_table_row_sums", self._h, ptr(out), stream_handle())
+        return out
+
+    def validate(self) -> int:
+        """Rows whose stored sum disagrees with the contents (0 when sums were computed here)."""
+        if self._given_sums is None:
+            return 0
+        out = C.c_uint64()
+        _lib.call("abftlp_eb_table_validate", self._h, ptr(self._given_sums), stream_handle(), C.byref(out))
+        return int(out.value)
+
+    def flip_bit(self, row: int, col: int, bit: int, stream=None) -> None:
+        """Corrupt element (row, col) after the row sums were taken (inject_eb_table's point)."""
+        _lib.call("abftlp_eb_table_flip_bit", self._h, row, col, bit, stream_handle(stream))
+
+
+def precompute_row_sums(rows, elem: str = "s8", dim: int | None = None) -> torch.Tensor:
+    """int32 per-row element sums (P:src/embedding_abft.cpp:39-45), computed on the device."""
+    rt = to_device(rows, torch.int8 if elem == "s8" else torch.uint8, ndim=2)
+    R = int(rt.shape[0])
+    if R == 0:
+        return torch.zeros(0, dtype=torch.int32, device=device())
+    ones = torch.ones(R, dtype=torch.float32, device=device())
+    return QuantEmbeddingTable(rt, ones, torch.zeros_like(ones), elem=elem, dim=dim).rowSums
+
+
+def _csr(bags: Sequence[IndexBag]):
+    lens = [len(b.indices) for b in bags]
+    offsets = np.zeros(len(bags) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offsets[1:])
+    idx = np.concatenate([np.asarray(b.indices, dtype=np.uint64).astype(np.int64) for b in bags]) if bags and \
+        offsets[-1] else np.zeros(0, dtype=np.int64)
+    weighted = any(b.weights is not None for b in bags)
+    w = None
+    if weighted:
+        parts = []
+        for b in bags:
+            if b.weights is not None:
+                if len(b.weights) != len(b.indices):
+                    raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "embedding_bag: weights length mismatch")
+                parts.append(np.asarray(b.weights, dtype=np.float32))
+            else:  # 1.0f weights are bit-identical to the unweighted path (P:tests/test_embedding_abft.cpp:120-132)
+                parts.append(np.ones(len(b.indices), dtype=np.float32))
+        w = np.concatenate(parts) if parts else np.zeros(0, np.float32)
+    return offsets, idx, w
+
+
+def eb_csr(table: QuantEmbeddingTable, offsets, indices, weights=None, checked: bool = True, stream=None):
+    """Pooled lookups over CSR bags in one launch. Returns (out[B, d], flags[B], rsum[B], csum[B],
+    flag_count) as device tensors (flags/sums/count are None when unchecked)."""
+    off = to_device(offsets, torch.int64)
+    idx = to_device(indices, torch.int64)
+    w = None if weights is None else to_device(weights, torch.float32)
+    nb = int(off.numel()) - 1
+    d = table.dim()
+    dev = device()
+    out = torch.zeros((max(nb, 0), d), dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    if checked:
+        flags = torch.zeros(max(nb, 0), dtype=torch.uint8, device=dev)
+        rsum = torch.zeros(max(nb, 0), dtype=torch.float64, device=dev)
+        csum = torch.zeros(max(nb, 0), dtype=torch.float64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("abftlp_eb_checked", table.handle, ptr(off), ptr(idx) if idx.numel() else C.c_void_p(8), nb, ptr(w),
+                  ptr(out), d, ptr(flags), ptr(rsum), ptr(csum), ptr(cnt), ptr(status), stream_handle(stream))
+    else:
+        flags = rsum = csum = cnt = None
+        _lib.call("abftlp_eb_unchecked", table.handle, ptr(off), ptr(idx) if idx.numel() else C.c_void_p(8), nb,
+                  ptr(w), ptr(out), d, ptr(status), stream_handle(stream))
+    if int(status.item()) & 1:
+        raise IndexError("embedding_bag: index out of range")
+    return out, flags, rsum, csum, cnt
+
+
+def embedding_bag(table: QuantEmbeddingTable, bag: IndexBag) -> torch.Tensor:
+    """Plain pooled lookup, fp32 accumulation (P:src/embedding_abft.cpp:47-60)."""
+    off, idx, w = _csr([bag])
+    return eb_csr(table, off, idx, w, checked=False)[0][0]
+
+
+def batch_abft_eb(table: QuantEmbeddingTable, bags: Sequence[IndexBag]) -> list[EbCheckedResult]:
+    """Independent checked lookups for every bag, one kernel launch (P:src/embedding_abft.cpp:85-91)."""
+    if not bags:
+        return []
+    off, idx, w = _csr(bags)
+    out, flags, rsum, csum, _ = eb_csr(table, off, idx, w, checked=True)
+    f, rs, cs = flags.cpu().numpy(), rsum.cpu().numpy(), csum.cpu().numpy()
+    return [EbCheckedResult(out[b], float(rs[b]), float(cs[b]), bool(f[b])) for b in range(len(bags))]
+
+
+def abft_embedding_bag(table: QuantEmbeddingTable, bag: IndexBag) -> EbCheckedResult:
+    """Lookup plus the row-sum check at the 1e-5 relative bound (P:src/embedding_abft.cpp:62-83)."""
+    return batch_abft_eb(table, [bag])[0]
+
+
+# ---------------------------------------------------------------- ABEB files (P:src/embedding_abft.cpp:93-145)
+_MAGIC = b"ABEB"
+
+
+def save_table(table: QuantEmbeddingTable, path: str) -> None:
+    """Binary container: "ABEB", u16 version 1, u64 R, u32 d, R x (d int8, f32 scale, f32 bias), R x i32."""
+    if table.elem != "s8" or table.scale_dtype != "f32":
+        raise ValueError("ABEB stores int8 rows with fp32 scale/bias")
+    rows = table.rows.cpu().numpy().view(np.int8)
+    sc = table.scales.cpu().numpy().astype(np.float32)
+    bi = table.biases.cpu().numpy().astype(np.float32)
+    sums = table.rowSums.cpu().numpy().astype(np.int32)
+    R, d = rows.shape
+    rec = np.zeros(R, dtype=[("q", np.int8, (d,)), ("s", "<f4"), ("b", "<f4")])
+    rec["q"], rec["s"], rec["b"] = rows, sc, bi
+    try:
+        with open(path, "wb") as f:
+            f.write(_MAGIC + struct.pack("<HQI", 1, R, d))
+            f.write(rec.tobytes())
+            f.write(sums.astype("<i4").tobytes())
+    except OSError as e:
+        raise _lib.IoError(_lib.ERR_IO, f"cannot open table file for writing: {path}") from e
+
+
+def load_table(path: str, validateRowSums: bool = True) -> QuantEmbeddingTable:
+    """Load an ABEB file onto the device; validation recomputes the sums on the GPU."""
+    try:
+        with open(path, "rb") as f:
+            blob = f.read()
+    except OSError as e:
+        raise _lib.IoError(_lib.ERR_IO, f"cannot open table file: {path}") from e
+    if len(blob) < 4 or blob[:4] != _MAGIC:
+        raise _lib.IoError(_lib.ERR_IO, f"not an embedding table file: {path}")
+    if len(blob) < 18:
+        raise _lib.IoError(_lib.ERR_IO, "table file truncated")
+    ver, R, d = struct.unpack_from("<HQI", blob, 4)
+    if ver != 1:
+        raise _lib.IoError(_lib.ERR_IO, "unsupported table file version")
+    if R == 0 or d == 0:
+        raise _lib.IoError(_lib.ERR_IO, "table file has empty dimensions")
+    need = 18 + R * (d + 8) + 4 * R
+    if len(blob) < need:
+        raise _lib.IoError(_lib.ERR_IO, "table file truncated")
+    rec = np.frombuffer(blob, dtype=[("q", np.int8, (d,)), ("s", "<f4"), ("b", "<f4")], count=R, offset=18)
+    sums = np.frombuffer(blob, dtype="<i4", count=R, offset=18 + R * (d + 8))
+    t = QuantEmbeddingTable(np.ascontiguousarray(rec["q"]), np.ascontiguousarray(rec["s"]),
+                            np.ascontiguousarray(rec["b"]), elem="s8", row_sums=sums.copy())
+    if validateRowSums and t.validate() != 0:
+        raise _lib.IoError(_lib.ERR_IO, "table row-sum checksums do not match contents")
+    return t
