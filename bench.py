@@ -1,0 +1,448 @@
+#!/usr/bin/env python3
+"""Benchmark driver (one JSON line on rank 0).
+
+Headline workload = BASELINE.json configs[1] ("G2"): checked int8 GEMM m=256, k=4096, n=4096,
+A u8 U[0,255], B s8 U[-128,127] (SplitMix64, the reference's draw protocol), B encoded ONCE and
+reused for a job of 1000 GEMMs with distinct A matrices; 1% of the runs inject one random bit
+flip (half into B' after encoding, half into C' through the epilogue hook) and every injected
+run must be flagged. One step = one such job; L2 is flushed between steps (a 256 MiB write).
+metric = checked int8 GEMM TOPS (2*m*n*k per GEMM, checksum column excluded).
+
+Secondary lines in the same JSON object: ABFT overhead vs the same kernel with checking compiled
+out, the cold single-GEMM latency, and the EmbeddingBag configs E3 (4M x 128 u8, Zipf bags) and
+E4 (8M x 64 int4 + fp16, weighted) in algorithmic HBM GB/s.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled from the
+reference sources) on all host cores for the same metric; it falls back to the C restatement
+(oracle/liboracle.so) when the reference build is absent.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+M, N, K = 256, 4096, 4096
+JOB = 1000
+SEED = 20260823
+OPS = 2 * M * N * K
+ALG_BYTES = M * K + K * (N + 1) + 4 * M * (N + 1) + M  # A, B' (incl. checksum column), C', flags
+
+
+def peaks():
+    p = {"hbm_gbs": 6446.6, "bf16_tflops": 1674.8, "source": "fallback (B200_PROFILING.md)"}
+    f = REPO / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        p = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "MEASURED_PEAKS.json"}
+    # No int8 peak is measured by the driver: use 2x the measured bf16 dense burst.
+    p["int8_tops"] = 2 * p["bf16_tflops"]
+    return p
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self):
+        self.samples, self.proc, self.thread = [], None, None
+
+    def start(self, dev_index: int):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(dev_index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm (CPU)
+def cpu_gemm_sample(threads: int, reps: int = 1):
+    """`threads` concurrent checked GEMMs at the G2 shape through the reference's abft_gemm
+    (pre-encoded weight, as the job encodes B once). Returns (TOPS, kind, seconds)."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+    a, b = O.gemm_inputs(SEED, 0, M, N, K)
+    R = O.ref()
+    kind = "reference" if R is not None else "port"
+    outs = [np.empty((M, N + 1), np.int32) for _ in range(threads)]
+    if R is not None:
+        w = R.ref_gemm_weight_new(O.P(b), O.sz(K), O.sz(N))
+
+        def one(i):
+            err = C.c_uint64()
+            R.ref_abft_gemm_w(O.P(a), O.sz(M), O.sz(K), C.c_void_p(w), O.P(outs[i]), C.byref(err))
+    else:
+        cs = O.row_checksums(b)
+
+        def one(i):
+            err = C.c_uint64()
+            O.orc().orc_abft_gemm(O.P(a), O.sz(M), O.sz(K), O.P(b), O.sz(N), O.P(cs), O.P(outs[i]), None,
+                                  C.byref(err))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ths = [threading.Thread(target=one, args=(i,)) for i in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    dt = time.perf_counter() - t0
+    if R is not None:
+        R.ref_gemm_weight_free(C.c_void_p(w))
+    return threads * reps * OPS / dt / 1e12, kind, dt
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_gemm_sample(threads)
+    times = []
+    for _ in range(args.steps):
+        tops, kind, dt = cpu_gemm_sample(threads)
+        times.append(dt)
+    total = sum(times)
+    value = args.steps * threads * OPS / total / 1e12
+    line = {"metric": "checked int8 GEMM TOPS", "value": value, "unit": "TOPS", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
+            "data": "synthetic (SplitMix64, the reference's draw protocol)",
+            "config": {"workload": "G2: checked GEMM m=256 k=4096 n=4096 (BASELINE configs[1]); one step = "
+                                   f"{threads} concurrent abft_gemm calls (one per host thread) on a pre-encoded B"},
+            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": threads, "kind": kind,
+                             "sample": f"{threads} G2 GEMMs per step on {threads} threads"},
+            "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu_arm(args, rank, world, dist):
+    import torch
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200.rng import SplitMix64
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream()
+    st = C.c_void_p(stream.cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    pk = peaks()
+    launches = 0
+
+    # ---- inputs resident in HBM before timing: B encoded once; JOB distinct A matrices
+    # Rank r owns the N-column shard r of a (N * world)-wide weight (weak scaling; no data-path
+    # collective -- only the per-run verdicts are OR-reduced across ranks at the end of a step).
+    b = torch.empty((K, N), dtype=torch.int8, device=dev)
+    L.call("abftlp_generate", vp(b), K * N, SEED, 1000 + rank, 0, 1, 0.0, 0.0, 0, st)
+    w = C.c_void_p()
+    L.call("abftlp_gemm_encode", vp(b), K, N, N, st, C.byref(w))
+    a_pool = torch.empty((JOB, M, K), dtype=torch.uint8, device=dev)
+    L.call("abftlp_generate", vp(a_pool), JOB * M * K, SEED, 0, 0, 0, 0.0, 0.0, 0, st)
+    n_cbuf = 8
+    c_ring = torch.empty((n_cbuf, M, N), dtype=torch.int32, device=dev)
+    csum = torch.empty((JOB, M), dtype=torch.int32, device=dev)
+    flags = torch.empty((JOB, M), dtype=torch.uint8, device=dev)
+    errs = torch.zeros(JOB, dtype=torch.int32, device=dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # 1% of the runs carry a fault: even ones flip a bit of B' (j < n, bit 0..7) before the GEMM and
+    # undo it after; odd ones flip a bit of C' (any column incl. the checksum, bit 0..31) in the epilogue.
+    rng = SplitMix64(SEED, 7 + rank)
+    fault_runs = sorted({rng.next_below(JOB) for _ in range(JOB // 100 * 3)})[: JOB // 100]
+    plan = {}
+    for idx, run in enumerate(fault_runs):
+        if idx % 2 == 0:
+            plan[run] = ("B", rng.next_below(K), rng.next_below(N), rng.next_below(8))
+        else:
+            plan[run] = ("C", rng.next_below(M), rng.next_below(N + 1), rng.next_below(32))
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(JOB)]
+
+    def job(checked=True, record=False):
+        nonlocal launches
+        for i in range(JOB):
+            f = plan.get(i)
+            fault = None
+            if f and f[0] == "B":
+                L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
+                launches += 1
+            elif f and f[0] == "C" and checked:
+                fault = C.byref(L.Fault(1, f[1], f[2], f[3]))
+            if record:
+                ev[i][0].record(stream)
+            c = c_ring[i % n_cbuf]
+            if checked:
+                L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c), N, vp(csum[i]), 1, vp(flags[i]),
+                       vp(errs[i:i + 1]), fault, st)
+            else:
+                L.call("abftlp_gemm_unchecked", vp(a_pool[i]), M, K, w, vp(c), N, st)
+            launches += 1
+            if record:
+                ev[i][1].record(stream)
+            if f and f[0] == "B":
+                L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
+                launches += 1
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(fn, steps, flush=True):
+        total, per = 0.0, []
+        for s in range(steps):
+            if flush:
+                L.call("abftlp_l2_flush", vp(flush_buf), flush_buf.numel(), s, st)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            barrier()
+            ms = e0.elapsed_time(e1)
+            if dist is not None:
+                t = torch.tensor([ms], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            per.append(ms)
+            total += ms
+        return total, per
+
+    # ---- warm-up (also compiles/caches tensor maps, workspaces)
+    for _ in range(args.warmup):
+        job(True)
+        job(False)
+    barrier()
+
+    clocks = Clocks()
+    clocks.start(dev.index)
+    launches = 0
+    t_total, t_steps = timed(lambda: job(True, record=True), args.steps)
+    kernel_us = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) * 1e3 for i in range(JOB) if i not in plan)
+    launches_timed = launches + args.steps  # + the L2 flush kernel before each step
+    clk = clocks.stop()
+
+    # parity of the job's verdicts: every injected run flagged, no clean run flagged
+    e = errs.cpu().numpy()
+    ok_clean = all(e[i] == 0 for i in range(JOB) if i not in plan)
+    c_runs = [r for r, f in plan.items() if f[0] == "C"]
+    b_runs = [r for r, f in plan.items() if f[0] == "B"]
+    ok_c = all(e[r] == 1 for r in c_runs)
+    ok_b = all(e[r] >= 1 for r in b_runs)
+    verdict = torch.tensor(e, device=dev)
+    if dist is not None:
+        dist.all_reduce(verdict, op=dist.ReduceOp.MAX)  # OR of the per-shard verdicts
+    # unchecked baseline (same kernel, checking compiled out) for the ABFT overhead
+    u_total, _ = timed(lambda: job(False), args.steps)
+
+    # ---- cold single GEMM (L2 flushed before each launch), kernel-only
+    cold = []
+    for s in range(10):
+        L.call("abftlp_l2_flush", vp(flush_buf), flush_buf.numel(), 100 + s, st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.call("abftlp_gemm_checked", vp(a_pool[s]), M, K, w, vp(c_ring[0]), N, vp(csum[0]), 1, vp(flags[0]),
+               vp(errs[0:1]), None, st)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cold.append(e0.elapsed_time(e1) * 1e3)
+
+    # ---- e2e: the same job through the host-buffer C-ABI call (pinned A in, C/csum/flags/count out)
+    e2e_runs = 100
+    a_host = torch.empty((M, K), dtype=torch.uint8).pin_memory()
+    a_host.copy_(a_pool[0].cpu())
+    c_host = torch.empty((M, N), dtype=torch.int32).pin_memory()
+    cs_host = torch.empty(M, dtype=torch.int32).pin_memory()
+    fl_host = torch.empty(M, dtype=torch.uint8).pin_memory()
+    ec = C.c_uint32()
+
+    def e2e_job():
+        for _ in range(e2e_runs):
+            L.call("abftlp_gemm_checked_host", C.c_void_p(a_host.data_ptr()), M, K, w, C.c_void_p(c_host.data_ptr()),
+                   N, C.c_void_p(cs_host.data_ptr()), C.c_void_p(fl_host.data_ptr()), C.byref(ec), st)
+    e2e_job()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_job()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_tops = world * e2e_runs * OPS / e2e_s / 1e12
+
+    secondary = eb_secondary(L, dev, st, vp, pk) if (rank == 0 and not args.no_eb) else None
+
+    L.lib.abftlp_gemm_weight_free(w)
+    if rank != 0:
+        return
+    value = world * args.steps * JOB * OPS / (t_total * 1e-3) / 1e12
+    achieved = OPS / (kernel_us * 1e-6) / 1e12
+    line = {
+        "metric": "checked int8 GEMM TOPS", "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8xs8->s32",
+        "data": "synthetic (SplitMix64, the reference's draw protocol); no dataset",
+        "config": {"workload": "G2 = BASELINE configs[1]: checked GEMM m=256 k=4096 n=4096, B encoded once, "
+                               f"job of {JOB} GEMMs with distinct A, 1% fault runs (B' and C' bit flips)",
+                   "step": f"one {JOB}-GEMM job", "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": f"N-column shard per GPU (n={N} per rank), verdicts OR-reduced",
+                   "gemm_kernel": "tcgen05 cta_group::2 int8, TMEM accumulators, fused mod-127 row check"},
+        "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": M * K * e2e_runs,
+                "d2h_bytes_per_step": (4 * M * N + 4 * M + M + 4) * e2e_runs,
+                "note": f"{e2e_runs} abftlp_gemm_checked_host calls (pinned host A in; C, csum, flags, count out)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["int8_tops"], "unit": "TOP/s",
+                     "frac": achieved / pk["int8_tops"], "traffic": None,
+                     "kernel": "gemm_pair_kernel (checked)", "kernel_us": kernel_us,
+                     "ops_per_launch": OPS, "alg_bytes_per_launch": ALG_BYTES,
+                     "peak_source": f"2 x bf16 burst from {pk['source']}",
+                     "note": "B' stays L2-resident across the job, so the per-launch bound is tensor, not HBM"},
+        "cold_gemm": {"us_median": statistics.median(cold), "alg_gbs": ALG_BYTES / (statistics.median(cold) * 1e-6) / 1e9,
+                      "hbm_frac": ALG_BYTES / (statistics.median(cold) * 1e-6) / 1e9 / pk["hbm_gbs"],
+                      "note": "single checked GEMM with L2 flushed (B' from HBM)"},
+        "abft_overhead_pct": 100.0 * (t_total - u_total) / u_total,
+        "parity": {"clean_runs_unflagged": bool(ok_clean), "c_faults_flagged": bool(ok_c),
+                   "b_faults_flagged": bool(ok_b), "fault_runs": len(plan)},
+        "gpu_launches": launches_timed,
+        "clocks": clk,
+    }
+    if secondary:
+        line["secondary"] = secondary
+    if not args.no_cpu and world == 1:
+        threads = os.cpu_count() or 1
+        tops, kind, dt = cpu_gemm_sample(threads)
+        line["cpu_baseline"] = {"value": tops, "unit": "TOPS", "cores": threads, "kind": kind,
+                                "sample": f"{threads} concurrent G2 abft_gemm calls ({dt:.1f} s wall)"}
+    print(json.dumps(line), flush=True)
+
+
+def eb_secondary(L, dev, st, vp, pk):
+    """E3 / E4 checked EmbeddingBag: algorithmic HBM GB/s (every lookup counted), L2 flushed per step."""
+    import torch
+    out = {}
+    rng = np.random.default_rng(3)
+    for name in ("E3", "E4"):
+        if name == "E3":
+            R, d, nb, elem, st_t, meta_b = 4_000_000, 128, 2048, 1, 0, 12
+            lens = rng.integers(20, 101, nb)
+            ranks = np.arange(1, R + 1, dtype=np.float64)
+            cdf = np.cumsum(ranks ** -1.05)
+            cdf /= cdf[-1]
+            perm = rng.permutation(R)
+            idx = perm[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+            wts = None
+            row_b = d
+        else:
+            R, d, nb, elem, st_t, meta_b = 8_000_000, 64, 4096, 2, 1, 8
+            lens = rng.integers(1, 151, nb)
+            idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
+            wts = torch.from_numpy(rng.uniform(0, 1, int(lens.sum())).astype(np.float32)).to(dev)
+            row_b = d // 2
+        rows = torch.randint(0, 256, (R, row_b), dtype=torch.uint8, device=dev)
+        sdt = torch.float32 if st_t == 0 else torch.float16
+        sc = (torch.rand(R, device=dev) * 9e-3 + 1e-3).to(sdt)
+        bi = (torch.rand(R, device=dev) * 2 - 1).to(sdt)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)).to(dev)
+        ix = torch.from_numpy(idx).to(dev)
+        tab = C.c_void_p()
+        L.call("abftlp_eb_table_create", elem, vp(rows), R, d, row_b, st_t, vp(sc), vp(bi), None, st, C.byref(tab))
+        o = torch.empty((nb, d), dtype=torch.float32, device=dev)
+        fl = torch.empty(nb, dtype=torch.uint8, device=dev)
+        fb = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        L_ = int(lens.sum())
+        alg = L_ * (row_b + meta_b + 4 + 8 + (4 if wts is not None else 0)) + 8 * (nb + 1) + 4 * nb * d + nb
+        res = {}
+        for checked in (True, False):
+            ts = []
+            for s in range(8):
+                L.call("abftlp_l2_flush", vp(fb), fb.numel(), s, st)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                if checked:
+                    L.call("abftlp_eb_checked", tab, vp(off), vp(ix), nb, vp(wts) if wts is not None else None,
+                           vp(o), d, vp(fl), None, None, None, None, st)
+                else:
+                    L.call("abftlp_eb_unchecked", tab, vp(off), vp(ix), nb, vp(wts) if wts is not None else None,
+                           vp(o), d, None, st)
+                e1.record()
+                torch.cuda.synchronize()
+                if s >= 2:
+                    ts.append(e0.elapsed_time(e1) * 1e3)
+            res[checked] = statistics.median(ts)
+        L.lib.abftlp_eb_table_free(tab)
+        gbs = alg / (res[True] * 1e-6) / 1e9
+        out[name] = {"checked_us": res[True], "unchecked_us": res[False], "alg_bytes": alg, "alg_gbs": gbs,
+                     "hbm_frac": gbs / pk["hbm_gbs"], "overhead_pct": 100 * (res[True] - res[False]) / res[False],
+                     "lookups": L_, "bags": nb}
+        del rows, sc, bi, off, ix, o, fl, fb
+        torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-eb", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    run_gpu_arm(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
