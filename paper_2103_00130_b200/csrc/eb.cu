@@ -1,18 +1,21 @@
-// ABFT EmbeddingBag for sm_100a: warp-per-bag checked / unchecked pooled lookups and the
-// row-sum encoder.
+// ABFT EmbeddingBag for sm_100a: checked / unchecked pooled lookups and the row-sum encoder.
 //
 //   eb_meta_kernel  replaces precompute_row_sums (P:src/embedding_abft.cpp:39-45) and packs the
 //                   per-row (scale, bias, rowSum) into one 16-B (fp32) or 8-B (fp16) record so a
 //                   lookup touches one metadata sector.
 //   eb_bag_kernel   replaces embedding_bag / abft_embedding_bag / batch_abft_eb
-//                   (P:src/embedding_abft.cpp:47-91). Lane l owns a fixed column slice, so every
-//                   output column is accumulated sequentially in bag order with the reference's
-//                   exact fp32 operation order (scale*q, +bias, *w, +=; no FMA contraction).
-//                   The row loads of up to 32 lookups are issued before any is consumed, so each
-//                   warp keeps 32 row-gathers in flight. cSum is the reference's sequential fp64
-//                   chain; rSum is computed by a warp tree when every partial sum is provably
-//                   exact in fp64 (then the order cannot matter) and by the reference's sequential
-//                   order otherwise -- bit-identical either way.
+//                   (P:src/embedding_abft.cpp:47-91). A bag is processed by WPB warps, each owning
+//                   a contiguous slice of the columns; lane l of a warp owns CPL columns of the slice.
+//                   Every output column is therefore accumulated sequentially in bag order with the
+//                   reference's exact fp32 operation order (scale*q, +bias, *w, +=; no FMA), which is
+//                   what makes the pooled vector bit-identical. Lookups are processed in chunks of 32:
+//                   the chunk's row offsets / scale / bias / weight are staged in shared memory
+//                   (broadcast reads), the 32 row gathers are issued before any is consumed, the
+//                   next chunk's indices are prefetched while the current one accumulates, and the
+//                   cSum terms w*(scale*rowSum + d*bias) are formed lane-parallel so only the fp64
+//                   additions stay sequential (as in the reference, P:src/embedding_abft.cpp:69-76).
+//                   rSum is computed order-free when every partial sum is provably exact in fp64 and
+//                   in the reference's sequential order otherwise -- bit-identical either way.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -99,27 +102,213 @@ __device__ __forceinline__ void bit_span(float v, int& emax, int& umin) {
     umin = min(umin, lo);
 }
 
+__device__ __forceinline__ double csum_term(float s, float b, int32_t rs, float w, double dd, bool weighted) {
+    double term = __dadd_rn(__dmul_rn(static_cast<double>(s), static_cast<double>(rs)), __dmul_rn(dd, static_cast<double>(b)));
+    if (weighted) term = __dmul_rn(static_cast<double>(w), term);
+    return term;
+}
+
 }  // namespace
 
-// CPL > 0: lane owns columns [lane*CPL, lane*CPL+CPL) (d == 32*CPL).
-// CPL == 0: generic layout, lane owns columns lane + 32*c (c < kGenericSlots), byte loads.
 constexpr int kGenericSlots = 8;
+constexpr int kChunk = 32;  // lookups gathered per round
 
-template <int ELEM, int SCALE, int CPL, bool WEIGHTED, bool CHECKED>
-__global__ void __launch_bounds__(256) eb_bag_kernel(const EbParams p, int log2d) {
-    constexpr bool kGeneric = CPL == 0;
-    constexpr int NC = kGeneric ? kGenericSlots : CPL;
-    constexpr int BPL = kGeneric ? 1 : (ELEM == kEbU4 ? CPL / 2 : CPL);
-    constexpr int R = kGeneric ? 8 : 32;  // lookups gathered per round
+struct ChunkStage {      // per warp
+    int64_t off[kChunk];  // row byte offset, -1 = skipped (out of range / past the bag)
+    float2 sb[kChunk];    // scale, bias
+    float w[kChunk];
+};
+
+// Fast path: d == 32 * CPL * WPB, rows 8-byte aligned. Block = 8 warps = 8 / WPB bags.
+template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
+__global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int log2d) {  // <= 64 regs: 32 warps/SM
+    constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;  // bytes per lane per row
+    constexpr int BAGS = 8 / WPB;
     using Word = typename LaneWord<BPL>::T;
+    __shared__ ChunkStage stage[8];
+    __shared__ double part_sum[8];
+    __shared__ int part_emax[8], part_umin[8];
+    __shared__ uint32_t blk_flags;
+    __shared__ uint32_t is_last;
 
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bag_local = warp / WPB, slice = warp % WPB;
+    const int64_t bag = static_cast<int64_t>(blockIdx.x) * BAGS + bag_local;
+    const int64_t lane_byte = static_cast<int64_t>(slice) * 32 * BPL + lane * BPL;
+    const double dd = static_cast<double>(p.dim);
+    ChunkStage& cs = stage[warp];
+    if (threadIdx.x == 0) blk_flags = 0;
+
+    float acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    double csum = 0.0;
+    bool oob = false;
+    if (bag < p.num_bags) {
+        const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
+        int64_t nidx = (beg + lane < end) ? p.indices[beg + lane] : -1;
+        for (int64_t base = beg; base < end; base += kChunk) {
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+            const int64_t my_idx = nidx;
+            const bool valid = lane < cnt && static_cast<uint64_t>(my_idx) < static_cast<uint64_t>(p.rows);
+            if (lane < cnt && !valid) oob = true;
+            cs.off[lane] = valid ? my_idx * p.row_stride : -1;
+            __syncwarp();
+            // gather the chunk's rows (independent of everything but the indices)
+            // Every slot issues its load (skipped slots read row 0, masked below): a conditional on the
+            // loaded value would make each load wait for the previous one.
+            Word data[kChunk];
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                const int64_t o = cs.off[t];
+                data[t] = load_row_word<BPL>(p.data + ((t < cnt && o >= 0) ? o : 0) + lane_byte);
+            }
+            // metadata of lookup (base + lane), overlapping the row gathers
+            float my_s = 0.f, my_b = 0.f, my_w = 1.f;
+            int32_t my_rs = 0;
+            if (valid) load_meta<SCALE>(p.meta, my_idx, my_s, my_b, my_rs);
+            if constexpr (WEIGHTED) {
+                if (lane < cnt) my_w = p.weights[base + lane];
+            }
+            // prefetch the next chunk's indices
+            nidx = (base + kChunk + lane < end) ? p.indices[base + kChunk + lane] : -1;
+            cs.sb[lane] = make_float2(my_s, my_b);
+            if constexpr (WEIGHTED) cs.w[lane] = my_w;
+            double my_term = 0.0;
+            if constexpr (CHECKED) {
+                if (slice == 0 && valid) my_term = csum_term(my_s, my_b, my_rs, my_w, dd, WEIGHTED);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                if (t < cnt && cs.off[t] >= 0) {  // warp-uniform
+                    const float2 sb = cs.sb[t];
+                    const float w = WEIGHTED ? cs.w[t] : 1.0f;
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        float x = __fadd_rn(__fmul_rn(sb.x, decode<ELEM>(data[t], c)), sb.y);
+                        if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                        acc[c] = __fadd_rn(acc[c], x);
+                    }
+                }
+            }
+            if constexpr (CHECKED) {
+                if (slice == 0) {
+                    for (int t = 0; t < cnt; ++t) {
+                        const double term = __shfl_sync(0xffffffffu, my_term, t);
+                        if (cs.off[t] >= 0) csum = __dadd_rn(csum, term);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
+        // pooled output: this warp's slice
+        float* dst = p.out + bag * p.ld_out + slice * 32 * CPL + lane * CPL;
+        if constexpr (CPL % 4 == 0) {
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+                for (int c = 0; c < CPL; c += 4)
+                    *reinterpret_cast<float4*>(dst + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
+            }
+        } else if constexpr (CPL == 2) {
+            if ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)
+                *reinterpret_cast<float2*>(dst) = make_float2(acc[0], acc[1]);
+            else {
+                dst[0] = acc[0];
+                dst[1] = acc[1];
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
+        }
+    }
+    if constexpr (CHECKED) {
+        // ---- per-slice exactness statistics and order-free partial sum
+        int emax = -100000, umin = 100000;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) bit_span(acc[c], emax, umin);
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) s = __dadd_rn(s, static_cast<double>(acc[c]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+            umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+        }
+        if (lane == 0) {
+            part_sum[warp] = s;
+            part_emax[warp] = emax;
+            part_umin[warp] = umin;
+        }
+        __syncthreads();  // slices of a bag (and their global outputs) are complete
+        if (slice == 0 && bag < p.num_bags) {
+            int E = -100000, U = 100000;
+            double exact = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < WPB; ++s2) {
+                E = max(E, part_emax[warp + s2]);
+                U = min(U, part_umin[warp + s2]);
+                exact = __dadd_rn(exact, part_sum[warp + s2]);
+            }
+            double rsum;
+            if (E == -100000) {
+                rsum = 0.0;
+            } else if (E + 1 + log2d - U <= 53) {
+                rsum = exact;  // every partial sum is an exact multiple of 2^U below 2^53 ulps: order-free
+            } else {
+                // the reference's order: j = 0 .. d-1 (P:src/embedding_abft.cpp:66-67)
+                rsum = 0.0;
+                const float* row = p.out + bag * p.ld_out;
+                for (int j0 = 0; j0 < p.dim; j0 += 32) {
+                    const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
+                    for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
+                        rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, v, l)));
+                }
+            }
+            // ---- err = |rSum - cSum| > 1e-5 * max(|rSum|, |cSum|, 1)   (P:src/embedding_abft.cpp:80-81)
+            const double diff = fabs(__dsub_rn(rsum, csum));
+            const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
+            const int flag = diff > __dmul_rn(1e-5, mx);
+            if (lane == 0) {
+                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (p.rsum) p.rsum[bag] = rsum;
+                if (p.csum) p.csum[bag] = csum;
+                if (flag) atomicAdd(&blk_flags, 1u);
+            }
+        }
+        if (p.flag_count) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
+                __threadfence();
+                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
+            }
+            __syncthreads();
+            if (is_last && threadIdx.x == 0) {
+                __threadfence();
+                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
+                atomicExch(p.ws_block_cnt, 0u);
+            }
+        }
+    }
+}
+
+// Generic path (any d <= 256, unaligned rows): warp per bag, lane owns columns lane + 32*c, byte loads.
+template <int ELEM, int SCALE, bool WEIGHTED, bool CHECKED>
+__global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, int log2d) {
+    constexpr int NC = kGenericSlots;
+    constexpr int R = 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bag = static_cast<int64_t>(blockIdx.x) * 8 + warp;
     __shared__ uint32_t blk_flags;
     __shared__ uint32_t is_last;
     if (threadIdx.x == 0) blk_flags = 0;
     __syncthreads();
-
     if (bag < p.num_bags) {
         const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
         float acc[NC];
@@ -143,134 +332,69 @@ __global__ void __launch_bounds__(256) eb_bag_kernel(const EbParams p, int log2d
                 }
                 if constexpr (WEIGHTED) my_w = p.weights[base + lane];
             }
-            if constexpr (!kGeneric) {
-                Word data[R];
+            uint32_t data[R][NC];
 #pragma unroll
-                for (int t = 0; t < R; ++t) {
+            for (int t = 0; t < R; ++t) {
+                const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const int64_t j = lane + 32 * c;
+                    // unconditional load at a safe address (row 0, byte 0 for skipped slots); decode at use
+                    const bool ok = t < cnt && it >= 0 && j < p.dim;
+                    const int64_t byte = ELEM == kEbU4 ? (j >> 1) : j;
+                    data[t][c] = __ldg(p.data + (ok ? it * p.row_stride + byte : 0));
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+                if (t < cnt) {
                     const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
-                    data[t] = (t < cnt && it >= 0) ? load_row_word<BPL>(p.data + it * p.row_stride + lane * BPL) : Word(0);
-                }
+                    const float s = __shfl_sync(0xffffffffu, my_s, t);
+                    const float b = __shfl_sync(0xffffffffu, my_b, t);
+                    const float w = WEIGHTED ? __shfl_sync(0xffffffffu, my_w, t) : 1.0f;
+                    const int32_t rs = __shfl_sync(0xffffffffu, my_rs, t);
+                    if (it >= 0) {
 #pragma unroll
-                for (int t = 0; t < R; ++t) {
-                    if (t < cnt) {
-                        const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
-                        const float s = __shfl_sync(0xffffffffu, my_s, t);
-                        const float b = __shfl_sync(0xffffffffu, my_b, t);
-                        const float w = WEIGHTED ? __shfl_sync(0xffffffffu, my_w, t) : 1.0f;
-                        const int32_t rs = __shfl_sync(0xffffffffu, my_rs, t);
-                        if (it >= 0) {
-#pragma unroll
-                            for (int c = 0; c < NC; ++c) {
-                                float x = __fadd_rn(__fmul_rn(s, decode<ELEM>(data[t], c)), b);
-                                if constexpr (WEIGHTED) x = __fmul_rn(w, x);
-                                acc[c] = __fadd_rn(acc[c], x);
-                            }
-                            if constexpr (CHECKED) {
-                                double term = __dadd_rn(__dmul_rn(static_cast<double>(s), static_cast<double>(rs)),
-                                                        __dmul_rn(dd, static_cast<double>(b)));
-                                if constexpr (WEIGHTED) term = __dmul_rn(static_cast<double>(w), term);
-                                csum = __dadd_rn(csum, term);
-                            }
+                        for (int c = 0; c < NC; ++c) {
+                            const uint32_t raw = data[t][c];
+                            const uint32_t jj = static_cast<uint32_t>(lane + 32 * c);
+                            const float q = ELEM == kEbS8   ? static_cast<float>(static_cast<int8_t>(raw))
+                                            : ELEM == kEbU8 ? static_cast<float>(raw & 0xFFu)
+                                                            : static_cast<float>((raw >> (4 * (jj & 1))) & 0xFu);
+                            float x = __fadd_rn(__fmul_rn(s, q), b);
+                            if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                            if (lane + 32 * c < p.dim) acc[c] = __fadd_rn(acc[c], x);
                         }
-                    }
-                }
-            } else {
-                uint32_t data[R][NC];
-#pragma unroll
-                for (int t = 0; t < R; ++t) {
-                    const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) {
-                        const int64_t j = lane + 32 * c;
-                        uint32_t v = 0;
-                        if (t < cnt && it >= 0 && j < p.dim) {
-                            const int64_t byte = ELEM == kEbU4 ? (j >> 1) : j;
-                            v = p.data[it * p.row_stride + byte];
-                            if (ELEM == kEbU4) v = (v >> (4 * (j & 1))) & 0xFu;
-                        }
-                        data[t][c] = v;
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < R; ++t) {
-                    if (t < cnt) {
-                        const int64_t it = __shfl_sync(0xffffffffu, my_idx, t);
-                        const float s = __shfl_sync(0xffffffffu, my_s, t);
-                        const float b = __shfl_sync(0xffffffffu, my_b, t);
-                        const float w = WEIGHTED ? __shfl_sync(0xffffffffu, my_w, t) : 1.0f;
-                        const int32_t rs = __shfl_sync(0xffffffffu, my_rs, t);
-                        if (it >= 0) {
-#pragma unroll
-                            for (int c = 0; c < NC; ++c) {
-                                const float q = ELEM == kEbS8 ? static_cast<float>(static_cast<int8_t>(data[t][c]))
-                                                              : static_cast<float>(data[t][c]);
-                                float x = __fadd_rn(__fmul_rn(s, q), b);
-                                if constexpr (WEIGHTED) x = __fmul_rn(w, x);
-                                if (lane + 32 * c < p.dim) acc[c] = __fadd_rn(acc[c], x);
-                            }
-                            if constexpr (CHECKED) {
-                                double term = __dadd_rn(__dmul_rn(static_cast<double>(s), static_cast<double>(rs)),
-                                                        __dmul_rn(dd, static_cast<double>(b)));
-                                if constexpr (WEIGHTED) term = __dmul_rn(static_cast<double>(w), term);
-                                csum = __dadd_rn(csum, term);
-                            }
-                        }
+                        if constexpr (CHECKED) csum = __dadd_rn(csum, csum_term(s, b, rs, w, dd, WEIGHTED));
                     }
                 }
             }
         }
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
-
-        // ---- pooled output
         float* dst = p.out + bag * p.ld_out;
-        if constexpr (!kGeneric) {
-            if constexpr (NC % 4 == 0) {
-                float* d0 = dst + lane * NC;
-                if ((reinterpret_cast<uintptr_t>(d0) & 15) == 0) {
 #pragma unroll
-                    for (int c = 0; c < NC; c += 4)
-                        *reinterpret_cast<float4*>(d0 + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) d0[c] = acc[c];
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < NC; ++c) dst[lane * NC + c] = acc[c];
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < NC; ++c)
-                if (lane + 32 * c < p.dim) dst[lane + 32 * c] = acc[c];
-        }
-
+        for (int c = 0; c < NC; ++c)
+            if (lane + 32 * c < p.dim) dst[lane + 32 * c] = acc[c];
         if constexpr (CHECKED) {
-            // ---- rSum = sum_j double(r[j]) in the reference's order (P:src/embedding_abft.cpp:66-67)
             int emax = -100000, umin = 100000;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) bit_span(acc[c], emax, umin);
+            for (int c = 0; c < NC; ++c)
+                if (lane + 32 * c < p.dim) bit_span(acc[c], emax, umin);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
                 umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
             }
             double rsum = 0.0;
-            if (emax == -100000) {
-                rsum = 0.0;
-            } else if (emax + 1 + log2d - umin <= 53) {
-                // every partial sum is an exactly representable multiple of 2^umin: order-free
+            if (emax != -100000 && emax + 1 + log2d - umin <= 53) {
                 double s = 0.0;
 #pragma unroll
-                for (int c = 0; c < NC; ++c) s = __dadd_rn(s, static_cast<double>(acc[c]));
+                for (int c = 0; c < NC; ++c)
+                    if (lane + 32 * c < p.dim) s = __dadd_rn(s, static_cast<double>(acc[c]));
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
                 rsum = s;
-            } else if constexpr (!kGeneric) {
-                for (int l = 0; l < 32; ++l)
-#pragma unroll
-                    for (int c = 0; c < NC; ++c)
-                        rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, acc[c], l)));
-            } else {
+            } else if (emax != -100000) {
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
                     for (int l = 0; l < 32; ++l) {
@@ -278,7 +402,6 @@ __global__ void __launch_bounds__(256) eb_bag_kernel(const EbParams p, int log2d
                         if (l + 32 * c < p.dim) rsum = __dadd_rn(rsum, static_cast<double>(v));
                     }
             }
-            // ---- err = |rSum - cSum| > 1e-5 * max(|rSum|, |cSum|, 1)   (P:src/embedding_abft.cpp:80-81)
             const double diff = fabs(__dsub_rn(rsum, csum));
             const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
             const int flag = diff > __dmul_rn(1e-5, mx);
@@ -360,22 +483,50 @@ __global__ void __launch_bounds__(256) eb_meta_kernel(const uint8_t* __restrict_
 }
 
 // ------------------------------------------------------------------ host launchers
-template <int ELEM, int SCALE, int CPL>
-static cudaError_t launch_bag_cpl(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
+template <int ELEM, int SCALE, int CPL, int WPB>
+static cudaError_t launch_bag_fast(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>((p.num_bags + (8 / WPB) - 1) / (8 / WPB));
+    const bool w = p.weights != nullptr;
+    if (checked) {
+        if (w)
+            eb_bag_kernel<ELEM, SCALE, CPL, WPB, true, true><<<blocks, 256, 0, st>>>(p, log2d);
+        else
+            eb_bag_kernel<ELEM, SCALE, CPL, WPB, false, true><<<blocks, 256, 0, st>>>(p, log2d);
+    } else {
+        if (w)
+            eb_bag_kernel<ELEM, SCALE, CPL, WPB, true, false><<<blocks, 256, 0, st>>>(p, log2d);
+        else
+            eb_bag_kernel<ELEM, SCALE, CPL, WPB, false, false><<<blocks, 256, 0, st>>>(p, log2d);
+    }
+    return cudaGetLastError();
+}
+
+template <int ELEM, int SCALE>
+static cudaError_t launch_bag_generic(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((p.num_bags + 7) / 8);
     const bool w = p.weights != nullptr;
     if (checked) {
         if (w)
-            eb_bag_kernel<ELEM, SCALE, CPL, true, true><<<blocks, 256, 0, st>>>(p, log2d);
+            eb_bag_generic_kernel<ELEM, SCALE, true, true><<<blocks, 256, 0, st>>>(p, log2d);
         else
-            eb_bag_kernel<ELEM, SCALE, CPL, false, true><<<blocks, 256, 0, st>>>(p, log2d);
+            eb_bag_generic_kernel<ELEM, SCALE, false, true><<<blocks, 256, 0, st>>>(p, log2d);
     } else {
         if (w)
-            eb_bag_kernel<ELEM, SCALE, CPL, true, false><<<blocks, 256, 0, st>>>(p, log2d);
+            eb_bag_generic_kernel<ELEM, SCALE, true, false><<<blocks, 256, 0, st>>>(p, log2d);
         else
-            eb_bag_kernel<ELEM, SCALE, CPL, false, false><<<blocks, 256, 0, st>>>(p, log2d);
+            eb_bag_generic_kernel<ELEM, SCALE, false, false><<<blocks, 256, 0, st>>>(p, log2d);
     }
     return cudaGetLastError();
+}
+
+// Warps per bag: enough warps to keep ~32 resident per SM when the batch is small.
+static int pick_wpb(int64_t num_bags, int64_t d_over_32, bool u4) {
+    const int64_t target = 148 * 32;
+    int wpb = 1;
+    while (wpb < 4 && num_bags * wpb * 2 <= target && (d_over_32 % (wpb * 2)) == 0 &&
+           (!u4 || (d_over_32 / (wpb * 2)) >= 2))
+        wpb *= 2;
+    return wpb;
 }
 
 template <int ELEM, int SCALE>
@@ -383,14 +534,28 @@ static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, c
     const int64_t d = p.dim;
     const bool aligned_rows = (p.row_stride % 8) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 8) == 0;
     if (aligned_rows && d % 32 == 0) {
-        const int64_t cpl = d / 32;
-        if (ELEM != kEbU4 && cpl == 1) return launch_bag_cpl<ELEM, SCALE, 1>(p, checked, log2d, st);
-        if (cpl == 2) return launch_bag_cpl<ELEM, SCALE, 2>(p, checked, log2d, st);
-        if (cpl == 4) return launch_bag_cpl<ELEM, SCALE, 4>(p, checked, log2d, st);
-        if (cpl == 8) return launch_bag_cpl<ELEM, SCALE, 8>(p, checked, log2d, st);
+        const int64_t d32 = d / 32;  // columns per lane when one warp owns the whole row
+        const int wpb = pick_wpb(p.num_bags, d32, ELEM == kEbU4);
+        const int64_t cpl = d32 / wpb;
+#define ABFT_FAST(CPL_, WPB_) \
+    if (cpl == CPL_ && wpb == WPB_) return launch_bag_fast<ELEM, SCALE, CPL_, WPB_>(p, checked, log2d, st)
+        if constexpr (ELEM != kEbU4) {
+            ABFT_FAST(1, 1);
+            ABFT_FAST(1, 2);
+            ABFT_FAST(1, 4);
+        }
+        ABFT_FAST(2, 1);
+        ABFT_FAST(2, 2);
+        ABFT_FAST(2, 4);
+        ABFT_FAST(4, 1);
+        ABFT_FAST(4, 2);
+        ABFT_FAST(4, 4);
+        ABFT_FAST(8, 1);
+        ABFT_FAST(8, 2);
+#undef ABFT_FAST
     }
     if (d > 32 * kGenericSlots) return cudaErrorInvalidValue;
-    return launch_bag_cpl<ELEM, SCALE, 0>(p, checked, log2d, st);
+    return launch_bag_generic<ELEM, SCALE>(p, checked, log2d, st);
 }
 
 cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st) {

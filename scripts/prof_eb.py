@@ -1,0 +1,59 @@
+"""Profiling driver for the EmbeddingBag kernel. usage: prof_eb.py E3|E4 [checked=1] [iters=4]"""
+import ctypes as C
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2103_00130_b200 import _lib as L  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "E3"
+checked = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+dev = torch.device("cuda")
+st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+rng = np.random.default_rng(3)
+if cfg == "E3":
+    R, d, nb, elem, sct = 4_000_000, 128, 2048, 1, 0
+    lens = rng.integers(20, 101, nb)
+    ranks = np.arange(1, R + 1, dtype=np.float64)
+    cdf = np.cumsum(ranks ** -1.05)
+    cdf /= cdf[-1]
+    idx = rng.permutation(R)[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+    w = None
+    rb = d
+else:
+    R, d, nb, elem, sct = 8_000_000, 64, 4096, 2, 1
+    lens = rng.integers(1, 151, nb)
+    idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
+    w = torch.from_numpy(rng.uniform(0, 1, int(lens.sum())).astype(np.float32)).to(dev)
+    rb = d // 2
+rows = torch.randint(0, 256, (R, rb), dtype=torch.uint8, device=dev)
+sdt = torch.float32 if sct == 0 else torch.float16
+sc = (torch.rand(R, device=dev) * 9e-3 + 1e-3).to(sdt)
+bi = (torch.rand(R, device=dev) * 2 - 1).to(sdt)
+off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)).to(dev)
+ix = torch.from_numpy(idx).to(dev)
+tab = C.c_void_p()
+L.call("abftlp_eb_table_create", elem, vp(rows), R, d, rb, sct, vp(sc), vp(bi), None, st, C.byref(tab))
+o = torch.empty((nb, d), dtype=torch.float32, device=dev)
+fl = torch.empty(nb, dtype=torch.uint8, device=dev)
+fb = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+ts = []
+for i in range(iters):
+    L.call("abftlp_l2_flush", vp(fb), fb.numel(), i, st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if checked:
+        L.call("abftlp_eb_checked", tab, vp(off), vp(ix), nb, vp(w) if w is not None else None, vp(o), d, vp(fl),
+               None, None, None, None, st)
+    else:
+        L.call("abftlp_eb_unchecked", tab, vp(off), vp(ix), nb, vp(w) if w is not None else None, vp(o), d, None, st)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) * 1e3)
+print(cfg, "checked" if checked else "unchecked", "us:", [round(t, 1) for t in ts])
