@@ -17,6 +17,7 @@
 //                   rSum is computed order-free when every partial sum is provably exact in fp64 and
 //                   in the reference's sequential order otherwise -- bit-identical either way.
 #include <cuda_fp16.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "abft_internal.h"
@@ -298,6 +299,249 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
     }
 }
 
+// ------------------------------------------------------------------ async-copy pipeline (main path)
+// Same column ownership and accumulation order as eb_bag_kernel, but the 32 row slices and the 32
+// metadata records of a chunk land in shared memory through cp.async (16-B copies, L1 bypass), double
+// buffered per warp: while chunk c is accumulated from shared memory, chunk c+1's gathers are in flight
+// and chunk c+2's indices are being loaded. Needs 16-byte aligned row slices.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+// L1-allocating variant for row data: Zipf-hot rows are then served by the SM's L1 instead of
+// hammering one L2 slice.
+__device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int BPL>
+struct AsyncStage {
+    uint8_t rows[2][kChunk][32 * BPL];  // this warp's column slice of each gathered row
+    uint4 meta[2][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B)
+    int64_t off[2][kChunk];             // row byte offset of the slice, -1 = skipped
+    float w[2][kChunk];
+    double term[kChunk];                // cSum terms of the chunk, summed in order by lane 0
+};
+
+template <int SCALE>
+__device__ __forceinline__ void smem_meta(const uint4& m, float& s, float& b, int32_t& rs) {
+    if constexpr (SCALE == kEbF32) {
+        s = __uint_as_float(m.x);
+        b = __uint_as_float(m.y);
+        rs = static_cast<int32_t>(m.z);
+    } else {
+        s = __half2float(__ushort_as_half(static_cast<unsigned short>(m.x & 0xFFFFu)));
+        b = __half2float(__ushort_as_half(static_cast<unsigned short>(m.x >> 16)));
+        rs = static_cast<int32_t>(m.y);
+    }
+}
+
+template <int BPL>
+__device__ __forceinline__ typename LaneWord<BPL>::T lds_word(const uint8_t* p) {
+    if constexpr (BPL == 1) return *p;
+    else if constexpr (BPL == 2) return *reinterpret_cast<const uint16_t*>(p);
+    else if constexpr (BPL == 4) return *reinterpret_cast<const uint32_t*>(p);
+    else return *reinterpret_cast<const uint64_t*>(p);
+}
+
+template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
+__global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int log2d) {
+    constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
+    constexpr int SLICE = 32 * BPL;        // bytes of a row this warp needs
+    constexpr int PIECES = SLICE / 16;     // 16-B copies per row slice
+    constexpr int PER_LANE = kChunk * PIECES / 32;
+    constexpr int BAGS = 8 / WPB;
+    extern __shared__ __align__(16) uint8_t eb_smem[];
+    AsyncStage<BPL>& S = reinterpret_cast<AsyncStage<BPL>*>(eb_smem)[threadIdx.x >> 5];
+    __shared__ double part_sum[8];
+    __shared__ int part_emax[8], part_umin[8];
+    __shared__ uint32_t blk_flags;
+    __shared__ uint32_t is_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bag_local = warp / WPB, slice = warp % WPB;
+    const int64_t bag = static_cast<int64_t>(blockIdx.x) * BAGS + bag_local;
+    const int64_t slice_byte = static_cast<int64_t>(slice) * SLICE;
+    const double dd = static_cast<double>(p.dim);
+    if (threadIdx.x == 0) blk_flags = 0;
+
+    float acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+    double csum = 0.0;
+    bool oob = false;
+    if (bag < p.num_bags) {
+        const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
+        const int nchunks = static_cast<int>((end - beg + kChunk - 1) / kChunk);
+        // issue the gathers of chunk `ch` into slot `sl` (indices in `ix`, weights loaded to `wv`)
+        auto issue = [&](int ch, int sl, int64_t ix, float& wv) {
+            const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+            const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(p.rows);
+            if (lane < cnt && !valid) oob = true;
+            S.off[sl][lane] = valid ? ix * p.row_stride + slice_byte : -1;
+            if (valid) {
+                if constexpr (SCALE == kEbF32)
+                    cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint4*>(p.meta) + ix);
+                else
+                    cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint2*>(p.meta) + ix);
+            }
+            if constexpr (WEIGHTED) wv = lane < cnt ? p.weights[base + lane] : 1.0f;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < PER_LANE; ++i) {
+                const int piece = lane + 32 * i;
+                const int r = piece / PIECES, q = piece % PIECES;
+                const int64_t o = S.off[sl][r];
+                if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], p.data + o + q * 16);
+            }
+            cp_async_commit();
+        };
+        int64_t idx_next = (beg + lane < end) ? p.indices[beg + lane] : -1;
+        float w_slot[2] = {1.0f, 1.0f};
+        if (nchunks > 0) {
+            issue(0, 0, idx_next, w_slot[0]);
+            idx_next = (beg + kChunk + lane < end) ? p.indices[beg + kChunk + lane] : -1;
+        }
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int sl = ch & 1;
+            const bool more = ch + 1 < nchunks;
+            if (more) {
+                issue(ch + 1, sl ^ 1, idx_next, w_slot[sl ^ 1]);
+                const int64_t nb = beg + static_cast<int64_t>(ch + 2) * kChunk + lane;
+                idx_next = nb < end ? p.indices[nb] : -1;
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            if constexpr (WEIGHTED) S.w[sl][lane] = w_slot[sl];
+            __syncwarp();
+            const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+            if constexpr (CHECKED) {
+                if (slice == 0) {
+                    double my_term = 0.0;  // skipped / out-of-range lookups contribute nothing
+                    if (lane < cnt && S.off[sl][lane] >= 0) {
+                        float s, b;
+                        int32_t rs;
+                        smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
+                        my_term = csum_term(s, b, rs, WEIGHTED ? S.w[sl][lane] : 1.0f, dd, WEIGHTED);
+                    }
+                    S.term[lane] = my_term;
+                }
+            }
+            for (int t = 0; t < cnt; ++t) {
+                if (S.off[sl][t] >= 0) {  // warp-uniform
+                    float s, b;
+                    int32_t rs;
+                    smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
+                    const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
+                    const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        float x = __fadd_rn(__fmul_rn(s, decode<ELEM>(word, c)), b);
+                        if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                        acc[c] = __fadd_rn(acc[c], x);
+                    }
+                }
+            }
+            if constexpr (CHECKED) {
+                // the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), one lane;
+                // adding 0.0 for a skipped slot leaves the sum bit-identical (x + 0.0 == x)
+                __syncwarp();
+                if (slice == 0 && lane == 0) {
+#pragma unroll 8
+                    for (int t = 0; t < cnt; ++t) csum = __dadd_rn(csum, S.term[t]);
+                }
+            }
+            __syncwarp();  // slot `sl` may be refilled by the next issue
+        }
+        csum = __shfl_sync(0xffffffffu, csum, 0);
+        if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
+        float* dst = p.out + bag * p.ld_out + slice * 32 * CPL + lane * CPL;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
+    }
+    if constexpr (CHECKED) {
+        int emax = -100000, umin = 100000;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) bit_span(acc[c], emax, umin);
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) s = __dadd_rn(s, static_cast<double>(acc[c]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+            umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+        }
+        if (lane == 0) {
+            part_sum[warp] = s;
+            part_emax[warp] = emax;
+            part_umin[warp] = umin;
+        }
+        // only the WPB warps of this bag synchronise (their slices and global outputs are complete)
+        if constexpr (WPB > 1)
+            named_bar_sync(1 + bag_local, 32 * WPB);
+        else
+            __syncwarp();
+        if (slice == 0 && bag < p.num_bags) {
+            int E = -100000, U = 100000;
+            double exact = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < WPB; ++s2) {
+                E = max(E, part_emax[warp + s2]);
+                U = min(U, part_umin[warp + s2]);
+                exact = __dadd_rn(exact, part_sum[warp + s2]);
+            }
+            double rsum;
+            if (E == -100000) {
+                rsum = 0.0;
+            } else if (E + 1 + log2d - U <= 53) {
+                rsum = exact;
+            } else {
+                rsum = 0.0;
+                const float* row = p.out + bag * p.ld_out;
+                for (int j0 = 0; j0 < p.dim; j0 += 32) {
+                    const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
+                    for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
+                        rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, v, l)));
+                }
+            }
+            const double diff = fabs(__dsub_rn(rsum, csum));
+            const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
+            const int flag = diff > __dmul_rn(1e-5, mx);
+            if (lane == 0) {
+                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (p.rsum) p.rsum[bag] = rsum;
+                if (p.csum) p.csum[bag] = csum;
+                if (flag) atomicAdd(&blk_flags, 1u);
+            }
+        }
+        if (p.flag_count) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
+                __threadfence();
+                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
+            }
+            __syncthreads();
+            if (is_last && threadIdx.x == 0) {
+                __threadfence();
+                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
+                atomicExch(p.ws_block_cnt, 0u);
+            }
+        }
+    }
+}
+
 // Generic path (any d <= 256, unaligned rows): warp per bag, lane owns columns lane + 32*c, byte loads.
 template <int ELEM, int SCALE, bool WEIGHTED, bool CHECKED>
 __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, int log2d) {
@@ -501,6 +745,32 @@ static cudaError_t launch_bag_fast(const EbParams& p, bool checked, int log2d, c
     return cudaGetLastError();
 }
 
+template <int ELEM, int SCALE, int CPL, int WPB, bool W, bool CK>
+static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t st) {
+    constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
+    constexpr int smem = 8 * static_cast<int>(sizeof(AsyncStage<BPL>));
+    auto kern = eb_bag_async_kernel<ELEM, SCALE, CPL, WPB, W, CK>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const unsigned blocks = static_cast<unsigned>((p.num_bags + (8 / WPB) - 1) / (8 / WPB));
+    kern<<<blocks, 256, smem, st>>>(p, log2d);
+    return cudaGetLastError();
+}
+
+template <int ELEM, int SCALE, int CPL, int WPB>
+static cudaError_t launch_bag_async(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
+    const bool w = p.weights != nullptr;
+    if (checked)
+        return w ? launch_async_one<ELEM, SCALE, CPL, WPB, true, true>(p, log2d, st)
+                 : launch_async_one<ELEM, SCALE, CPL, WPB, false, true>(p, log2d, st);
+    return w ? launch_async_one<ELEM, SCALE, CPL, WPB, true, false>(p, log2d, st)
+             : launch_async_one<ELEM, SCALE, CPL, WPB, false, false>(p, log2d, st);
+}
+
 template <int ELEM, int SCALE>
 static cudaError_t launch_bag_generic(const EbParams& p, bool checked, int log2d, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>((p.num_bags + 7) / 8);
@@ -537,6 +807,26 @@ static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, c
         const int64_t d32 = d / 32;  // columns per lane when one warp owns the whole row
         const int wpb = pick_wpb(p.num_bags, d32, ELEM == kEbU4);
         const int64_t cpl = d32 / wpb;
+        const bool async_ok = (p.row_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 16) == 0 &&
+                              (reinterpret_cast<uintptr_t>(p.meta) % 16) == 0 && !std::getenv("ABFTLP_EB_SYNC");
+        if (async_ok) {
+#define ABFT_ASYNC(CPL_, WPB_) \
+    if (cpl == CPL_ && wpb == WPB_) return launch_bag_async<ELEM, SCALE, CPL_, WPB_>(p, checked, log2d, st)
+            if constexpr (ELEM != kEbU4) {
+                ABFT_ASYNC(1, 1);
+                ABFT_ASYNC(1, 2);
+                ABFT_ASYNC(1, 4);
+            }
+            ABFT_ASYNC(2, 1);
+            ABFT_ASYNC(2, 2);
+            ABFT_ASYNC(2, 4);
+            ABFT_ASYNC(4, 1);
+            ABFT_ASYNC(4, 2);
+            ABFT_ASYNC(4, 4);
+            ABFT_ASYNC(8, 1);
+            ABFT_ASYNC(8, 2);
+#undef ABFT_ASYNC
+        }
 #define ABFT_FAST(CPL_, WPB_) \
     if (cpl == CPL_ && wpb == WPB_) return launch_bag_fast<ELEM, SCALE, CPL_, WPB_>(p, checked, log2d, st)
         if constexpr (ELEM != kEbU4) {
