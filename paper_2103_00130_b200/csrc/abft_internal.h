@@ -26,46 +26,55 @@ constexpr int kPairM = 256;
 constexpr int kBK = 128;      // K bytes per k-block = one 128-byte swizzle span
 constexpr int kRowAlign = 256;  // B' rows are padded to a multiple of this
 
-// Encoded weight B' = [B | cs]^T stored K-block-major:
-//   bt[kb][j][kk] = B[kb*128 + kk][j]   for j < n
-//   bt[kb][n][kk] = cs[kb*128 + kk]      (the checksum column lives in row n of B')
-//   zero for n < j < n_pad and for kb*128 + kk >= k.
+// Encoded weight: B stored transposed, K-block-major, for the mainloop's TMA requests:
+//   bt[kb][j][kk] = B[kb*128 + kk][j]   for j < n, zero for n <= j < n_pad and kb*128 + kk >= k.
 // One k-block slab of a tile (rows j0..j0+R) is contiguous (R*128 bytes), so each TMA request is
-// one long burst, and the checksum column is produced by the main MMA of the tile that holds row n.
+// one long burst. The checksum column of the reference's [B | cs] (P:src/gemm_abft.cpp:73-85) is
+// kept as the vector cs (k_pad bytes, zero beyond k): C'[:, n] = A*cs is a GEMV, computed exactly on
+// CUDA cores by the epilogue warps (each N tile takes a K share), so it never costs an MMA tile.
 struct GemmWeight {
     int64_t k = 0, n = 0;          // logical sizes (PackedEncodedWeight::k()/n())
-    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad >= n + 1
+    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad >= n
     int8_t* bt = nullptr;          // k_pad/128 x n_pad x 128
-    int8_t* cs = nullptr;          // k (WeightChecksum::values, each in [0,126])
+    int8_t* cs = nullptr;          // k_pad (WeightChecksum::values, each in [0,126]; zero pad)
     bool owns = true;
     size_t bt_cap = 0, cs_cap = 0;  // allocation capacities (campaign scratch re-encodes in place)
     CUtensorMap map_b[3]{};         // 3D box {128, BN/2, KS} for BN = 64, 128, 256
-    uint64_t offset(int64_t i, int64_t j) const {  // byte offset of logical element (i, j), j <= n
-        return static_cast<uint64_t>((i / kBK) * n_pad * kBK + j * kBK + (i % kBK));
+    // device pointer of logical element (i, j) of [B | cs], j <= n
+    int8_t* element(int64_t i, int64_t j) const {
+        return j == n ? cs + i : bt + ((i / kBK) * n_pad * kBK + j * kBK + (i % kBK));
     }
 };
 
+// Per-row accumulator of the checked epilogue: bits 63..32 = sum of the tiles' A*cs shares (the exact
+// int32 checksum column, < 2^31 for k < 65793), 31..20 = tiles arrived (n_tiles <= 4095), 19..0 = sum
+// of the tiles' row residues (each < 127, so < 2^20).
+constexpr int kRowAccCountShift = 20;
+constexpr unsigned long long kRowAccCountMask = 0xFFFull;
+constexpr unsigned long long kRowAccResMask = (1ull << kRowAccCountShift) - 1;
+constexpr int kMaxCheckedNTiles = 4095;
+
 struct GemmParams {
-    int m, n;          // logical output size (n excludes the checksum column)
+    int m, n, k;       // logical sizes (n excludes the checksum column)
     int k_blocks;      // 128-byte K blocks
-    int n_tiles;       // N tiles covered by the MMA (includes the tile holding row n when CHECKED)
+    int n_tiles;       // N tiles of BN columns
     int m_tiles;       // 256-row pair tiles
     int num_tiles;     // m_tiles * n_tiles
     int32_t* c;
     int64_t ldc;
-    int32_t* csum;  // checksum column C'[:, n] (checked only)
+    const uint8_t* a;  // A (u8, row-major, lda % 16 == 0) for the checksum GEMV
+    int64_t lda;
+    const int8_t* cs;  // checksum vector (k_pad bytes, zero pad)
+    int32_t* csum;     // checksum column C'[:, n] (checked only)
     int64_t csum_ld;
     uint8_t* flags;      // per-row error flags (checked only)
     uint32_t* err_count; // number of flagged rows (checked only)
     // self-resetting per-stream workspace
-    uint32_t* row_res;    // [m] sum of per-tile row residues (each < 127)
-    int32_t* csum_acc;    // [m] checksum column value
-    uint32_t* half_cnt;   // [m_tiles*2] arrivals per 128-row half
-    uint32_t* err_acc;    // [1]
-    uint32_t* done_cnt;   // [1]
+    unsigned long long* row_acc;  // [m] see kRowAcc*: A*cs share sum | tile arrivals | residue sum
+    unsigned long long* err_pack; // [1] (finished rows) << 32 | (flagged rows so far)
     // in-epilogue fault hook (P:src/fault_lab.cpp:192-195 semantics): flip `bit` of C'(row, col)
     int fault_active, fault_row, fault_col, fault_bit;
-    unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
+    unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
 };
 
 enum EpiMode { kEpiTmaStore = 0, kEpiDirect = 2, kEpiNone = 4 };

@@ -296,7 +296,7 @@ CampaignReport run_gemm_campaign(const CampaignConfig& cfg) {
             SplitMix64 rng(seed, t * kStride + kInject);
             const uint64_t i = rng.next_below(static_cast<uint64_t>(k));
             const uint64_t j = rng.next_below(static_cast<uint64_t>(n));  // checksum column excluded
-            int8_t* cell = w->bt + w->offset(static_cast<int64_t>(i), static_cast<int64_t>(j));
+            int8_t* cell = w->element(static_cast<int64_t>(i), static_cast<int64_t>(j));
             if (cfg.fault.model == FaultModel::single_bit_flip)
                 flip_bit(cell, 0, draw_bit(rng, cfg.fault.bitRange, 8), st);
             else

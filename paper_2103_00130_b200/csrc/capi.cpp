@@ -455,8 +455,7 @@ abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uin
         if (i >= static_cast<uint64_t>(W.k) || j > static_cast<uint64_t>(W.n))
             throw std::out_of_range("inject_weight_B: coordinates out of range");
         if (bit >= 8) throw std::out_of_range("flip_bit: bit index out of range");
-        abftk::flip_bit(W.bt, W.offset(static_cast<int64_t>(i), static_cast<int64_t>(j)), bit, as_stream(stream));
-        if (j == static_cast<uint64_t>(W.n)) abftk::flip_bit(W.cs, i, bit, as_stream(stream));  // keep the vector in sync
+        abftk::flip_bit(W.element(static_cast<int64_t>(i), static_cast<int64_t>(j)), 0, bit, as_stream(stream));
         return ABFTLP_OK;
     });
 }

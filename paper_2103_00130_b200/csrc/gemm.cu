@@ -2,9 +2,9 @@
 //
 //   encode_weight_kernel  replaces compute_row_checksums + PackedEncodedWeight
 //                         (P:src/gemm_abft.cpp:60-91): one pass over B producing the mod-127 row
-//                         checksums cs and B' = [B | cs]^T in the K-block-major layout the mainloop
-//                         streams (abft_internal.h: GemmWeight). The checksum is row n of B', so the
-//                         tile that holds row n computes C'[:, n] = A*cs with the same MMAs.
+//                         checksums cs and B^T in the K-block-major layout the mainloop streams
+//                         (abft_internal.h: GemmWeight). The checksum column C'[:, n] = A*cs is a
+//                         GEMV done by the epilogue warps while the tensor cores run the tile.
 //   gemm_pair_kernel      replaces abft_gemm + verify_checksums / plain_gemm
 //                         (P:src/gemm_abft.cpp:30-56, 93-124). Persistent CTA pairs
 //                         (cluster of 2, tcgen05.mma.cta_group::2 kind::i8, M=256 x N=BN, A u8 x
@@ -13,9 +13,11 @@
 //                         requests: the per-SM TMA engine completes requests ~serially, so bytes per
 //                         request set the ingest rate). Two TMEM accumulators let the epilogue of
 //                         tile i overlap the mainloop of tile i+1. The CHECKED epilogue reduces
-//                         every output row mod 127 straight from TMEM, takes the checksum column
-//                         from the tile that holds it, and the last CTA of each 128-row half
-//                         compares and publishes flags -- no second pass over C.
+//                         every output row mod 127 straight from TMEM, adds its K share of
+//                         A*cs (exact int32, dp4a), and folds both plus an arrival count into one
+//                         64-bit atomic per row; the thread that completes a row compares and
+//                         publishes its flag -- no second pass over C, no fences or counters, and
+//                         no extra MMA tile for the checksum column.
 //   verify_kernel         replaces verify_checksums (P:src/gemm_abft.cpp:113-124) for post-hoc
 //                         checks (faults injected into C after the product).
 #include <cuda_runtime.h>
@@ -28,7 +30,7 @@ namespace abftk {
 // ============================================================ encoder
 // Block handles a 64-row slab of B (64 consecutive p, inside one k-block) and walks all n_pad
 // columns in 64-wide chunks, so the int64 row sums stay block-local (as the reference). Writes
-// B'[kb][j][p % 128] (64 contiguous bytes per j), then the checksum row j = n.
+// B'[kb][j][p % 128] (64 contiguous bytes per j) and cs[p] (zero for k <= p < k_pad).
 __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __restrict__ b, int64_t k, int64_t n,
                                                             int64_t ldb, int8_t* __restrict__ bt, int64_t n_pad,
                                                             int8_t* __restrict__ cs) {
@@ -61,32 +63,50 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
     if (tid < 64) {
         const long long s = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
         const int64_t p = p0 + tid;
-        const int8_t v = p < k ? static_cast<int8_t>(mod127(s)) : static_cast<int8_t>(0);
-        slab[n * kBK + tid] = v;  // checksum row of B'
-        if (p < k) cs[p] = v;
+        cs[p] = p < k ? static_cast<int8_t>(mod127(s)) : static_cast<int8_t>(0);
     }
 }
 
-// Replace the checksum row of B' (and the cs vector) with caller-supplied values.
-__global__ void set_checksums_kernel(int8_t* __restrict__ bt, int8_t* __restrict__ cs, const int8_t* __restrict__ src,
-                                     int64_t k, int64_t n, int64_t n_pad) {
+// Replace the checksum vector with caller-supplied values.
+__global__ void set_checksums_kernel(int8_t* __restrict__ cs, const int8_t* __restrict__ src, int64_t k) {
     for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < k;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int8_t v = src[p];
-        bt[(p / kBK) * n_pad * kBK + n * kBK + (p % kBK)] = v;
-        cs[p] = v;
-    }
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        cs[p] = src[p];
 }
 
 // Logical k x (n+1) view [B | cs] of an encoded weight (PackedEncodedWeight::at contract).
-__global__ void read_encoded_kernel(const int8_t* __restrict__ bt, int64_t k, int64_t n, int64_t n_pad,
-                                    int8_t* __restrict__ out) {
+__global__ void read_encoded_kernel(const int8_t* __restrict__ bt, const int8_t* __restrict__ cs, int64_t k,
+                                    int64_t n, int64_t n_pad, int8_t* __restrict__ out) {
     const int64_t total = k * (n + 1);
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = e / (n + 1), j = e - i * (n + 1);
-        out[e] = bt[(i / kBK) * n_pad * kBK + j * kBK + (i % kBK)];
+        out[e] = j == n ? cs[i] : bt[(i / kBK) * n_pad * kBK + j * kBK + (i % kBK)];
     }
+}
+
+// ============================================================ checksum GEMV share
+// sum_{p in [k0, k1)} A[row][p] * cs[p], exact in 32 bits (A <= 255, cs <= 126, k < 65793 as the
+// reference's int32 accumulation). 16-byte loads (lda % 16 == 0), four u8 x u8 dot products per dp4a.
+__device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int row, int k0, int k1) {
+    const uint8_t* arow = p.a + static_cast<int64_t>(row) * p.lda;
+    uint32_t s = 0;
+    int kk = k0;
+    for (; kk + 128 <= k1; kk += 128) {
+        uint4 av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = __ldg(reinterpret_cast<const uint4*>(arow + kk + 16 * u));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(p.cs + kk + 16 * u));
+            s = __dp4a(av[u].x, cv.x, s);
+            s = __dp4a(av[u].y, cv.y, s);
+            s = __dp4a(av[u].z, cv.z, s);
+            s = __dp4a(av[u].w, cv.w, s);
+        }
+    }
+    for (; kk < k1; ++kk) s += static_cast<uint32_t>(arow[kk]) * static_cast<uint32_t>(static_cast<uint8_t>(p.cs[kk]));
+    return s;
 }
 
 // ============================================================ GEMM (CTA pairs)
@@ -121,7 +141,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint32_t* bcast = tmem_holder + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -216,29 +235,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         }
     } else {
         // ---------------- epilogue: warps 2..5, thread <-> one row of this CTA's 128-row half
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int ncols = CHECKED ? p.n + 1 : p.n;
+        const int q = warp & 3;                  // TMEM lane quarter this warp may access
+        const int etid = threadIdx.x - 64;       // 0..127
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         int local = 0, chunk_ctr = 0;
         for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
             const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
             const int acc = local & 1;
             const uint32_t aph = (local >> 1) & 1;
+            const int row0 = mt * kPairM + static_cast<int>(rank) * kBM + q * 32;  // first row of this warp
+            const int row = row0 + lane;
+            // This tile's share of the checksum column C'[row][n] = sum_p A[row][p]*cs[p]: K blocks
+            // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
+            uint32_t cs_part = 0;
+            if constexpr (CHECKED) {
+                const int kb0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
+                const int kb1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
+                if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, row, kb0 * kBK, min(kb1 * kBK, p.k));
+            }
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
-            const int row0 = mt * kPairM + static_cast<int>(rank) * kBM + q * 32;  // first row of this warp
-            const int row = row0 + lane;
             const int n0 = nt * BN;
             const uint32_t t_row = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-            const bool fault_here = p.fault_active && row == p.fault_row;
+            const bool fault_here = p.fault_active && row == p.fault_row && p.fault_col < p.n;
             long long rsum = 0;
-            int32_t csv = 0;
-            bool has_cs = false;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int col0 = n0 + c * 32;
-                if (col0 >= ncols) break;  // warp-uniform
+                if (col0 >= p.n) break;  // warp-uniform
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(t_row + c * 32, v);
                 tmem_wait_ld();
@@ -253,16 +278,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                         for (int j = 0; j < 32; ++j) rsum += static_cast<int32_t>(v[j]);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
+                        for (int j = 0; j < 32; ++j)
                             if (col0 + j < p.n) rsum += static_cast<int32_t>(v[j]);
-                            if (col0 + j == p.n) {
-                                csv = static_cast<int32_t>(v[j]);
-                                has_cs = true;
-                            }
-                        }
                     }
                 }
-                if (col0 >= p.n) continue;  // the checksum column is not part of C
                 if constexpr (EPI == kEpiTmaStore) {
                     uint8_t* buf = staging + (q * 2 + (chunk_ctr & 1)) * 4096;
                     if (chunk_ctr >= 2) {
@@ -300,59 +319,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                     mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc * 8));
             }
             if constexpr (CHECKED) {
+                // mod is a ring homomorphism: the residue of the int64 row sum equals the sum of the
+                // per-tile residues mod 127 (P:src/gemm_abft.cpp:119-122 reduces the row sum once).
+                // One 64-bit atomic per row carries this tile's GEMV share, one arrival and its residue
+                // (kRowAcc* layout). Atomics on one address are totally ordered, so the thread that
+                // brings arrival n_tiles holds the complete row and finalizes it -- no fences, no
+                // counters, no second pass.
+                int fin = 0, flag = 0;
                 if (row < p.m) {
-                    // mod is a ring homomorphism: the residue of the int64 row sum equals the sum of the
-                    // per-tile residues mod 127 (P:src/gemm_abft.cpp:119-122 reduces the row sum once).
-                    atomicAdd(&p.row_res[row], static_cast<uint32_t>(mod127(rsum)));
-                    if (has_cs) p.csum_acc[row] = csv;
+                    const unsigned long long add = (static_cast<unsigned long long>(cs_part) << 32) |
+                                                   (1ull << kRowAccCountShift) |
+                                                   static_cast<unsigned long long>(mod127(rsum));
+                    const unsigned long long v = atomicAdd(&p.row_acc[row], add) + add;
+                    if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.n_tiles)) {
+                        fin = 1;
+                        int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
+                        if (p.fault_active && row == p.fault_row && p.fault_col == p.n)
+                            csv ^= static_cast<int32_t>(1u << p.fault_bit);  // fault in C'[:, n]
+                        const uint32_t res = static_cast<uint32_t>(v & kRowAccResMask) % 127u;
+                        flag = static_cast<int32_t>(res) != mod127(csv);
+                        p.flags[row] = static_cast<uint8_t>(flag);
+                        p.csum[static_cast<int64_t>(row) * p.csum_ld] = csv;
+                        p.row_acc[row] = 0ull;  // self-resetting workspace
+                    }
                 }
-                // All 128 threads' contributions are issued; one release by one thread publishes them
-                // (release is cumulative over the barrier), and only warp (threadIdx 64..95) waits for
-                // the arrival count -- the other epilogue warps move on to the next tile.
-                named_bar_sync(1, 128);
-                if (warp == 2) {
-                    const int half = mt * 2 + static_cast<int>(rank);
-                    uint32_t prev = 0;
-                    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.half_cnt[half], 1u);
-                    prev = __shfl_sync(0xffffffffu, prev, 0);
-                    if (trace && local == 0 && lane == 0) trace[8] = globaltimer();
-                    if (prev == static_cast<uint32_t>(p.n_tiles - 1)) {
-                        // Last tile of this 128-row half: every contribution is visible. Finalize the 128
-                        // rows (4 per lane) and leave the workspace zeroed for the next call.
-                        __threadfence();  // every lane acquires (lane 0's acquire is not warp-cumulative)
-                        const int hrow0 = mt * kPairM + static_cast<int>(rank) * kBM;
-                        uint32_t accs[4];
-                        int32_t css[4];
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int rr = hrow0 + r * 32 + lane;
-                            accs[r] = rr < p.m ? ld_relaxed_gpu(&p.row_res[rr]) : 0u;
-                            css[r] = rr < p.m ? static_cast<int32_t>(ld_relaxed_gpu(
-                                                    reinterpret_cast<uint32_t*>(&p.csum_acc[rr])))
-                                              : 0;
-                        }
-                        uint32_t cnt = 0;
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const int rr = hrow0 + r * 32 + lane;
-                            int flag = 0;
-                            if (rr < p.m) {
-                                flag = static_cast<int32_t>(accs[r] % 127u) != mod127(css[r]);
-                                p.flags[rr] = static_cast<uint8_t>(flag);
-                                p.csum[static_cast<int64_t>(rr) * p.csum_ld] = css[r];
-                                p.row_res[rr] = 0u;
-                            }
-                            cnt += __popc(__ballot_sync(0xffffffffu, flag));
-                        }
-                        if (lane == 0) {
-                            p.half_cnt[half] = 0u;
-                            if (cnt) atomicAdd(p.err_acc, cnt);
-                            const uint32_t done = atom_add_acq_rel_gpu(p.done_cnt, 1u);
-                            if (done == static_cast<uint32_t>(2 * p.m_tiles - 1)) {
-                                *p.err_count = atomicExch(p.err_acc, 0u);
-                                *p.done_cnt = 0u;
-                            }
-                        }
+                if (trace && local == 0 && threadIdx.x == 64) trace[8] = globaltimer();
+                const uint32_t nfin = __popc(__ballot_sync(0xffffffffu, fin));
+                const uint32_t nflag = __popc(__ballot_sync(0xffffffffu, flag));
+                if (lane == 0 && nfin) {
+                    // (finished rows) << 32 | (flagged rows); the call's last finished row publishes
+                    const unsigned long long prev = atomicAdd(p.err_pack, (static_cast<unsigned long long>(nfin) << 32) | nflag);
+                    if ((prev >> 32) + nfin == static_cast<unsigned long long>(p.m)) {
+                        *p.err_count = static_cast<uint32_t>(prev) + nflag;
+                        *p.err_pack = 0ull;
                     }
                 }
             }
@@ -454,12 +453,12 @@ int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st) {
     int64_t blocks = (w.k * (w.n + 1) + 255) / 256;
     if (blocks > 4096) blocks = 4096;
-    read_encoded_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(w.bt, w.k, w.n, w.n_pad, out);
+    read_encoded_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(w.bt, w.cs, w.k, w.n, w.n_pad, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st) {
-    set_checksums_kernel<<<static_cast<unsigned>((w.k + 255) / 256), 256, 0, st>>>(w.bt, w.cs, src, w.k, w.n, w.n_pad);
+    set_checksums_kernel<<<static_cast<unsigned>((w.k + 255) / 256), 256, 0, st>>>(w.cs, src, w.k);
     return cudaGetLastError();
 }
 

@@ -71,12 +71,9 @@ static CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* base, uint64_
 // leave every counter at zero on exit, so one workspace serves any number of ordered calls.
 struct Workspace {
     int device = 0;
-    uint32_t* row_res = nullptr;
-    int32_t* csum_acc = nullptr;
+    unsigned long long* row_acc = nullptr;  // GEMM: per-row (A*cs share sum) << 32 | residue sum
     int64_t rows_cap = 0;
-    uint32_t* half_cnt = nullptr;
-    int64_t halves_cap = 0;
-    uint32_t* small = nullptr;  // [0] err_acc [1] done_cnt [2] verify acc [3] verify blocks [4] eb acc [5] eb blocks
+    uint32_t* small = nullptr;  // [0..1] spare [2] verify acc [3] verify blocks [4] eb acc [5] eb blocks
     uint8_t* scratch = nullptr;  // A repack buffer
     size_t scratch_cap = 0;
     std::mutex mu;
@@ -143,7 +140,7 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
     if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
     if (!d_b) throw std::invalid_argument("null argument");
     if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
-    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n + 1, kRowAlign);
+    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, kRowAlign);
     const size_t need_bt = static_cast<size_t>(n_pad * k_pad);
     if (!w.bt || need_bt > w.bt_cap || static_cast<size_t>(k_pad) > w.cs_cap) {
         if (w.bt) {
@@ -206,7 +203,8 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
     const int pairs = std::max(1, device_sm_count() / 2);
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t kb = k_pad / kBK;
-    const int64_t ncols = checked ? n + 1 : n;
+    (void)checked;  // checked and unchecked run the same MMA tiles (the checksum column is a GEMV)
+    const int64_t ncols = n;
     const int epi = c_tma_ok ? kEpiTmaStore : kEpiDirect;
     if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn[,epi]" tuning override
         int bn = 0, e = -1;
@@ -277,22 +275,17 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (!c_tma_ok && t.epi != kEpiNone) t.epi = kEpiDirect;
 
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
-    const int64_t ncols = checked ? w.n + 1 : w.n;
-    const int64_t n_tiles = (ncols + t.bn - 1) / t.bn;
+    const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
     const int64_t kb = w.k_pad / kBK;
     if (m_tiles * n_tiles > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
 
-    if (checked && m > ws.rows_cap) {
-        int64_t cap_a = ws.rows_cap, cap_b = ws.rows_cap;  // row_res and csum_acc share one capacity
-        grow(ws.row_res, cap_a, m, st);
-        grow(ws.csum_acc, cap_b, m, st);
-        ws.rows_cap = std::min(cap_a, cap_b);
-    }
-    if (checked) grow(ws.half_cnt, ws.halves_cap, 2 * m_tiles, st);
+    if (checked && n_tiles > kMaxCheckedNTiles) throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
+    if (checked) grow(ws.row_acc, ws.rows_cap, m, st);
 
     GemmParams p{};
     p.m = static_cast<int>(m);
     p.n = static_cast<int>(w.n);
+    p.k = static_cast<int>(w.k);
     p.k_blocks = static_cast<int>(kb);
     p.n_tiles = static_cast<int>(n_tiles);
     p.m_tiles = static_cast<int>(m_tiles);
@@ -303,11 +296,11 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.csum_ld = csum_ld;
     p.flags = d_flags;
     p.err_count = d_err_count;
-    p.row_res = ws.row_res;
-    p.csum_acc = ws.csum_acc;
-    p.half_cnt = ws.half_cnt;
-    p.err_acc = ws.small + 0;
-    p.done_cnt = ws.small + 1;
+    p.a = a;
+    p.lda = a_ld;
+    p.cs = w.cs;
+    p.row_acc = ws.row_acc;
+    p.err_pack = reinterpret_cast<unsigned long long*>(ws.small + 8);
     p.trace = g_trace;
     if (has_fault) {
         p.fault_active = 1;
