@@ -22,6 +22,8 @@
 //                         checks (faults injected into C after the product).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "abft_internal.h"
 #include "ptx.cuh"
 
@@ -112,14 +114,30 @@ __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int row, int
 // ============================================================ GEMM (CTA pairs)
 template <int BN>
 struct PairCfg {
-    static constexpr int KS = BN == 64 ? 4 : 2;             // k-blocks per pipeline stage
+    // k-blocks per pipeline stage. Measured on B200: an SM's TMA requests pipeline (issue ~50 ns each,
+    // completions ~100-200 ns apart under full load), so what sustains ingest is BYTES IN FLIGHT, not
+    // bytes per request -- small stages, as many as shared memory holds.
+#ifndef ABFT_KS64
+#define ABFT_KS64 4
+#endif
+#ifndef ABFT_KS128
+#define ABFT_KS128 2
+#endif
+#ifndef ABFT_KS256
+#define ABFT_KS256 2
+#endif
+#ifndef ABFT_STAGING_BUFS
+#define ABFT_STAGING_BUFS 2
+#endif
+    static constexpr int KS = BN == 64 ? ABFT_KS64 : BN == 128 ? ABFT_KS128 : ABFT_KS256;
+    static constexpr int kStagingBufs = ABFT_STAGING_BUFS;  // per epilogue warp
     static constexpr int kABytes = kBM * kBK;                // per CTA per k-block (its 128 rows of A)
     static constexpr int kBBytes = (BN / 2) * kBK;           // per CTA per k-block (its half of the B' tile)
     static constexpr int kStageBytes = KS * (kABytes + kBBytes);
-    static constexpr int kStaging = 4 * 2 * 4096;            // epilogue: 4 warps x 2 x (32 rows x 32 int32)
+    static constexpr int kStaging = 4 * kStagingBufs * 4096; // epilogue: 4 warps x bufs x (32 rows x 32 int32)
     static constexpr int kBarBytes = 512;
-    static constexpr int kRawStages = (220 * 1024 - 1024 - kStaging - kBarBytes) / kStageBytes;
-    static constexpr int kStages = kRawStages > 8 ? 8 : kRawStages;
+    static constexpr int kRawStages = (227 * 1024 - 1024 - kStaging - kBarBytes) / kStageBytes;
+    static constexpr int kStages = kRawStages > 16 ? 16 : kRawStages;
     static constexpr uint32_t kTmemCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kStaging + kBarBytes;
     static_assert(kStages >= 2, "need a double-buffered ring");
@@ -161,9 +179,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
+        griddep_launch_dependents();  // the next kernel's prologue may overlap this grid
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
         if (EPI == kEpiTmaStore) tma_prefetch(&tmC);
+        // warm L2 with this pair's first stages (before griddep_wait: prefetches only touch L2)
+        if (pair < p.num_tiles) {
+            const int mt = pair / p.n_tiles, nt = pair - mt * p.n_tiles;
+            const int pre = kb_steps < STAGES ? kb_steps : STAGES;
+            for (int ks = 0; ks < pre; ++ks) {
+                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS);
+                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS);
+            }
+        }
     }
     // Barriers must be visible to the peer before any TMA / commit targets them; TMEM is allocated
     // afterwards by the MMA warp so the producer's first loads overlap the allocation.
@@ -179,6 +207,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         tc_fence_after();
         tmem = *tmem_holder;
     }
+
+    // Everything above is independent of the preceding kernel's results; from here on global memory is
+    // read and written (PDL: blocks until the previous grid on the stream has completed).
+    griddep_wait();
 
     if (warp == 0) {
         // ---------------- TMA producer (both CTAs; completion counted on the leader's barrier)
@@ -236,7 +268,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     } else {
         // ---------------- epilogue: warps 2..5, thread <-> one row of this CTA's 128-row half
         const int q = warp & 3;                  // TMEM lane quarter this warp may access
-        const int etid = threadIdx.x - 64;       // 0..127
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         int local = 0, chunk_ctr = 0;
         for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
@@ -283,9 +314,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                     }
                 }
                 if constexpr (EPI == kEpiTmaStore) {
-                    uint8_t* buf = staging + (q * 2 + (chunk_ctr & 1)) * 4096;
-                    if (chunk_ctr >= 2) {
-                        if (lane == 0) bulk_wait_read<1>();
+                    constexpr int NB = Cfg::kStagingBufs;
+                    uint8_t* buf = staging + (q * NB + (chunk_ctr % NB)) * 4096;
+                    if (chunk_ctr >= NB) {
+                        if (lane == 0) bulk_wait_read<NB - 1>();
                         __syncwarp();
                     }
 #pragma unroll
@@ -422,8 +454,18 @@ static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    kern<<<2 * pairs, 192, Cfg::kSmemBytes, st>>>(a, b, c, p);
-    return cudaGetLastError();
+    static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
 }
 
 template <int BN, bool CHECKED>

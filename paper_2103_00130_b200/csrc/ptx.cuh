@@ -245,6 +245,23 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
         : "memory");
 }
 
+// L2 prefetch of a 3D tensor box (no smem destination, no completion): safe before griddepcontrol.wait,
+// L2 being the point of coherence.
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Lets the next kernel on the stream start its prologue while this one runs; griddep_wait() blocks until
+// the preceding grid has completed and its memory is visible (a no-op without the launch attribute).
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
