@@ -5,7 +5,9 @@ Headline workload = BASELINE.json configs[1] ("G2"): checked int8 GEMM m=256, k=
 A u8 U[0,255], B s8 U[-128,127] (SplitMix64, the reference's draw protocol), B encoded ONCE and
 reused for a job of 1000 GEMMs with distinct A matrices; 1% of the runs inject one random bit
 flip (half into B' after encoding, half into C' through the epilogue hook) and every injected
-run must be flagged. One step = one such job; L2 is flushed between steps (a 256 MiB write).
+run must be flagged. One step = one such job, replayed as a CUDA graph of the 1000 launches (the
+kernels use programmatic dependent launch, so each GEMM's prologue overlaps the previous one's tail);
+L2 is flushed between steps (a 256 MiB read).
 metric = checked int8 GEMM TOPS (2*m*n*k per GEMM, checksum column excluded).
 
 Secondary lines in the same JSON object: ABFT overhead vs the same kernel with checking compiled
@@ -161,11 +163,13 @@ def run_gpu_arm(args, rank, world, dist):
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    stream = torch.cuda.current_stream()
+    # one dedicated stream: the library's per-stream workspace is allocated during warm-up, so the job
+    # can then be captured into a CUDA graph (no allocation happens under capture)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     st = C.c_void_p(stream.cuda_stream)
     vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     pk = peaks()
-    launches = 0
 
     # ---- inputs resident in HBM before timing: B encoded once; JOB distinct A matrices
     # Rank r owns the N-column shard r of a (N * world)-wide weight (weak scaling; no data-path
@@ -194,32 +198,28 @@ def run_gpu_arm(args, rank, world, dist):
         else:
             plan[run] = ("C", rng.next_below(M), rng.next_below(N + 1), rng.next_below(32))
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(JOB)]
-
-    def job(checked=True, record=False):
-        nonlocal launches
+    def job(checked=True):
+        """Issues the whole job on `st`; returns the number of kernels it launches."""
+        n = 0
         for i in range(JOB):
             f = plan.get(i)
             fault = None
             if f and f[0] == "B":
                 L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
-                launches += 1
+                n += 1
             elif f and f[0] == "C" and checked:
                 fault = C.byref(L.Fault(1, f[1], f[2], f[3]))
-            if record:
-                ev[i][0].record(stream)
             c = c_ring[i % n_cbuf]
             if checked:
                 L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c), N, vp(csum[i]), 1, vp(flags[i]),
                        vp(errs[i:i + 1]), fault, st)
             else:
                 L.call("abftlp_gemm_unchecked", vp(a_pool[i]), M, K, w, vp(c), N, st)
-            launches += 1
-            if record:
-                ev[i][1].record(stream)
+            n += 1
             if f and f[0] == "B":
                 L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
-                launches += 1
+                n += 1
+        return n
 
     def barrier():
         if dist is not None:
@@ -246,19 +246,30 @@ def run_gpu_arm(args, rank, world, dist):
             total += ms
         return total, per
 
-    # ---- warm-up (also compiles/caches tensor maps, workspaces)
-    for _ in range(args.warmup):
+    # ---- warm-up on the job stream (workspace, tensor maps, kernel attributes), then capture the job:
+    # a step replays 1000 GEMM launches (+ the fault-injection kernels) without per-launch host cost.
+    for _ in range(max(1, args.warmup)):
         job(True)
         job(False)
+    barrier()
+    graphs = {}
+    kernels_per_job = {}
+    for ck in (True, False):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            kernels_per_job[ck] = job(ck)
+        graphs[ck] = g
+    torch.cuda.set_stream(stream)
+    for _ in range(args.warmup):
+        graphs[True].replay()
+        graphs[False].replay()
     barrier()
 
     clocks = Clocks()
     clocks.start(dev.index)
-    launches = 0
-    t_total, t_steps = timed(lambda: job(True, record=True), args.steps)
-    kernel_us = statistics.mean(ev[i][0].elapsed_time(ev[i][1]) * 1e3 for i in range(JOB) if i not in plan)
-    launches_timed = launches + args.steps  # + the L2 flush kernel before each step
+    t_total, t_steps = timed(graphs[True].replay, args.steps)
     clk = clocks.stop()
+    launches_timed = args.steps * (kernels_per_job[True] + 1)  # + the L2 flush kernel before each step
 
     # parity of the job's verdicts: every injected run flagged, no clean run flagged
     e = errs.cpu().numpy()
@@ -271,7 +282,22 @@ def run_gpu_arm(args, rank, world, dist):
     if dist is not None:
         dist.all_reduce(verdict, op=dist.ReduceOp.MAX)  # OR of the per-shard verdicts
     # unchecked baseline (same kernel, checking compiled out) for the ABFT overhead
-    u_total, _ = timed(lambda: job(False), args.steps)
+    u_total, _ = timed(graphs[False].replay, args.steps)
+
+    # ---- per-launch duration of the checked kernel (events around each launch, no graph, L2 warm
+    # with B'; distinct A per launch as in the job): the roofline's denominator
+    per_launch = []
+    torch.cuda.synchronize()
+    torch.cuda._sleep(4_000_000)  # ~2 ms: the host enqueues every launch below before the GPU reaches them
+    for i in range(60):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c_ring[i % n_cbuf]), N, vp(csum[i]), 1,
+               vp(flags[i]), vp(errs[i:i + 1]), None, st)
+        e1.record(stream)
+        per_launch.append((e0, e1))
+    torch.cuda.synchronize()
+    kernel_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in per_launch[10:])
 
     # ---- cold single GEMM (L2 flushed before each launch), kernel-only
     cold = []
@@ -324,7 +350,8 @@ def run_gpu_arm(args, rank, world, dist):
         "data": "synthetic (SplitMix64, the reference's draw protocol); no dataset",
         "config": {"workload": "G2 = BASELINE configs[1]: checked GEMM m=256 k=4096 n=4096, B encoded once, "
                                f"job of {JOB} GEMMs with distinct A, 1% fault runs (B' and C' bit flips)",
-                   "step": f"one {JOB}-GEMM job", "l2": "flushed between steps (256 MiB write, untimed)",
+                   "step": f"one {JOB}-GEMM job", "l2": "flushed between steps (256 MiB read, untimed); the job's 1 GB of A exceeds L2",
+                   "launch": "CUDA graph of the job's launches, programmatic dependent launch between GEMMs",
                    "parallelism": f"N-column shard per GPU (n={N} per rank), verdicts OR-reduced",
                    "gemm_kernel": "tcgen05 cta_group::2 int8, TMEM accumulators, fused mod-127 row check"},
         "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": M * K * e2e_runs,
@@ -333,6 +360,8 @@ def run_gpu_arm(args, rank, world, dist):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["int8_tops"], "unit": "TOP/s",
                      "frac": achieved / pk["int8_tops"], "traffic": None,
                      "kernel": "gemm_pair_kernel (checked)", "kernel_us": kernel_us,
+                     "kernel_us_how": "median CUDA-event duration of single checked launches queued behind a sleep kernel (distinct A, B' L2-warm, no PDL overlap)",
+                     "job_us_per_gemm": t_total * 1e3 / (args.steps * JOB),
                      "ops_per_launch": OPS, "alg_bytes_per_launch": ALG_BYTES,
                      "peak_source": f"2 x bf16 burst from {pk['source']}",
                      "note": "B' stays L2-resident across the job, so the per-launch bound is tensor, not HBM"},
