@@ -128,6 +128,20 @@ abftlp_status abftlp_eb_unchecked(const abftlp_eb_table* t, const int64_t* d_off
                                   const float* d_weights, float* d_out, uint64_t ld_out,
                                   int32_t* d_status, abftlp_stream stream);
 
+/* Checked pooled lookups that write straight into per-destination buffers: the table-wise sharded
+ * DLRM exchange fused into the lookup kernel. Bag b's pooled vector goes to
+ * d_out_dest[b / bags_per_dest] + (b % bags_per_dest) * ld_out and its flag to
+ * d_flag_dest[b / bags_per_dest][(b % bags_per_dest) * flag_ld]. d_out_dest / d_flag_dest are DEVICE
+ * arrays of pointers, which may point into peer GPUs' memory mapped over NVLink (CUDA IPC / symmetric
+ * memory), so the all-to-all of pooled outputs overlaps the lookups instead of following them. Same
+ * arithmetic and verdicts as abftlp_eb_checked. */
+abftlp_status abftlp_eb_checked_scatter(const abftlp_eb_table* t, const int64_t* d_offsets,
+                                        const int64_t* d_indices, uint64_t num_bags,
+                                        const float* d_weights, float* const* d_out_dest,
+                                        uint64_t ld_out, uint8_t* const* d_flag_dest, uint64_t flag_ld,
+                                        uint64_t bags_per_dest, uint32_t* d_flag_count,
+                                        int32_t* d_status, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ fault injection */
 /* XOR bit `bit` of element `index` of an array of `elem_bytes`-wide integers
  * (flip_bit, P:src/fault_lab.hpp:87-93). */

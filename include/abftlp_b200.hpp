@@ -361,6 +361,7 @@ inline std::vector<EbCheckedResult> batch_abft_eb(const DeviceTable& table, cons
     }
     std::vector<EbCheckedResult> res(B);
     if (B == 0) return res;
+    if (indices.empty()) indices.push_back(0);  // a valid (never read) pointer for all-empty batches
     detail::DBuf doff(offsets.data(), 8 * (B + 1)), didx(indices.data(), 8 * indices.size()),
         dw(weights.data(), 4 * weights.size()), dout(4 * B * (d ? d : 1)), dfl(B), drs(8 * B), dcs(8 * B);
     if (checked)

@@ -103,6 +103,7 @@ _SIGS = {
     "abftlp_eb_table_row_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_checked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp, vp, vp, vp, vp]),
     "abftlp_eb_unchecked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp]),
+    "abftlp_eb_checked_scatter": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, u64, u64, vp, vp, vp]),
     "abftlp_flip_bit": (i32, [vp, u32, u64, u32, vp]),
     "abftlp_gemm_weight_flip_bit": (i32, [vp, u64, u64, u32, vp]),
     "abftlp_eb_table_flip_bit": (i32, [vp, u64, u64, u32, vp]),

@@ -125,6 +125,13 @@ struct EbParams {
     int32_t* status;       // nullable; bit 0 = index out of range
     uint32_t* ws_flag_acc;
     uint32_t* ws_block_cnt;
+    // scatter mode (table-wise sharded exchange fused into the lookups): when out_dest is set, bag b
+    // writes out_dest[b / bags_per_dest] + (b % bags_per_dest) * ld_out and its flag to
+    // flag_dest[b / bags_per_dest][(b % bags_per_dest) * flag_ld] (pointers may be NVLink peer memory)
+    float* const* out_dest;
+    uint8_t* const* flag_dest;
+    int64_t bags_per_dest;
+    int64_t flag_ld;
 };
 
 }  // namespace abftk

@@ -435,6 +435,25 @@ abftlp_status abftlp_eb_unchecked(const abftlp_eb_table* t, const int64_t* d_off
     });
 }
 
+abftlp_status abftlp_eb_checked_scatter(const abftlp_eb_table* t, const int64_t* d_offsets, const int64_t* d_indices,
+                                        uint64_t num_bags, const float* d_weights, float* const* d_out_dest,
+                                        uint64_t ld_out, uint8_t* const* d_flag_dest, uint64_t flag_ld,
+                                        uint64_t bags_per_dest, uint32_t* d_flag_count, int32_t* d_status,
+                                        abftlp_stream stream) {
+    if (!t || !d_out_dest || !d_flag_dest) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::EbScatter sc;
+        sc.out_dest = d_out_dest;
+        sc.flag_dest = d_flag_dest;
+        sc.bags_per_dest = static_cast<int64_t>(bags_per_dest);
+        sc.flag_ld = static_cast<int64_t>(flag_ld);
+        abftk::eb_run(*t->t, d_offsets, d_indices, static_cast<int64_t>(num_bags), d_weights, nullptr,
+                      static_cast<int64_t>(ld_out), true, nullptr, nullptr, nullptr, d_flag_count, d_status,
+                      as_stream(stream), &sc);
+        return ABFTLP_OK;
+    });
+}
+
 // ============================================================ fault injection
 abftlp_status abftlp_flip_bit(void* d_ptr, uint32_t elem_bytes, uint64_t index, uint32_t bit, abftlp_stream stream) {
     if (!d_ptr) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");

@@ -25,6 +25,16 @@
 
 namespace abftk {
 
+// Output row / flag slot of a bag: local buffers, or a destination table (sharded exchange, EbParams).
+__device__ __forceinline__ float* out_row(const EbParams& p, int64_t bag) {
+    if (p.out_dest) return p.out_dest[bag / p.bags_per_dest] + (bag % p.bags_per_dest) * p.ld_out;
+    return p.out + bag * p.ld_out;
+}
+__device__ __forceinline__ uint8_t* flag_slot(const EbParams& p, int64_t bag) {
+    if (p.flag_dest) return p.flag_dest[bag / p.bags_per_dest] + (bag % p.bags_per_dest) * p.flag_ld;
+    return p.flags ? p.flags + bag : nullptr;
+}
+
 namespace {
 
 template <int BPL>
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
         }
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
         // pooled output: this warp's slice
-        float* dst = p.out + bag * p.ld_out + slice * 32 * CPL + lane * CPL;
+        float* dst = out_row(p, bag) + slice * 32 * CPL + lane * CPL;
         if constexpr (CPL % 4 == 0) {
             if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
             } else {
                 // the reference's order: j = 0 .. d-1 (P:src/embedding_abft.cpp:66-67)
                 rsum = 0.0;
-                const float* row = p.out + bag * p.ld_out;
+                const float* row = out_row(p, bag);
                 for (int j0 = 0; j0 < p.dim; j0 += 32) {
                     const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
                     for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
@@ -276,7 +286,7 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
             const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
             const int flag = diff > __dmul_rn(1e-5, mx);
             if (lane == 0) {
-                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
                 if (p.rsum) p.rsum[bag] = rsum;
                 if (p.csum) p.csum[bag] = csum;
                 if (flag) atomicAdd(&blk_flags, 1u);
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
         }
         csum = __shfl_sync(0xffffffffu, csum, 0);
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
-        float* dst = p.out + bag * p.ld_out + slice * 32 * CPL + lane * CPL;
+        float* dst = out_row(p, bag) + slice * 32 * CPL + lane * CPL;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
     }
@@ -508,7 +518,7 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
                 rsum = exact;
             } else {
                 rsum = 0.0;
-                const float* row = p.out + bag * p.ld_out;
+                const float* row = out_row(p, bag);
                 for (int j0 = 0; j0 < p.dim; j0 += 32) {
                     const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
                     for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
@@ -519,7 +529,7 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
             const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
             const int flag = diff > __dmul_rn(1e-5, mx);
             if (lane == 0) {
-                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
                 if (p.rsum) p.rsum[bag] = rsum;
                 if (p.csum) p.csum[bag] = csum;
                 if (flag) atomicAdd(&blk_flags, 1u);
@@ -615,7 +625,7 @@ __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, i
             }
         }
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
-        float* dst = p.out + bag * p.ld_out;
+        float* dst = out_row(p, bag);
 #pragma unroll
         for (int c = 0; c < NC; ++c)
             if (lane + 32 * c < p.dim) dst[lane + 32 * c] = acc[c];
@@ -650,7 +660,7 @@ __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, i
             const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
             const int flag = diff > __dmul_rn(1e-5, mx);
             if (lane == 0) {
-                if (p.flags) p.flags[bag] = static_cast<uint8_t>(flag);
+                if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
                 if (p.rsum) p.rsum[bag] = rsum;
                 if (p.csum) p.csum[bag] = csum;
                 if (flag) atomicAdd(&blk_flags, 1u);

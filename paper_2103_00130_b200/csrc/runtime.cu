@@ -412,13 +412,17 @@ uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaSt
 
 void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices, int64_t num_bags,
             const float* d_weights, float* d_out, int64_t ld_out, bool checked, uint8_t* d_flags, double* d_rsum,
-            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st) {
+            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st, const EbScatter* scatter) {
     if (num_bags < 0) throw std::invalid_argument("embedding_bag: negative bag count");
     if (num_bags == 0) {
         if (checked && d_flag_count) cuda_check(cudaMemsetAsync(d_flag_count, 0, 4, st), "cudaMemsetAsync");
         return;
     }
-    if (!d_offsets || !d_indices || !d_out) throw std::invalid_argument("null argument");
+    if (scatter) {
+        if (!scatter->out_dest || scatter->bags_per_dest <= 0 || (checked && !scatter->flag_dest))
+            throw std::invalid_argument("embedding_bag: invalid scatter destinations");
+    }
+    if (!d_offsets || !d_indices || (!d_out && !scatter)) throw std::invalid_argument("null argument");
     if (ld_out < t.dim) throw std::invalid_argument("embedding_bag: ld_out < dim");
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
@@ -441,6 +445,12 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     p.status = d_status;
     p.ws_flag_acc = ws.small + 4;
     p.ws_block_cnt = ws.small + 5;
+    if (scatter) {
+        p.out_dest = scatter->out_dest;
+        p.flag_dest = checked ? scatter->flag_dest : nullptr;
+        p.bags_per_dest = scatter->bags_per_dest;
+        p.flag_ld = scatter->flag_ld;
+    }
     const cudaError_t e = launch_eb_bags(t.elem, t.scale_type, p, checked, st);
     if (e == cudaErrorInvalidValue) throw std::invalid_argument("embedding_bag: unsupported dimension");
     cuda_check(e, "eb_bag_kernel");

@@ -42,9 +42,17 @@ void eb_table_rebuild(EbTable& t, int elem, const void* d_rows, int64_t rows, in
 void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st);
 // Number of rows whose stored sum differs from the recomputed one (synchronizes `st`).
 uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaStream_t st);
+// Destination table of the scatter mode (see EbParams): device arrays of per-destination pointers.
+struct EbScatter {
+    float* const* out_dest = nullptr;
+    uint8_t* const* flag_dest = nullptr;
+    int64_t bags_per_dest = 0;
+    int64_t flag_ld = 1;
+};
 void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices, int64_t num_bags,
             const float* d_weights, float* d_out, int64_t ld_out, bool checked, uint8_t* d_flags, double* d_rsum,
-            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st);
+            double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st,
+            const EbScatter* scatter = nullptr);
 int64_t eb_elem_row_bytes(int elem, int64_t dim);
 
 // ---- fault lab

@@ -173,6 +173,29 @@ def eb_csr(table: QuantEmbeddingTable, offsets, indices, weights=None, checked: 
     return out, flags, rsum, csum, cnt
 
 
+def eb_csr_scatter(table: QuantEmbeddingTable, offsets, indices, weights, out_dests, flag_dests, ld_out: int,
+                   flag_ld: int, bags_per_dest: int, stream=None) -> torch.Tensor:
+    """Checked lookups writing bag b to ``out_dests[b // bags_per_dest]`` row ``b % bags_per_dest`` (row
+    stride ``ld_out`` floats) and its flag to ``flag_dests[...]`` (stride ``flag_ld``): the sharded
+    exchange fused into the lookup kernel (abftlp_eb_checked_scatter). ``out_dests``/``flag_dests`` are
+    device tensors (views) whose first element is the destination base. Returns the flag count."""
+    off = to_device(offsets, torch.int64)
+    idx = to_device(indices, torch.int64)
+    w = None if weights is None else to_device(weights, torch.float32)
+    nb = int(off.numel()) - 1
+    dev = device()
+    optrs = torch.tensor([t.data_ptr() for t in out_dests], dtype=torch.int64, device=dev)
+    fptrs = torch.tensor([t.data_ptr() for t in flag_dests], dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("abftlp_eb_checked_scatter", table.handle, ptr(off), ptr(idx) if idx.numel() else C.c_void_p(8), nb,
+              ptr(w), ptr(optrs), ld_out, ptr(fptrs), flag_ld, bags_per_dest, ptr(cnt), ptr(status),
+              stream_handle(stream))
+    if int(status.item()) & 1:
+        raise IndexError("embedding_bag: index out of range")
+    return cnt
+
+
 def embedding_bag(table: QuantEmbeddingTable, bag: IndexBag) -> torch.Tensor:
     """Plain pooled lookup, fp32 accumulation (P:src/embedding_abft.cpp:47-60)."""
     off, idx, w = _csr([bag])

@@ -1,0 +1,75 @@
+"""GPU side of the sharding path: the scatter-mode lookup kernel (abftlp_eb_checked_scatter)
+writes every bag into its destination slot bit-identically to the plain kernel, and the sharded classes
+run on the CUDA library (world size 1 on the single test GPU; the multi-rank host logic is covered by
+tests/test_sharded.py with gloo)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _table(E, elem, R, d, seed, f16=False):
+    rng = np.random.default_rng(seed)
+    rb = d // 2 if elem == "u4" else d
+    lo, hi = (-128, 128) if elem == "s8" else (0, 256)
+    rows = rng.integers(lo, hi, (R, rb)).astype(np.int8 if elem == "s8" else np.uint8)
+    sdt = np.float16 if f16 else np.float32
+    sc = rng.uniform(1e-3, 1e-2, R).astype(sdt)
+    bi = rng.uniform(-1, 1, R).astype(sdt)
+    return rows, sc, bi, E.QuantEmbeddingTable(rows, sc, bi, elem=elem, dim=d)
+
+
+@pytest.mark.parametrize("elem,d,f16,weighted", [("u8", 128, False, False), ("u4", 64, True, True),
+                                                 ("s8", 40, False, True), ("s8", 256, False, False)])
+def test_scatter_kernel_matches_plain(elem, d, f16, weighted):
+    from paper_2103_00130_b200 import embedding as E
+    rows, sc, bi, t = _table(E, elem, 3000, d, 7, f16)
+    rng = np.random.default_rng(11)
+    G, Bg, Tg, slot = 3, 5, 2, 1
+    B = G * Bg
+    lens = rng.integers(0, 90, B)
+    lens[4] = 0
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    idx = rng.integers(0, 3000, off[-1]).astype(np.int64)
+    w = rng.uniform(0, 1, off[-1]).astype(np.float32) if weighted else None
+    out, flags, _, _, cnt = E.eb_csr(t, off, idx, w)
+    send = torch.full((G, Bg, Tg, d), float("nan"), dtype=torch.float32, device="cuda")
+    send_f = torch.full((G, Bg, Tg), 7, dtype=torch.uint8, device="cuda")
+    n = E.eb_csr_scatter(t, off, idx, w, [send[g, 0, slot] for g in range(G)], [send_f[g, 0, slot:] for g in range(G)],
+                         ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
+    got = send[:, :, slot].reshape(B, d)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), out.cpu().numpy().view(np.uint32))
+    assert np.array_equal(send_f[:, :, slot].reshape(B).cpu().numpy(), flags.cpu().numpy())
+    assert int(n.item()) == int(cnt.item())
+    # the other slot is untouched
+    assert torch.isnan(send[:, :, 0]).all() and (send_f[:, :, 0] == 7).all()
+    r_ref, _, _, e_ref = O.eb(rows, sc, bi, off, idx, w, elem=elem, dim=d)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), r_ref.view(np.uint32))
+
+
+def test_sharded_classes_world1():
+    from paper_2103_00130_b200 import embedding as E
+    from paper_2103_00130_b200 import sharded as S
+    a, b = O.gemm_inputs(20260823, 0, 96, 300, 256)
+    g = S.ShardedAbftGemm(torch.from_numpy(b).cuda(), 300)
+    r = g(a)
+    ct, fl, err = O.abft_gemm(a, b)
+    assert np.array_equal(r.cTemp.cpu().numpy(), ct) and r.errCount == err == 0
+    r2 = g(a, fault=(7, 300, 31))  # checksum column, sign bit
+    assert r2.errCount == 1 and int(r2.rowFlags[7].item()) == 1
+    T, B, d = 3, 8, 64
+    tables, bags, refs = {}, {}, {}
+    for t in range(T):
+        rows, sc, bi, tab = _table(E, "u8", 1000, d, 20 + t)
+        rng = np.random.default_rng(40 + t)
+        off = np.concatenate([[0], np.cumsum(rng.integers(0, 30, B))]).astype(np.int64)
+        idx = rng.integers(0, 1000, off[-1]).astype(np.int64)
+        tables[t], bags[t] = tab, (off, idx, None)
+        refs[t] = O.eb(rows, sc, bi, off, idx, None, elem="u8", dim=d)
+    out, flags = S.ShardedEmbeddingBags(tables, T, B, d)(bags)
+    for t in range(T):
+        assert np.array_equal(out[:, t].cpu().numpy().view(np.uint32), refs[t][0].view(np.uint32))
+        assert np.array_equal(flags[:, t].cpu().numpy(), refs[t][3])
