@@ -77,7 +77,9 @@ struct GemmParams {
     unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
 };
 
-enum EpiMode { kEpiTmaStore = 0, kEpiDirect = 2, kEpiNone = 4 };
+// C' write-out: TMA store of 32x32 chunks; coalesced st.global.v4 after a swizzled smem transpose
+// (keeps the SM's TMA engine free for the next tile's loads); scalar stores (unaligned C); none (bench).
+enum EpiMode { kEpiTmaStore = 0, kEpiStg = 1, kEpiDirect = 2, kEpiNone = 4 };
 
 struct GemmTiling {
     int bn, epi;

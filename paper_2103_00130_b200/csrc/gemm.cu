@@ -131,6 +131,8 @@ struct PairCfg {
 #endif
     static constexpr int KS = BN == 64 ? ABFT_KS64 : BN == 128 ? ABFT_KS128 : ABFT_KS256;
     static constexpr int kStagingBufs = ABFT_STAGING_BUFS;  // per epilogue warp
+    static constexpr int kProducers = 3;                   // TMA issuing warps: A lo, A hi, B'
+    static_assert(KS % 2 == 0, "the A stage is split in two K halves");
     static constexpr int kABytes = kBM * kBK;                // per CTA per k-block (its 128 rows of A)
     static constexpr int kBBytes = (BN / 2) * kBK;           // per CTA per k-block (its half of the B' tile)
     static constexpr int kStageBytes = KS * (kABytes + kBBytes);
@@ -145,7 +147,7 @@ struct PairCfg {
 };
 
 template <int BN, bool CHECKED, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
     using Cfg = PairCfg<BN>;
@@ -169,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], Cfg::kProducers);  // one expect_tx arrival per producer warp (leader)
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -183,22 +185,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
         if (EPI == kEpiTmaStore) tma_prefetch(&tmC);
-        // warm L2 with this pair's first stages (before griddep_wait: prefetches only touch L2)
-        if (pair < p.num_tiles) {
-            const int mt = pair / p.n_tiles, nt = pair - mt * p.n_tiles;
-            const int pre = kb_steps < STAGES ? kb_steps : STAGES;
-            for (int ks = 0; ks < pre; ++ks) {
-                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS);
-                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS);
-            }
-        }
     }
     // Barriers must be visible to the peer before any TMA / commit targets them; TMEM is allocated
     // afterwards by the MMA warp so the producer's first loads overlap the allocation.
     cluster_sync();
     if (trace && threadIdx.x == 0) trace[1] = globaltimer();
+    // warm L2 with this pair's first stages while the previous grid finishes (before griddep_wait:
+    // prefetches only touch L2, the point of coherence); one producer warp per operand part
+    if ((warp == 0 || warp >= 6) && lane == 0 && pair < p.num_tiles) {
+        const int role = warp == 0 ? 0 : warp - 5;
+        const int mt = pair / p.n_tiles, nt = pair - mt * p.n_tiles;
+        const int pre = kb_steps < STAGES ? kb_steps : STAGES;
+        const int rot = nt % kb_steps;
+        for (int ks0 = 0; ks0 < pre; ++ks0) {
+            const int ks = (ks0 + rot) % kb_steps;
+            if (role < 2)
+                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * (KS / 2));
+            else
+                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS);
+        }
+    }
     uint32_t tmem = 0;
-    if (warp >= 1) {
+    if (warp >= 1 && warp <= 5) {
         if (warp == 1) {
             tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
             tc_fence_before();
@@ -212,23 +220,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     // read and written (PDL: blocks until the previous grid on the stream has completed).
     griddep_wait();
 
-    if (warp == 0) {
-        // ---------------- TMA producer (both CTAs; completion counted on the leader's barrier)
+    if (warp == 0 || warp >= 6) {
+        // ---------------- TMA producers (both CTAs; completion counted on the leader's barrier). An SM
+        // serves the TMA requests of ONE issuing warp one after another (~275-300 ns each under load,
+        // scripts/pipe_bench9.cu), so the stage is split over three warps issuing in parallel:
+        // A k-blocks [0, KS/2), A k-blocks [KS/2, KS), and the B' slab.
         if (lane == 0) {
-            const uint64_t pol_b = policy_evict_last();  // weights are re-used across calls
-            const uint64_t pol_a = policy_evict_last();  // A is re-read by every N tile of the call
+            const int role = warp == 0 ? 0 : warp - 5;  // 0, 1: A halves; 2: B'
+            const uint64_t pol = policy_evict_last();   // A is re-read by every N tile, B' by every call
+            constexpr int KH = KS / 2;
+            constexpr uint32_t bytes[3] = {KH * Cfg::kABytes, (KS - KH) * Cfg::kABytes, KS * Cfg::kBBytes};
             int it = 0;
             for (int t = pair; t < p.num_tiles; t += npairs) {
                 const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-                for (int ks = 0; ks < kb_steps; ++ks, ++it) {
+                // Tiles of one M block read the same A rows; starting each tile at a different K step
+                // spreads those reads over all of A's L2 lines instead of hammering one k-block's lines
+                // (integer accumulation is exact, so the K order does not change the result).
+                const int rot = nt % kb_steps;
+                for (int ks0 = 0; ks0 < kb_steps; ++ks0, ++it) {
+                    const int ks = ks0 + rot < kb_steps ? ks0 + rot : ks0 + rot - kb_steps;
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
-                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
-                    tma_load_3d_pair(st, &tmA, &full[s], 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS, pol_a);
-                    tma_load_3d_pair(st + KS * Cfg::kABytes, &tmB, &full[s], 0,
-                                     nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS, pol_b);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes[role]);
+                    if (role < 2)
+                        tma_load_3d_pair(st + role * KH * Cfg::kABytes, &tmA, &full[s], 0,
+                                         mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * KH, pol);
+                    else
+                        tma_load_3d_pair(st + KS * Cfg::kABytes, &tmB, &full[s], 0,
+                                         nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS, pol);
                 }
             }
         }
@@ -249,6 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     if (trace && local == 0 && ks == 0) trace[2] = globaltimer();
+                    if (trace && local == 0 && ks >= 1 && ks <= 7) trace[8 + ks] = globaltimer();  // stage arrivals
                     const uint32_t a0 = smem_u32(smem + s * Cfg::kStageBytes);
                     const uint32_t b0 = a0 + KS * Cfg::kABytes;
 #pragma unroll
@@ -256,8 +278,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                         const uint64_t da = umma_desc_sw128(a0 + j * Cfg::kABytes);
                         const uint64_t db = umma_desc_sw128(b0 + j * Cfg::kBBytes);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 32; ++kk)  // UMMA K = 32 bytes for 8-bit operands
+                        for (int kk = 0; kk < kBK / 32; ++kk) {  // UMMA K = 32 bytes for 8-bit operands
+#ifndef ABFT_NO_MMA  // (experiment switch: pure load pipeline)
                             mma_i8_pair(d, da + 2 * kk, db + 2 * kk, idesc, (ks | j | kk) != 0 ? 1u : 0u);
+#endif
+                        }
                     }
                     mma_commit_pair(&empty[s]);  // frees the slot in both CTAs once these MMAs read it
                 }
@@ -331,6 +356,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                         bulk_commit();
                     }
                     ++chunk_ctr;
+                } else if constexpr (EPI == kEpiStg) {
+                    // transpose the warp's 32x32 chunk through its staging buffer so every store
+                    // instruction writes four full 128-byte row segments
+                    uint8_t* buf = staging + q * Cfg::kStagingBufs * 4096;
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq)
+                        *reinterpret_cast<uint4*>(buf + lane * 128 + ((qq ^ (lane & 7)) << 4)) =
+                            make_uint4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+                    __syncwarp();
+                    const int rsub = lane >> 3, cq = lane & 7;
+                    const int gcol = col0 + cq * 4;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = i * 4 + rsub;
+                        const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 128 + ((cq ^ (r & 7)) << 4));
+                        const int grow = row0 + r;
+                        if (grow < p.m && gcol < p.n) {
+                            int32_t* dst = p.c + static_cast<int64_t>(grow) * p.ldc + gcol;
+                            if (gcol + 3 < p.n) {
+                                *reinterpret_cast<uint4*>(dst) = val;
+                            } else {
+                                const uint32_t e4[4] = {val.x, val.y, val.z, val.w};
+                                for (int e = 0; e < 4 && gcol + e < p.n; ++e) dst[e] = static_cast<int32_t>(e4[e]);
+                            }
+                        }
+                    }
+                    __syncwarp();
                 } else if constexpr (EPI == kEpiDirect) {
                     if (row < p.m) {
                         int32_t* crow = p.c + static_cast<int64_t>(row) * p.ldc;
@@ -457,7 +509,7 @@ static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap
     static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -474,6 +526,7 @@ static cudaError_t launch_epi(int epi, int pairs, const CUtensorMap& a, const CU
     switch (epi) {
         case kEpiTmaStore: return launch_one<BN, CHECKED, kEpiTmaStore>(pairs, a, b, c, p, st);
         case kEpiNone: return launch_one<BN, CHECKED, kEpiNone>(pairs, a, b, c, p, st);
+        case kEpiStg: return launch_one<BN, CHECKED, kEpiStg>(pairs, a, b, c, p, st);
         default: return launch_one<BN, CHECKED, kEpiDirect>(pairs, a, b, c, p, st);
     }
 }

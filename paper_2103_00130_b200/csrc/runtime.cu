@@ -209,8 +209,11 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
     if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn[,epi]" tuning override
         int bn = 0, e = -1;
         const int got = std::sscanf(env, "%d,%d", &bn, &e);
-        if (got >= 1 && (bn == 64 || bn == 128 || bn == 256))
-            return {bn, (got == 2 && e == kEpiNone) ? kEpiNone : epi};
+        if (got >= 1 && (bn == 64 || bn == 128 || bn == 256)) {
+            if (got == 2 && e == kEpiNone) return {bn, kEpiNone};
+            if (got == 2 && (e == kEpiTmaStore || e == kEpiStg) && c_tma_ok) return {bn, e};
+            return {bn, epi};
+        }
     }
     GemmTiling best{64, epi};
     double best_cost = 1e300;
@@ -308,8 +311,9 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         p.fault_col = static_cast<int>(fault->col);
         p.fault_bit = static_cast<int>(fault->bit);
     }
+    // box = half a stage's k-blocks: two producer warps load the two halves in parallel
     const CUtensorMap map_a = make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
-                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_ks(t.bn));
+                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_ks(t.bn) / 2);
     CUtensorMap map_c;
     std::memset(&map_c, 0, sizeof(map_c));
     if (t.epi == kEpiTmaStore)

@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
             const uint32_t ph = (i / stages) & 1;
             mbar_wait(&full[s], ph);
             // release the slot in every CTA of the cluster
-            for (int r = 0; r < cs; ++r) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[s]), r));
+            if (cs == 1) mbar_arrive_local(&empty[s]);
+            else for (int r = 0; r < cs; ++r) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[s]), r));
         }
         out[blockIdx.x] = globaltimer() - t0;
     }

@@ -93,7 +93,7 @@ def test_shapes_bit_exact(G, m, n, k):
     assert check_against_oracle(G, a, b).errCount == 0
 
 
-@pytest.mark.parametrize("tiling", ["256", "128", "64", "256,2", "128,2", "64,2"])
+@pytest.mark.parametrize("tiling", ["256", "128", "64", "256,2", "128,2", "64,2", "256,1", "128,1", "64,1"])
 def test_g2_tilings_bit_exact(G, tiling, monkeypatch):
     """Every N-tile / split-K / epilogue variant gives the identical C' and verdicts."""
     monkeypatch.setenv("ABFTLP_GEMM_TILING", tiling)
