@@ -345,6 +345,12 @@ def run_gpu_arm(args, rank, world, dist):
     if rank != 0:
         return
     value = world * args.steps * JOB * OPS / (t_total * 1e-3) / 1e12
+    # DRAM traffic of the checked kernel from the committed ncu --set full capture (profiles/)
+    traffic, traffic_src = None, None
+    caps = sorted(REPO.glob("profiles/r*/ncu_gemm_g2_*.json"))
+    if caps:
+        cap = json.loads(caps[-1].read_text())
+        traffic, traffic_src = cap.get("traffic_bytes_per_launch"), str(caps[-1].relative_to(REPO))
     achieved = OPS / (kernel_us * 1e-6) / 1e12
     line = {
         "metric": "checked int8 GEMM TOPS", "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
@@ -361,7 +367,8 @@ def run_gpu_arm(args, rank, world, dist):
                 "d2h_bytes_per_step": (4 * M * N + 4 * M + M + 4) * e2e_runs,
                 "note": f"{e2e_runs} abftlp_gemm_checked_host calls (pinned host A in; C, csum, flags, count out)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["int8_tops"], "unit": "TOP/s",
-                     "frac": achieved / pk["int8_tops"], "traffic": None,
+                     "frac": achieved / pk["int8_tops"], "traffic": traffic, "traffic_unit": "bytes/launch",
+                     "traffic_source": traffic_src,
                      "kernel": "gemm_pair_kernel (checked)", "kernel_us": kernel_us,
                      "kernel_us_how": "timed-region device time / checked GEMM launches (CUDA events, max over ranks)",
                      "single_launch_us": single_launch_us,
