@@ -425,6 +425,13 @@ def eb_secondary(L, dev, st, vp, pk):
         ix = torch.from_numpy(idx).to(dev)
         tab = C.c_void_p()
         L.call("abftlp_eb_table_create", elem, vp(rows), R, d, row_b, st_t, vp(sc), vp(bi), None, st, C.byref(tab))
+        n_faults = 0
+        if name == "E4":  # BASELINE configs[3]: one random bit flip in 0.1% of the rows, after the row sums
+            vic = torch.from_numpy(rng.choice(R, R // 1000, replace=False).astype(np.int64)).to(dev)
+            fc = torch.from_numpy(rng.integers(0, d, R // 1000).astype(np.int64)).to(dev)
+            fbits = torch.from_numpy(rng.integers(0, 4, R // 1000).astype(np.int32)).to(dev)
+            L.call("abftlp_eb_table_flip_bits", tab, vp(vic), vp(fc), vp(fbits), R // 1000, None, st)
+            n_faults = R // 1000
         o = torch.empty((nb, d), dtype=torch.float32, device=dev)
         fl = torch.empty(nb, dtype=torch.uint8, device=dev)
         fb = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -448,11 +455,12 @@ def eb_secondary(L, dev, st, vp, pk):
                 if s >= 2:
                     ts.append(e0.elapsed_time(e1) * 1e3)
             res[checked] = statistics.median(ts)
+        flagged = int(fl.to(torch.int64).sum().item())
         L.lib.abftlp_eb_table_free(tab)
         gbs = alg / (res[True] * 1e-6) / 1e9
         out[name] = {"checked_us": res[True], "unchecked_us": res[False], "alg_bytes": alg, "alg_gbs": gbs,
                      "hbm_frac": gbs / pk["hbm_gbs"], "overhead_pct": 100 * (res[True] - res[False]) / res[False],
-                     "lookups": L_, "bags": nb}
+                     "lookups": L_, "bags": nb, "injected_row_faults": n_faults, "flagged_bags": flagged}
         del rows, sc, bi, off, ix, o, fl, fb
         torch.cuda.empty_cache()
     return out

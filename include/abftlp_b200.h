@@ -152,9 +152,17 @@ abftlp_status abftlp_flip_bit(void* d_ptr, uint32_t elem_bytes, uint64_t index, 
 abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uint64_t j,
                                           uint32_t bit, abftlp_stream stream);
 /* Flip bit (< element width) of table element (row, col) after row sums were computed
- * (inject_eb_table, P:src/fault_lab.cpp:139-166). Mutates the caller's row buffer. */
+ * (inject_eb_table, P:src/fault_lab.cpp:139-166). Mutates the caller's row buffer and the table's
+ * device-resident interleaved copy (the lookups read the latter). Rows changed by other means after
+ * abftlp_eb_table_create are not seen by the lookups: inject through these calls. */
 abftlp_status abftlp_eb_table_flip_bit(abftlp_eb_table* t, uint64_t row, uint64_t col,
                                        uint32_t bit, abftlp_stream stream);
+/* Batched table faults: flip bit d_bits[i] (< element width) of element (d_rows[i], d_cols[i]) for
+ * i < count (device arrays); repeated coordinates compose like sequential flips. Out-of-range entries
+ * are skipped and set bit 1 of *d_status (nullable). Same target as abftlp_eb_table_flip_bit. */
+abftlp_status abftlp_eb_table_flip_bits(abftlp_eb_table* t, const int64_t* d_rows, const int64_t* d_cols,
+                                        const int32_t* d_bits, uint64_t count, int32_t* d_status,
+                                        abftlp_stream stream);
 /* Seeded generators reproducing SplitMix64(seed, stream) draws off .. off+count-1
  * (P:src/rng.hpp:10-43): kind 0 = u8 next_below(256), 1 = s8 next_int(-128,127),
  * 2 = f32 (float)next_real(lo, hi), 3 = i64 next_below(bound). */

@@ -107,6 +107,7 @@ _SIGS = {
     "abftlp_flip_bit": (i32, [vp, u32, u64, u32, vp]),
     "abftlp_gemm_weight_flip_bit": (i32, [vp, u64, u64, u32, vp]),
     "abftlp_eb_table_flip_bit": (i32, [vp, u64, u64, u32, vp]),
+    "abftlp_eb_table_flip_bits": (i32, [vp, vp, vp, vp, u64, vp, vp]),
     "abftlp_generate": (i32, [vp, u64, u64, u64, u64, i32, f64, f64, u64, vp]),
     "abftlp_l2_flush": (i32, [vp, u64, i32, vp]),
 }

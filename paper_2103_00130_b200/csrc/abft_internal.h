@@ -108,11 +108,16 @@ struct EbTable {
     int64_t row_stride = 0;  // bytes between consecutive rows
     const uint8_t* data = nullptr;  // borrowed: caller keeps the rows alive
     void* meta = nullptr;           // owned: EbMetaF32[rows] or EbMetaF16[rows]
+    // owned interleaved copy (row bytes + metadata record in one 64-byte slot) when both fit: the
+    // lookups read this instead of (data, meta); nullptr otherwise
+    uint8_t* packed = nullptr;
+    int64_t rec_stride = 0, meta_off = 0, packed_cap = 0;
 };
 
 struct EbParams {
     const uint8_t* data;
     const void* meta;
+    int64_t meta_stride;  // bytes between consecutive metadata records
     int64_t rows, dim, row_stride;
     const int64_t* offsets;  // [num_bags + 1]
     const int64_t* indices;
@@ -127,6 +132,8 @@ struct EbParams {
     int32_t* status;       // nullable; bit 0 = index out of range
     uint32_t* ws_flag_acc;
     uint32_t* ws_block_cnt;
+    unsigned long long* ws_bag_ctr;  // persistent kernels' next-bag counter (self-resetting)
+    unsigned long long* trace;       // debug: per-warp timeline (16 slots), nullptr = off
     // scatter mode (table-wise sharded exchange fused into the lookups): when out_dest is set, bag b
     // writes out_dest[b / bags_per_dest] + (b % bags_per_dest) * ld_out and its flag to
     // flag_dest[b / bags_per_dest][(b % bags_per_dest) * flag_ld] (pointers may be NVLink peer memory)

@@ -395,6 +395,7 @@ CampaignReport run_eb_campaign(const CampaignConfig& cfg) {
                 flip_bit(cell, 0, draw_bit(rng, cfg.fault.bitRange, 8), st);
             else
                 set_random(cell, 8, rng.state, st);
+            eb_pack(table, st);  // the lookups read the interleaved copy; row sums stay pristine
         }
         eb_run(table, offsets.p, indices.p, batch, nullptr, out.p, d, true, flags.p, nullptr, nullptr, nullptr,
                nullptr, st);

@@ -4,6 +4,7 @@
 // Error model mirrors the reference's `guarded` (P:src/capi.cpp:28-41): invalid_argument and
 // out_of_range -> ABFTLP_ERR_INVALID_ARGUMENT, runtime_error -> ABFTLP_ERR_IO, anything else
 // (including CUDA failures) -> ABFTLP_ERR_INTERNAL; the message goes to a thread-local string.
+#include <cstdint>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -483,20 +484,19 @@ abftlp_status abftlp_eb_table_flip_bit(abftlp_eb_table* t, uint64_t row, uint64_
                                        abftlp_stream stream) {
     if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
-        const abftk::EbTable& T = *t->t;
-        if (row >= static_cast<uint64_t>(T.rows) || col >= static_cast<uint64_t>(T.dim))
+        if (row > static_cast<uint64_t>(INT64_MAX) || col > static_cast<uint64_t>(INT64_MAX))
             throw std::out_of_range("inject_eb_table: coordinates out of range");
-        const uint32_t width = T.elem == abftk::kEbU4 ? 4u : 8u;
-        if (bit >= width) throw std::out_of_range("flip_bit: bit index out of range");
-        uint64_t byte = row * static_cast<uint64_t>(T.row_stride);
-        uint32_t b = bit;
-        if (T.elem == abftk::kEbU4) {
-            byte += col / 2;
-            b += 4u * static_cast<uint32_t>(col & 1);
-        } else {
-            byte += col;
-        }
-        abftk::flip_bit(const_cast<uint8_t*>(T.data), byte, b, as_stream(stream));
+        abftk::eb_flip_bit(*t->t, static_cast<int64_t>(row), static_cast<int64_t>(col), bit, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_table_flip_bits(abftlp_eb_table* t, const int64_t* d_rows, const int64_t* d_cols,
+                                        const int32_t* d_bits, uint64_t count, int32_t* d_status,
+                                        abftlp_stream stream) {
+    if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_flip_bits(*t->t, d_rows, d_cols, d_bits, static_cast<int64_t>(count), d_status, as_stream(stream));
         return ABFTLP_OK;
     });
 }
@@ -515,6 +515,10 @@ abftlp_status abftlp_generate(void* d_out, uint64_t count, uint64_t seed, uint64
 // Debug: record 8 globaltimer stamps per GEMM CTA into d_trace (NULL disables). Not in the headers.
 __attribute__((visibility("default"))) void abftlp_debug_gemm_trace(unsigned long long* d_trace) {
     abftk::set_gemm_trace(d_trace);
+}
+// Debug: 16 globaltimer stamps per EmbeddingBag warp of the async kernel (NULL disables). Not in the headers.
+__attribute__((visibility("default"))) void abftlp_debug_eb_trace(unsigned long long* d_trace) {
+    abftk::set_eb_trace(d_trace);
 }
 
 abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream) {

@@ -24,6 +24,7 @@
 #include "ptx.cuh"
 
 namespace abftk {
+int device_sm_count();
 
 // Output row / flag slot of a bag: local buffers, or a destination table (sharded exchange, EbParams).
 __device__ __forceinline__ float* out_row(const EbParams& p, int64_t bag) {
@@ -80,14 +81,15 @@ __device__ __forceinline__ float decode(W w, int c) {
 }
 
 template <int SCALE>
-__device__ __forceinline__ void load_meta(const void* meta, int64_t i, float& s, float& b, int32_t& rs) {
+__device__ __forceinline__ void load_meta(const void* meta, int64_t i, int64_t stride, float& s, float& b, int32_t& rs) {
+    const uint8_t* rec = reinterpret_cast<const uint8_t*>(meta) + i * stride;
     if constexpr (SCALE == kEbF32) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(meta) + i);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(rec));
         s = __uint_as_float(v.x);
         b = __uint_as_float(v.y);
         rs = static_cast<int32_t>(v.z);
     } else {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(meta) + i);
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(rec));
         s = __half2float(__ushort_as_half(static_cast<unsigned short>(v.x & 0xFFFFu)));
         b = __half2float(__ushort_as_half(static_cast<unsigned short>(v.x >> 16)));
         rs = static_cast<int32_t>(v.y);
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
             // metadata of lookup (base + lane), overlapping the row gathers
             float my_s = 0.f, my_b = 0.f, my_w = 1.f;
             int32_t my_rs = 0;
-            if (valid) load_meta<SCALE>(p.meta, my_idx, my_s, my_b, my_rs);
+            if (valid) load_meta<SCALE>(p.meta, my_idx, p.meta_stride, my_s, my_b, my_rs);
             if constexpr (WEIGHTED) {
                 if (lane < cnt) my_w = p.weights[base + lane];
             }
@@ -325,19 +327,36 @@ __device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Chunk slots in flight per warp: deep enough that a whole E4-sized bag (<= 160 lookups) is gathered in
+// one round trip; fewer for wide slices (shared memory).
+template <int BPL>
+struct AsyncRing {
+    static constexpr int SLICE = 32 * BPL;
+#ifndef ABFT_EB_NST32
+#define ABFT_EB_NST32 6
+#endif
+#ifndef ABFT_EB_NST64
+#define ABFT_EB_NST64 4
+#endif
+    static constexpr int NST = SLICE <= 32 ? ABFT_EB_NST32 : SLICE <= 64 ? ABFT_EB_NST64 : SLICE <= 128 ? 3 : 2;
+};
 template <int BPL>
 struct AsyncStage {
-    uint8_t rows[2][kChunk][32 * BPL];  // this warp's column slice of each gathered row
-    uint4 meta[2][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B)
-    int64_t off[2][kChunk];             // row byte offset of the slice, -1 = skipped
-    float w[2][kChunk];
-    double term[kChunk];                // cSum terms of the chunk, summed in order by lane 0
+    static constexpr int NST = AsyncRing<BPL>::NST;
+    uint8_t rows[NST][kChunk][32 * BPL];  // this warp's column slice of each gathered row
+    uint4 meta[NST][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B); zero = neutral slot
+    float w[NST][kChunk];
+    int64_t off[kChunk];                  // row byte offsets of the chunk being issued, -1 = none
+    double term[kChunk];                  // cSum terms of the chunk, summed in order by lane 0
 };
 
 template <int SCALE>
@@ -361,194 +380,260 @@ __device__ __forceinline__ typename LaneWord<BPL>::T lds_word(const uint8_t* p) 
     else return *reinterpret_cast<const uint64_t*>(p);
 }
 
+// Small unsigned integer -> float without the (quarter-rate) I2F: splice v into the mantissa of 2^23 and
+// subtract 2^23 -- exact for v < 2^23. `bias` folds a constant offset into the same subtraction.
+__device__ __forceinline__ float splice_u2f(uint32_t v, float bias) {
+    return __fsub_rn(__uint_as_float(0x4B000000u | v), bias);
+}
+template <int ELEM, typename W>
+__device__ __forceinline__ float decode_fast(W w, int c) {
+    if constexpr (ELEM == kEbS8)  // int8 = (u8 ^ 0x80) - 128
+        return splice_u2f((static_cast<uint32_t>(w >> (8 * c)) & 0xFFu) ^ 0x80u, 8388608.0f + 128.0f);
+    else if constexpr (ELEM == kEbU8)
+        return splice_u2f(static_cast<uint32_t>(w >> (8 * c)) & 0xFFu, 8388608.0f);
+    else
+        return splice_u2f(static_cast<uint32_t>(w >> (4 * c)) & 0xFu, 8388608.0f);
+}
+
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
 __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
     constexpr int SLICE = 32 * BPL;        // bytes of a row this warp needs
     constexpr int PIECES = SLICE / 16;     // 16-B copies per row slice
     constexpr int PER_LANE = kChunk * PIECES / 32;
-    constexpr int BAGS = 8 / WPB;
+    constexpr int GROUPS = 8 / WPB;        // bag groups (WPB warps each) per block
     extern __shared__ __align__(16) uint8_t eb_smem[];
     AsyncStage<BPL>& S = reinterpret_cast<AsyncStage<BPL>*>(eb_smem)[threadIdx.x >> 5];
     __shared__ double part_sum[8];
     __shared__ int part_emax[8], part_umin[8];
+    __shared__ long long grp_bag[GROUPS];
     __shared__ uint32_t blk_flags;
     __shared__ uint32_t is_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int bag_local = warp / WPB, slice = warp % WPB;
-    const int64_t bag = static_cast<int64_t>(blockIdx.x) * BAGS + bag_local;
+    const int grp = warp / WPB, slice = warp % WPB;
     const int64_t slice_byte = static_cast<int64_t>(slice) * SLICE;
     const double dd = static_cast<double>(p.dim);
     if (threadIdx.x == 0) blk_flags = 0;
+    __syncthreads();
+    auto group_sync = [&]() {
+        if constexpr (WPB > 1)
+            named_bar_sync(1 + grp, 32 * WPB);
+        else
+            __syncwarp();
+    };
 
-    float acc[CPL];
+    // Persistent bag groups: each takes the next bag from a global counter, so long and short bags
+    // balance across SMs (the work per bag varies 150x in E4). The next bag id is requested while the
+    // current one is processed, hiding the atomic's round trip.
+    constexpr int NST = AsyncStage<BPL>::NST;
+    // The first bag of every group is static (its global group id); later ones come from the counter,
+    // offset by the number of groups -- 2k simultaneous atomics on one address at launch cost ~2.5 us.
+    const unsigned long long n_groups = static_cast<unsigned long long>(gridDim.x) * GROUPS;
+    auto fetch = [&]() -> unsigned long long {
+        unsigned long long b0 = 0;
+        if (slice == 0 && lane == 0) b0 = n_groups + atomicAdd(p.ws_bag_ctr, 1ull);
+        return b0;
+    };
+    auto share = [&](unsigned long long b0) -> int64_t {  // broadcast lane 0 / slice 0's id to the group
+        if constexpr (WPB == 1) {
+            return static_cast<int64_t>(__shfl_sync(0xffffffffu, b0, 0));
+        } else {
+            if (slice == 0 && lane == 0) grp_bag[grp] = static_cast<long long>(b0);
+            group_sync();
+            const int64_t v = grp_bag[grp];
+            group_sync();
+            return v;
+        }
+    };
+    unsigned long long* tr = p.trace ? p.trace + 16ull * (blockIdx.x * 8 + warp) : nullptr;
+    if (tr && lane == 0) tr[0] = globaltimer();
+    int nb_done = 0;
+    int64_t bag = static_cast<int64_t>(blockIdx.x) * GROUPS + grp;
+    while (bag < p.num_bags) {
+        const unsigned long long next_req = fetch();  // in flight while this bag is processed
+        if (tr && lane == 0 && nb_done < 4) tr[1 + 3 * nb_done] = globaltimer();
+
+        float acc[CPL];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
-    double csum = 0.0;
-    bool oob = false;
-    if (bag < p.num_bags) {
+        for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+        double csum = 0.0;
+        bool oob = false;
         const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
         const int nchunks = static_cast<int>((end - beg + kChunk - 1) / kChunk);
-        // issue the gathers of chunk `ch` into slot `sl` (indices in `ix`, weights loaded to `wv`)
-        auto issue = [&](int ch, int sl, int64_t ix, float& wv) {
-            const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
-            const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(p.rows);
-            if (lane < cnt && !valid) oob = true;
-            S.off[sl][lane] = valid ? ix * p.row_stride + slice_byte : -1;
-            if (valid) {
-                if constexpr (SCALE == kEbF32)
-                    cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint4*>(p.meta) + ix);
-                else
-                    cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint2*>(p.meta) + ix);
-            }
-            if constexpr (WEIGHTED) wv = lane < cnt ? p.weights[base + lane] : 1.0f;
-            __syncwarp();
+        // Issue the gathers of chunk `ch` (indices `ix`, one per lane) into ring slot ch % NST. Slots past
+        // the bag or out of range get a neutral record (scale = bias = 0, weight 1): they add +0.0, an
+        // exact no-op on the running sums (which start at +0.0 and never become -0.0 in round-to-nearest),
+        // so the consumer needs no per-lookup branch. Row pieces, metadata and weights all land through
+        // cp.async; one commit group per chunk (empty groups keep the count uniform).
+        auto issue = [&](int ch, int64_t ix) {
+            if (ch < nchunks) {
+                const int sl = ch % NST;
+                const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
+                const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+                const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(p.rows);
+                if (lane < cnt && !valid) oob = true;
+                S.off[lane] = valid ? ix * p.row_stride + slice_byte : -1;
+                if (valid) {
+                    if constexpr (SCALE == kEbF32)
+                        cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(p.meta) + ix * p.meta_stride);
+                    else
+                        cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(p.meta) + ix * p.meta_stride);
+                    if constexpr (WEIGHTED) cp_async4(&S.w[sl][lane], p.weights + base + lane);
+                } else {
+                    S.meta[sl][lane] = make_uint4(0u, 0u, 0u, 0u);
+                    if constexpr (WEIGHTED) S.w[sl][lane] = 1.0f;
+                }
+                __syncwarp();
 #pragma unroll
-            for (int i = 0; i < PER_LANE; ++i) {
-                const int piece = lane + 32 * i;
-                const int r = piece / PIECES, q = piece % PIECES;
-                const int64_t o = S.off[sl][r];
-                if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], p.data + o + q * 16);
+                for (int i = 0; i < PER_LANE; ++i) {
+                    const int piece = lane + 32 * i;
+                    const int r = piece / PIECES, q = piece % PIECES;
+                    const int64_t o = S.off[r];
+                    if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], p.data + o + q * 16);
+                }
+                __syncwarp();  // S.off is reused by the next issue
             }
             cp_async_commit();
         };
-        int64_t idx_next = (beg + lane < end) ? p.indices[beg + lane] : -1;
-        float w_slot[2] = {1.0f, 1.0f};
-        if (nchunks > 0) {
-            issue(0, 0, idx_next, w_slot[0]);
-            idx_next = (beg + kChunk + lane < end) ? p.indices[beg + kChunk + lane] : -1;
+        auto index_of = [&](int ch) -> int64_t {
+            const int64_t e = beg + static_cast<int64_t>(ch) * kChunk + lane;
+            return e < end ? p.indices[e] : -1;
+        };
+        // prologue: NST-1 chunks in flight, the index of the next one loaded ahead
+        {
+            int64_t ixs[NST - 1];
+#pragma unroll
+            for (int c = 0; c < NST - 1; ++c) ixs[c] = c < nchunks ? index_of(c) : -1;
+#pragma unroll
+            for (int c = 0; c < NST - 1; ++c) issue(c, ixs[c]);
         }
+        int64_t ix_ahead = NST - 1 < nchunks ? index_of(NST - 1) : -1;
         for (int ch = 0; ch < nchunks; ++ch) {
-            const int sl = ch & 1;
-            const bool more = ch + 1 < nchunks;
-            if (more) {
-                issue(ch + 1, sl ^ 1, idx_next, w_slot[sl ^ 1]);
-                const int64_t nb = beg + static_cast<int64_t>(ch + 2) * kChunk + lane;
-                idx_next = nb < end ? p.indices[nb] : -1;
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            if constexpr (WEIGHTED) S.w[sl][lane] = w_slot[sl];
+            const int sl = ch % NST;
+            issue(ch + NST - 1, ix_ahead);
+            ix_ahead = ch + NST < nchunks ? index_of(ch + NST) : -1;
+            cp_async_wait<NST - 1>();  // chunk ch has landed
             __syncwarp();
+            if (tr && lane == 0 && ch == 0 && nb_done < 4) tr[2 + 3 * nb_done] = globaltimer();
             const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
             const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
             if constexpr (CHECKED) {
-                if (slice == 0) {
-                    double my_term = 0.0;  // skipped / out-of-range lookups contribute nothing
-                    if (lane < cnt && S.off[sl][lane] >= 0) {
-                        float s, b;
-                        int32_t rs;
-                        smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
-                        my_term = csum_term(s, b, rs, WEIGHTED ? S.w[sl][lane] : 1.0f, dd, WEIGHTED);
-                    }
-                    S.term[lane] = my_term;
-                }
-            }
-            for (int t = 0; t < cnt; ++t) {
-                if (S.off[sl][t] >= 0) {  // warp-uniform
+                if (slice == 0) {  // neutral slots give an exact 0.0 term
                     float s, b;
                     int32_t rs;
-                    smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
-                    const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
-                    const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
+                    smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
+                    S.term[lane] = csum_term(s, b, rs, WEIGHTED ? S.w[sl][lane] : 1.0f, dd, WEIGHTED);
+                }
+            }
+            const int tmax = (cnt + 3) & ~3;  // slots cnt..tmax-1 are neutral
+#pragma unroll 4
+            for (int t = 0; t < tmax; ++t) {
+                float s, b;
+                int32_t rs;
+                smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
+                const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
+                const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
 #pragma unroll
-                    for (int c = 0; c < CPL; ++c) {
-                        float x = __fadd_rn(__fmul_rn(s, decode<ELEM>(word, c)), b);
-                        if constexpr (WEIGHTED) x = __fmul_rn(w, x);
-                        acc[c] = __fadd_rn(acc[c], x);
-                    }
+                for (int c = 0; c < CPL; ++c) {
+                    float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(word, c)), b);
+                    if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                    acc[c] = __fadd_rn(acc[c], x);
                 }
             }
             if constexpr (CHECKED) {
-                // the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), one lane;
-                // adding 0.0 for a skipped slot leaves the sum bit-identical (x + 0.0 == x)
+                // the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), one lane
                 __syncwarp();
                 if (slice == 0 && lane == 0) {
 #pragma unroll 8
                     for (int t = 0; t < cnt; ++t) csum = __dadd_rn(csum, S.term[t]);
                 }
             }
-            __syncwarp();  // slot `sl` may be refilled by the next issue
+            __syncwarp();  // slot `sl` may be refilled by a later issue
         }
+        cp_async_wait<0>();  // drain the (empty) trailing groups before the ring is reused
         csum = __shfl_sync(0xffffffffu, csum, 0);
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
         float* dst = out_row(p, bag) + slice * 32 * CPL + lane * CPL;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
-    }
-    if constexpr (CHECKED) {
-        int emax = -100000, umin = 100000;
+        if constexpr (CHECKED) {
+            int emax = -100000, umin = 100000;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) bit_span(acc[c], emax, umin);
-        double s = 0.0;
+            for (int c = 0; c < CPL; ++c) bit_span(acc[c], emax, umin);
+            double sm = 0.0;
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) s = __dadd_rn(s, static_cast<double>(acc[c]));
+            for (int c = 0; c < CPL; ++c) sm = __dadd_rn(sm, static_cast<double>(acc[c]));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
-            s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-        }
-        if (lane == 0) {
-            part_sum[warp] = s;
-            part_emax[warp] = emax;
-            part_umin[warp] = umin;
-        }
-        // only the WPB warps of this bag synchronise (their slices and global outputs are complete)
-        if constexpr (WPB > 1)
-            named_bar_sync(1 + bag_local, 32 * WPB);
-        else
-            __syncwarp();
-        if (slice == 0 && bag < p.num_bags) {
-            int E = -100000, U = 100000;
-            double exact = 0.0;
-#pragma unroll
-            for (int s2 = 0; s2 < WPB; ++s2) {
-                E = max(E, part_emax[warp + s2]);
-                U = min(U, part_umin[warp + s2]);
-                exact = __dadd_rn(exact, part_sum[warp + s2]);
+            for (int o = 16; o > 0; o >>= 1) {
+                emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+                umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+                sm = __dadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, o));
             }
-            double rsum;
-            if (E == -100000) {
-                rsum = 0.0;
-            } else if (E + 1 + log2d - U <= 53) {
-                rsum = exact;
-            } else {
-                rsum = 0.0;
-                const float* row = out_row(p, bag);
-                for (int j0 = 0; j0 < p.dim; j0 += 32) {
-                    const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
-                    for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
-                        rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, v, l)));
+            if (lane == 0) {
+                part_sum[warp] = sm;
+                part_emax[warp] = emax;
+                part_umin[warp] = umin;
+            }
+            // only the WPB warps of this bag synchronise (their slices and outputs are complete)
+            group_sync();
+            if (slice == 0) {
+                int E = -100000, U = 100000;
+                double exact = 0.0;
+#pragma unroll
+                for (int s2 = 0; s2 < WPB; ++s2) {
+                    E = max(E, part_emax[warp + s2]);
+                    U = min(U, part_umin[warp + s2]);
+                    exact = __dadd_rn(exact, part_sum[warp + s2]);
+                }
+                double rsum;
+                if (E == -100000) {
+                    rsum = 0.0;
+                } else if (E + 1 + log2d - U <= 53) {
+                    rsum = exact;  // every partial sum is exact, so any order gives the reference's value
+                } else {
+                    rsum = 0.0;  // the reference's sequential order over the stored outputs
+                    const float* row = out_row(p, bag);
+                    for (int j0 = 0; j0 < p.dim; j0 += 32) {
+                        const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
+                        for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
+                            rsum = __dadd_rn(rsum, static_cast<double>(__shfl_sync(0xffffffffu, v, l)));
+                    }
+                }
+                const double diff = fabs(__dsub_rn(rsum, csum));
+                const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
+                const int flag = diff > __dmul_rn(1e-5, mx);
+                if (lane == 0) {
+                    if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
+                    if (p.rsum) p.rsum[bag] = rsum;
+                    if (p.csum) p.csum[bag] = csum;
+                    if (flag) atomicAdd(&blk_flags, 1u);
                 }
             }
-            const double diff = fabs(__dsub_rn(rsum, csum));
-            const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
-            const int flag = diff > __dmul_rn(1e-5, mx);
-            if (lane == 0) {
-                if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
-                if (p.rsum) p.rsum[bag] = rsum;
-                if (p.csum) p.csum[bag] = csum;
-                if (flag) atomicAdd(&blk_flags, 1u);
-            }
+            group_sync();  // part_* may be rewritten by the group's next bag
         }
-        if (p.flag_count) {
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
-                __threadfence();
-                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
-            }
-            __syncthreads();
-            if (is_last && threadIdx.x == 0) {
-                __threadfence();
-                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
-                atomicExch(p.ws_block_cnt, 0u);
-            }
-        }
+        if (tr && lane == 0 && nb_done < 4) tr[3 + 3 * nb_done] = globaltimer();
+        ++nb_done;
+        bag = share(next_req);
+    }
+    if (tr && lane == 0) {
+        tr[13] = globaltimer();
+        tr[14] = nb_done;
+    }
+    // last block out publishes the flag count and resets the per-stream counters
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (CHECKED && blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
+        __threadfence();
+        is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t total = atomicExch(p.ws_flag_acc, 0u);
+        if (CHECKED && p.flag_count) *p.flag_count = total;
+        atomicExch(p.ws_block_cnt, 0u);
+        atomicExch(p.ws_bag_ctr, 0ull);
     }
 }
 
@@ -582,7 +667,7 @@ __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, i
                     oob = true;
                 } else {
                     my_idx = ix;
-                    load_meta<SCALE>(p.meta, ix, my_s, my_b, my_rs);
+                    load_meta<SCALE>(p.meta, ix, p.meta_stride, my_s, my_b, my_rs);
                 }
                 if constexpr (WEIGHTED) my_w = p.weights[base + lane];
             }
@@ -766,7 +851,14 @@ static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t s
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const unsigned blocks = static_cast<unsigned>((p.num_bags + (8 / WPB) - 1) / (8 / WPB));
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+        if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    }
+    const int64_t need = (p.num_bags + (8 / WPB) - 1) / (8 / WPB);
+    const int64_t cap = static_cast<int64_t>(per_sm) * device_sm_count();
+    const unsigned blocks = static_cast<unsigned>(need < cap ? need : cap);
     kern<<<blocks, 256, smem, st>>>(p, log2d);
     return cudaGetLastError();
 }
@@ -891,6 +983,76 @@ cudaError_t launch_eb_meta(int elem, int scale, const uint8_t* data, int64_t row
         else ABFT_META(kEbU4, kEbF16);
     }
 #undef ABFT_META
+    return cudaGetLastError();
+}
+
+// Interleaved record layout (EbTable::packed): row bytes, then the metadata record, in one 64-byte
+// slot per row, so a lookup is one 64-byte DRAM access instead of two scattered ones. One thread per
+// 16-byte piece of the record.
+__global__ void eb_pack_kernel(const uint8_t* __restrict__ data, int64_t rows, int64_t row_bytes, int64_t row_stride,
+                               const uint8_t* __restrict__ meta, int64_t meta_bytes, int64_t meta_off,
+                               int64_t rec_stride, uint8_t* __restrict__ packed) {
+    const int64_t pieces = rec_stride / 16;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pieces;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / pieces, q = e - r * pieces;
+        alignas(16) uint8_t buf[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int64_t o = q * 16 + i;
+            uint8_t v = 0;
+            if (o < row_bytes) v = data[r * row_stride + o];
+            else if (o >= meta_off && o < meta_off + meta_bytes) v = meta[r * meta_bytes + (o - meta_off)];
+            buf[i] = v;
+        }
+        *reinterpret_cast<uint4*>(packed + r * rec_stride + q * 16) = *reinterpret_cast<const uint4*>(buf);
+    }
+}
+
+cudaError_t launch_eb_pack(const uint8_t* data, int64_t rows, int64_t row_bytes, int64_t row_stride, const void* meta,
+                           int64_t meta_bytes, int64_t meta_off, int64_t rec_stride, uint8_t* packed, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    int64_t blocks = (rows * (rec_stride / 16) + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    eb_pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(data, rows, row_bytes, row_stride,
+                                                                  reinterpret_cast<const uint8_t*>(meta), meta_bytes,
+                                                                  meta_off, rec_stride, packed);
+    return cudaGetLastError();
+}
+
+// Batched table faults (fault lab): flip bit bits[i] (< element width) of element (rows[i], cols[i]) in
+// buffer a (row stride sa) and, when set, in buffer b (stride sb) -- 32-bit atomic XORs, so repeated
+// coordinates compose exactly as sequential flips. Out-of-range entries set bit 1 of *status.
+__global__ void flip_cells_kernel(uint8_t* a, int64_t sa, uint8_t* b, int64_t sb, const int64_t* __restrict__ rows,
+                                  const int64_t* __restrict__ cols, const int32_t* __restrict__ bits, int64_t n,
+                                  int64_t nrows, int64_t dim, int u4, int32_t* status) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = rows[i], c = cols[i];
+        const int32_t bt = bits[i];
+        if (r < 0 || r >= nrows || c < 0 || c >= dim || bt < 0 || bt >= (u4 ? 4 : 8)) {
+            if (status) atomicOr(status, 2);
+            continue;
+        }
+        const int64_t cb = u4 ? c / 2 : c;
+        const uint32_t bitpos = static_cast<uint32_t>(bt) + (u4 ? 4u * static_cast<uint32_t>(c & 1) : 0u);
+        const uint64_t oa = static_cast<uint64_t>(r * sa + cb);
+        atomicXor(reinterpret_cast<unsigned int*>(a + (oa & ~uint64_t{3})), (1u << bitpos) << (8 * (oa & 3)));
+        if (b) {
+            const uint64_t ob = static_cast<uint64_t>(r * sb + cb);
+            atomicXor(reinterpret_cast<unsigned int*>(b + (ob & ~uint64_t{3})), (1u << bitpos) << (8 * (ob & 3)));
+        }
+    }
+}
+
+cudaError_t launch_flip_cells(uint8_t* a, int64_t sa, uint8_t* b, int64_t sb, const int64_t* rows, const int64_t* cols,
+                              const int32_t* bits, int64_t n, int64_t nrows, int64_t dim, bool u4, int32_t* status,
+                              cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 1184) blocks = 1184;
+    flip_cells_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(a, sa, b, sb, rows, cols, bits, n, nrows, dim,
+                                                                     u4 ? 1 : 0, status);
     return cudaGetLastError();
 }
 

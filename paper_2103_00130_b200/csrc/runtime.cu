@@ -73,7 +73,7 @@ struct Workspace {
     int device = 0;
     unsigned long long* row_acc = nullptr;  // GEMM: per-row (A*cs share sum) << 32 | residue sum
     int64_t rows_cap = 0;
-    uint32_t* small = nullptr;  // [0..1] spare [2] verify acc [3] verify blocks [4] eb acc [5] eb blocks
+    uint32_t* small = nullptr;  // [2] verify acc [3] verify blocks [4] eb flag acc [5] eb blocks [6..7] eb bag counter (u64) [8..9] GEMM err_pack (u64) [12] eb validate count
     uint8_t* scratch = nullptr;  // A repack buffer
     size_t scratch_cap = 0;
     std::mutex mu;
@@ -113,6 +113,8 @@ static void grow(T*& ptr, int64_t& cap, int64_t need, cudaStream_t st) {
 // ------------------------------------------------------------------ GEMM
 static unsigned long long* g_trace = nullptr;  // debug: per-CTA phase timestamps
 void set_gemm_trace(unsigned long long* d_trace) { g_trace = d_trace; }
+static unsigned long long* g_eb_trace = nullptr;  // debug: per-warp EmbeddingBag timeline
+void set_eb_trace(unsigned long long* d_trace) { g_eb_trace = d_trace; }
 
 int gemm_ks(int bn);
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
@@ -336,6 +338,35 @@ void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum
 // ------------------------------------------------------------------ EmbeddingBag
 int64_t eb_elem_row_bytes(int elem, int64_t dim) { return elem == kEbU4 ? (dim + 1) / 2 : dim; }
 
+// Interleave each row with its metadata record into one 64-byte slot when both fit (e.g. int4 x 64 +
+// fp16 scale/bias + row sum = 40 B): a lookup then touches one DRAM burst instead of two scattered
+// ones. The copy is owned by the table; the caller's rows stay the reference copy for row sums.
+void eb_pack(EbTable& t, cudaStream_t st) {
+    const int64_t row_bytes = eb_elem_row_bytes(t.elem, t.dim);
+    const int64_t meta_bytes = t.scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16);
+    const int64_t meta_off = round_up(row_bytes, 16);
+    const bool want = meta_off + meta_bytes <= 64 && std::getenv("ABFTLP_EB_NOPACK") == nullptr;
+    const int64_t need = want ? 64 * t.rows : 0;
+    if (t.packed && (!want || need > t.packed_cap)) {
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        cudaFree(t.packed);
+        t.packed = nullptr;
+        t.packed_cap = 0;
+    }
+    if (!want) {
+        t.rec_stride = t.meta_off = 0;
+        return;
+    }
+    if (!t.packed) {
+        cuda_check(cudaMalloc(&t.packed, static_cast<size_t>(need)), "cudaMalloc(eb packed)");
+        t.packed_cap = need;
+    }
+    t.rec_stride = 64;
+    t.meta_off = meta_off;
+    cuda_check(launch_eb_pack(t.data, t.rows, row_bytes, t.row_stride, t.meta, meta_bytes, meta_off, 64, t.packed, st),
+               "eb_pack_kernel");
+}
+
 EbTable* eb_table_create(int elem, const void* d_rows, int64_t rows, int64_t dim, int64_t row_stride, int scale_type,
                          const void* d_scales, const void* d_biases, const int32_t* d_given_sums, cudaStream_t st) {
     if (elem < kEbS8 || elem > kEbU4) throw std::invalid_argument("eb_table_create: unknown element type");
@@ -356,6 +387,7 @@ EbTable* eb_table_create(int elem, const void* d_rows, int64_t rows, int64_t dim
         cuda_check(launch_eb_meta(elem, scale_type, t->data, rows, dim, row_stride, d_scales, d_biases, d_given_sums,
                                   t->meta, nullptr, nullptr, st),
                    "eb_meta_kernel");
+        eb_pack(*t, st);
     } catch (...) {
         eb_table_free(t);
         throw;
@@ -385,6 +417,7 @@ void eb_table_rebuild(EbTable& t, int elem, const void* d_rows, int64_t rows, in
     cuda_check(launch_eb_meta(elem, scale_type, t.data, rows, dim, row_stride, d_scales, d_biases, d_given_sums,
                               t.meta, nullptr, nullptr, st),
                "eb_meta_kernel");
+    eb_pack(t, st);
 }
 
 void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st) {
@@ -396,6 +429,7 @@ void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st) {
 void eb_table_free(EbTable* t) {
     if (!t) return;
     cudaFree(t->meta);
+    cudaFree(t->packed);
     delete t;
 }
 
@@ -403,7 +437,7 @@ uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaSt
     if (!d_given_sums) return 0;
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
-    uint32_t* cnt = ws.small + 8;
+    uint32_t* cnt = ws.small + 12;  // (own slot: [8..9] is the GEMM err_pack)
     cuda_check(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st), "cudaMemsetAsync");
     cuda_check(launch_eb_meta(t.elem, t.scale_type, t.data, t.rows, t.dim, t.row_stride, nullptr, nullptr, d_given_sums,
                               nullptr, nullptr, cnt, st),
@@ -431,11 +465,13 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
     EbParams p{};
-    p.data = t.data;
-    p.meta = t.meta;
+    p.data = t.packed ? t.packed : t.data;
+    p.meta = t.packed ? static_cast<const void*>(t.packed + t.meta_off) : t.meta;
+    p.meta_stride = t.packed ? t.rec_stride
+                             : static_cast<int64_t>(t.scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16));
     p.rows = t.rows;
     p.dim = t.dim;
-    p.row_stride = t.row_stride;
+    p.row_stride = t.packed ? t.rec_stride : t.row_stride;
     p.offsets = d_offsets;
     p.indices = d_indices;
     p.weights = d_weights;
@@ -449,6 +485,8 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     p.status = d_status;
     p.ws_flag_acc = ws.small + 4;
     p.ws_block_cnt = ws.small + 5;
+    p.ws_bag_ctr = reinterpret_cast<unsigned long long*>(ws.small + 6);
+    p.trace = g_eb_trace;
     if (scatter) {
         p.out_dest = scatter->out_dest;
         p.flag_dest = checked ? scatter->flag_dest : nullptr;
@@ -458,6 +496,29 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     const cudaError_t e = launch_eb_bags(t.elem, t.scale_type, p, checked, st);
     if (e == cudaErrorInvalidValue) throw std::invalid_argument("embedding_bag: unsupported dimension");
     cuda_check(e, "eb_bag_kernel");
+}
+
+void eb_flip_bit(EbTable& t, int64_t row, int64_t col, uint32_t bit, cudaStream_t st) {
+    if (row < 0 || row >= t.rows || col < 0 || col >= t.dim)
+        throw std::out_of_range("inject_eb_table: coordinates out of range");
+    const uint32_t width = t.elem == kEbU4 ? 4u : 8u;
+    if (bit >= width) throw std::out_of_range("flip_bit: bit index out of range");
+    const int64_t cb = t.elem == kEbU4 ? col / 2 : col;
+    const uint32_t b = bit + (t.elem == kEbU4 ? 4u * static_cast<uint32_t>(col & 1) : 0u);
+    // the caller's rows are borrowed const for the lookups; injection is the one sanctioned writer
+    cuda_check(launch_flip_bit(const_cast<uint8_t*>(t.data), static_cast<uint64_t>(row * t.row_stride + cb), b, st),
+               "flip_bit_kernel");
+    if (t.packed)
+        cuda_check(launch_flip_bit(t.packed, static_cast<uint64_t>(row * t.rec_stride + cb), b, st), "flip_bit_kernel");
+}
+
+void eb_flip_bits(EbTable& t, const int64_t* d_rows, const int64_t* d_cols, const int32_t* d_bits, int64_t n,
+                  int32_t* d_status, cudaStream_t st) {
+    if (n < 0) throw std::invalid_argument("inject_eb_table: negative count");
+    if (n > 0 && (!d_rows || !d_cols || !d_bits)) throw std::invalid_argument("null argument");
+    cuda_check(launch_flip_cells(const_cast<uint8_t*>(t.data), t.row_stride, t.packed, t.rec_stride, d_rows, d_cols,
+                                 d_bits, n, t.rows, t.dim, t.elem == kEbU4, d_status, st),
+               "flip_cells_kernel");
 }
 
 // ------------------------------------------------------------------ fault lab

@@ -40,6 +40,13 @@ void eb_table_rebuild(EbTable& t, int elem, const void* d_rows, int64_t rows, in
                       int scale_type, const void* d_scales, const void* d_biases, const int32_t* d_given_sums,
                       cudaStream_t st);
 void eb_row_sums(const EbTable& t, int32_t* d_out, cudaStream_t st);
+// (Re)build the table's interleaved row+metadata copy from the caller's rows and the stored metadata
+// (keeps the stored row sums: used after writing faults straight into the rows).
+void eb_pack(EbTable& t, cudaStream_t st);
+// Fault lab: flip table bits in the caller's rows and in the table's interleaved copy (if any).
+void eb_flip_bit(EbTable& t, int64_t row, int64_t col, uint32_t bit, cudaStream_t st);
+void eb_flip_bits(EbTable& t, const int64_t* d_rows, const int64_t* d_cols, const int32_t* d_bits, int64_t n,
+                  int32_t* d_status, cudaStream_t st);
 // Number of rows whose stored sum differs from the recomputed one (synchronizes `st`).
 uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaStream_t st);
 // Destination table of the scatter mode (see EbParams): device arrays of per-destination pointers.
@@ -70,6 +77,11 @@ cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t 
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,
                           uint8_t* flags, uint32_t* err_count, uint32_t* ws_acc, uint32_t* ws_blocks, cudaStream_t st);
 cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st);
+cudaError_t launch_eb_pack(const uint8_t* data, int64_t rows, int64_t row_bytes, int64_t row_stride, const void* meta,
+                           int64_t meta_bytes, int64_t meta_off, int64_t rec_stride, uint8_t* packed, cudaStream_t st);
+cudaError_t launch_flip_cells(uint8_t* a, int64_t sa, uint8_t* b, int64_t sb, const int64_t* rows, const int64_t* cols,
+                              const int32_t* bits, int64_t n, int64_t nrows, int64_t dim, bool u4, int32_t* status,
+                              cudaStream_t st);
 cudaError_t launch_eb_meta(int elem, int scale, const uint8_t* data, int64_t rows, int64_t dim, int64_t row_stride,
                            const void* scales, const void* biases, const int32_t* given_sums, void* meta,
                            int32_t* sums_out, uint32_t* mismatch, cudaStream_t st);
@@ -104,5 +116,6 @@ struct SplitMix64 {
 
 int device_sm_count();
 void set_gemm_trace(unsigned long long* d_trace);  // debug instrumentation (nullptr = off)
+void set_eb_trace(unsigned long long* d_trace);
 
 }  // namespace abftk

@@ -114,6 +114,19 @@ class QuantEmbeddingTable:
         """Corrupt element (row, col) after the row sums were taken (inject_eb_table's point)."""
         _lib.call("abftlp_eb_table_flip_bit", self._h, row, col, bit, stream_handle(stream))
 
+    def flip_bits(self, rows, cols, bits, stream=None) -> None:
+        """Batched inject_eb_table: flip bits[i] of element (rows[i], cols[i]) for every i, on the device."""
+        r = to_device(rows, torch.int64)
+        c = to_device(cols, torch.int64)
+        b = to_device(bits, torch.int32)
+        if not (r.numel() == c.numel() == b.numel()):
+            raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "flip_bits: length mismatch")
+        status = torch.zeros(1, dtype=torch.int32, device=device())
+        _lib.call("abftlp_eb_table_flip_bits", self._h, ptr(r), ptr(c), ptr(b), r.numel(), ptr(status),
+                  stream_handle(stream))
+        if int(status.item()) & 2:
+            raise IndexError("inject_eb_table: coordinates out of range")
+
 
 def precompute_row_sums(rows, elem: str = "s8", dim: int | None = None) -> torch.Tensor:
     """int32 per-row element sums (P:src/embedding_abft.cpp:39-45), computed on the device."""

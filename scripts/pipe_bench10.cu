@@ -1,0 +1,86 @@
+// Microbenchmark 10: random-record gather rate from HBM (the E3/E4 EmbeddingBag access pattern).
+// N random record indices into a table far larger than L2; each record (rec bytes) is read with 16-B
+// loads by rec/16 consecutive lanes; U records per lane-group in flight. L2 flushed (read) before each rep.
+//   usage: pipe_bench10 rec_bytes rows n U
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+__global__ void flush(const int4* buf, long long n, int* sink) {
+    int acc = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc ^= __ldcg(buf + i).x;
+    if (acc == 0x12345678) *sink = acc;
+}
+
+template <int U>
+__global__ void gather(const uint4* __restrict__ tab, const long long* __restrict__ idx, long long n, int rec16,
+                       unsigned* sink) {
+    const int lanes_per_rec = rec16;
+    const long long groups_total = ((long long)gridDim.x * blockDim.x) / lanes_per_rec;
+    const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / lanes_per_rec;
+    const int part = threadIdx.x % lanes_per_rec;
+    unsigned acc = 0;
+    for (long long base = g0; base < n; base += groups_total * U) {
+        uint4 v[U];
+        long long r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long e = base + u * groups_total;
+            r[u] = e < n ? idx[e] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldg(tab + r[u] * rec16 + part);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].w;
+    }
+    if (acc == 0x9e3779b9u) *sink = acc;
+}
+
+int main(int argc, char** argv) {
+    const int rec = atoi(argv[1]);
+    const long long rows = atoll(argv[2]), n = atoll(argv[3]);
+    const int U = atoi(argv[4]);
+    const int rec16 = rec / 16;
+    uint4* tab;
+    cudaMalloc(&tab, rows * rec);
+    cudaMemset(tab, 1, rows * rec);
+    std::vector<long long> h(n);
+    unsigned long long x = 88172645463325252ull;
+    for (long long i = 0; i < n; ++i) {
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+        h[i] = (long long)(x % (unsigned long long)rows);
+    }
+    long long* idx;
+    cudaMalloc(&idx, n * 8);
+    cudaMemcpy(idx, h.data(), n * 8, cudaMemcpyHostToDevice);
+    int4* fb;
+    cudaMalloc(&fb, 256 << 20);
+    cudaMemset(fb, 0, 256 << 20);
+    unsigned* sink;
+    cudaMalloc(&sink, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        flush<<<148 * 8, 256>>>(fb, (256 << 20) / 16, (int*)sink);
+        cudaEventRecord(e0);
+        const int blocks = 148 * 8;
+        if (U == 1) gather<1><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        else if (U == 2) gather<2><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        else if (U == 4) gather<4><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        else gather<8><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    const double us = best * 1e3;
+    printf("rec %4d B, %lld random of %lld rows, U=%d: %7.2f us  %6.2f rec/ns  %7.1f GB/s useful  (%s)\n", rec, n, rows, U,
+           us, n / us / 1e3, n * (double)rec / us / 1e3, cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}

@@ -29,6 +29,11 @@ if cfg == "E3":
 else:
     R, d, nb, elem, sct = 8_000_000, 64, 4096, 2, 1
     lens = rng.integers(1, 151, nb)
+    if cfg == "E4fixed":  # same total lookups, every bag the mean length (load-balance probe)
+        lens = np.full(nb, int(round(lens.mean())))
+    if cfg == "E4short":  # same total lookups in 4x as many 4x shorter bags
+        nb = nb * 4
+        lens = np.full(nb, int(round(lens.mean() / 4)))
     idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
     w = torch.from_numpy(rng.uniform(0, 1, int(lens.sum())).astype(np.float32)).to(dev)
     rb = d // 2

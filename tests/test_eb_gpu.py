@@ -164,13 +164,10 @@ def test_baseline_configs_full_size(E, cfg):
     bits = rng.integers(0, width, len(victims))
     for r_, c_, b_ in zip(victims[:64], cols[:64], bits[:64]):  # through the C ABI injector
         t.flip_bit(int(r_), int(c_), int(b_))
-    # the rest in one vectorised XOR on the same (borrowed) device rows
-    vr, vc, vb = victims[64:], cols[64:], bits[64:]
-    byte = vc // 2 if elem == "u4" else vc
-    mask = (1 << (vb + (4 * (vc & 1) if elem == "u4" else 0))).astype(np.uint8)
-    rows_t[torch.from_numpy(vr).cuda(), torch.from_numpy(byte).cuda()] ^= torch.from_numpy(mask).cuda()
+    # the rest through the batched device injector (abftlp_eb_table_flip_bits)
+    t.flip_bits(victims[64:], cols[64:], bits[64:])
     torch.cuda.synchronize()
-    rows2 = rows_t.cpu().numpy()
+    rows2 = rows_t.cpu().numpy()  # the injector also mutates the caller's (borrowed) rows
     sums = O.row_sums(rows, elem, d)
     ref2 = O.eb(rows2, sc, bi, off, idx, w, elem=elem, dim=d, row_sums_=sums)
     out2, flags2, rsum2, csum2, _ = E.eb_csr(t, off, idx, w)
