@@ -86,6 +86,37 @@ abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t ld
                                        int32_t* csum, uint8_t* row_flags, uint32_t* err_count,
                                        abftlp_stream stream);
 
+/* ------------------------------------------------------------------ requantization */
+/* RequantParams (P:src/quant.hpp:24-32): out = clamp(round_half_away((cf - biasC) / scaleC), 0, 255) with
+ * cf = scaleA*scaleB*C + scaleA*biasB*rowSumA[i] + scaleB*biasA*colSumB[j] + k*biasA*biasB, all in
+ * double in the reference's order (P:src/quant.cpp:77-102); bit-identical results. */
+typedef struct {
+    double scaleA, biasA, scaleB, biasB, scaleC, biasC;
+    uint64_t k;
+} abftlp_requant_params;
+
+/* Checked GEMM with the requantization fused into the epilogue: u8 d_out (m x n, ld_out) =
+ * requantize(C') with the checksum column excluded, computed from the tile in TMEM after any injected C'
+ * fault, plus the usual verdicts. d_c may be NULL (no int32 C' written; csum/flags still produced).
+ * scaleC <= 0 -> ABFTLP_ERR_INVALID_ARGUMENT ("requantize: scaleC must be positive"). */
+abftlp_status abftlp_gemm_checked_requant(const uint8_t* d_a, uint64_t m, uint64_t lda,
+                                          const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
+                                          int32_t* d_csum, uint64_t csum_ld, uint8_t* d_row_flags,
+                                          uint32_t* d_err_count, const abftlp_fault* fault,
+                                          const int32_t* d_row_sum_a, const int32_t* d_col_sum_b,
+                                          const abftlp_requant_params* params, uint8_t* d_out,
+                                          uint64_t ld_out, abftlp_stream stream);
+/* Standalone requantize over an existing C' (first n columns of each row; a checksum column is never
+ * read). Replaces requantize (P:src/quant.cpp:77-102). */
+abftlp_status abftlp_requantize(const int32_t* d_c, uint64_t ldc, uint64_t m, uint64_t n,
+                                const int32_t* d_row_sum_a, const int32_t* d_col_sum_b,
+                                const abftlp_requant_params* params, uint8_t* d_out, uint64_t ld_out,
+                                abftlp_stream stream);
+/* row_sums(A) for u8 A (P:src/quant.cpp:104-110) and col_sums(B) of an encoded weight (P:src/quant.cpp:112-118). */
+abftlp_status abftlp_row_sums_u8(const uint8_t* d_a, uint64_t m, uint64_t k, uint64_t lda, int32_t* d_out,
+                                 abftlp_stream stream);
+abftlp_status abftlp_gemm_weight_col_sums(const abftlp_gemm_weight* w, int32_t* d_out, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ EmbeddingBag */
 typedef struct abftlp_eb_table_s abftlp_eb_table;
 

@@ -602,3 +602,36 @@ int orc_abft_gemm_parallel(const uint8_t* a, size_t m, size_t k, const int8_t* b
     free(reps);
     return 0;
 }
+
+/* ------------------------------------------------------------ requantization (P:src/quant.cpp:10-14, 77-118)
+ * params = {scaleA, biasA, scaleB, biasB, scaleC, biasC} (RequantParams, P:src/quant.hpp:24-32), k separate.
+ * cf = sA*sB*c + sA*bB*rowSumA[i] + sB*bA*colSumB[j] + k*bA*bB in the reference's left-to-right double
+ * order; out = clamp(round_half_away((cf - bC) / sC), 0, 255). Columns >= n (a checksum column) are never
+ * read. Returns -1 (invalid_argument) when scaleC <= 0. */
+static double round_half_away(double x) { return x >= 0.0 ? floor(x + 0.5) : ceil(x - 0.5); }
+int orc_requantize(const int32_t* c, size_t ldc, size_t m, size_t n, const int32_t* row_sum_a,
+                   const int32_t* col_sum_b, const double* prm, uint64_t k, uint8_t* out, size_t ld_out) {
+    const double sA = prm[0], bA = prm[1], sB = prm[2], bB = prm[3], sC = prm[4], bC = prm[5];
+    if (!(sC > 0.0)) return -1;
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            const double cf = sA * sB * (double)c[i * ldc + j] + sA * bB * (double)row_sum_a[i] +
+                              sB * bA * (double)col_sum_b[j] + (double)k * bA * bB;
+            double r = round_half_away((cf - bC) / sC);
+            r = r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
+            out[i * ld_out + j] = (uint8_t)r;
+        }
+    return 0;
+}
+void orc_row_sums_u8(const uint8_t* a, size_t m, size_t k, size_t lda, int32_t* out) {
+    for (size_t i = 0; i < m; ++i) {
+        int32_t s = 0;
+        for (size_t p = 0; p < k; ++p) s += (int32_t)a[i * lda + p];
+        out[i] = s;
+    }
+}
+void orc_col_sums_i8(const int8_t* b, size_t k, size_t n, size_t ldb, int32_t* out) {
+    for (size_t j = 0; j < n; ++j) out[j] = 0;
+    for (size_t i = 0; i < k; ++i)
+        for (size_t j = 0; j < n; ++j) out[j] += (int32_t)b[i * ldb + j];
+}

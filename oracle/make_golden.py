@@ -18,6 +18,7 @@ REPO = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(REPO / "tests"))
 import oracle_api as O  # noqa: E402
 from campaign_configs import CAMPAIGNS  # noqa: E402
+from golden_cases import requant_inputs  # noqa: E402
 
 OUT = REPO / "tests" / "golden"
 P = O.P
@@ -145,12 +146,24 @@ def rng_golden(R):
     return out
 
 
+def requant_golden(R):
+    out = []
+    for seed in range(24):
+        m, n, k, c, rs, cs, prm = requant_inputs(seed)
+        q = np.empty((m, n), np.uint8)
+        rc = R.ref_requantize(P(c), sz(m), sz(n), C.c_int(1), P(rs), P(cs), P(prm), C.c_uint64(k), P(q))
+        assert rc == 0
+        out.append({"seed": seed, "m": m, "n": n, "k": k, "out": q.reshape(-1).tolist()})
+    return out
+
+
 def main():
     R = O.ref()
     if R is None:
         sys.exit("oracle/_ref/libabftlp_ref.so missing: run `make -C oracle ref` where /root/reference exists")
     OUT.mkdir(parents=True, exist_ok=True)
-    for name, fn in [("rng", rng_golden), ("gemm", gemm_golden), ("eb", eb_golden), ("campaigns", campaigns_golden)]:
+    for name, fn in [("rng", rng_golden), ("gemm", gemm_golden), ("eb", eb_golden), ("campaigns", campaigns_golden),
+                     ("requant", requant_golden)]:
         data = {"generator": "oracle/make_golden.py", "source": "reference built from /root/reference/proj/src",
                 "cases": fn(R)}
         (OUT / f"{name}.json").write_text(json.dumps(data, indent=1) + "\n")

@@ -13,6 +13,7 @@
 //   precompute_row_sums, abft_embedding_bag src/embedding_abft.hpp:38-47
 //   inject_weight_B / _intermediate_C / _eb_table  src/fault_lab.hpp:101-106
 //   SplitMix64                              src/rng.hpp:10-43
+//   requantize, row_sums, col_sums          src/quant.hpp:24-71
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -23,6 +24,7 @@
 #include "embedding_abft.hpp"
 #include "fault_lab.hpp"
 #include "gemm_abft.hpp"
+#include "quant.hpp"
 #include "rng.hpp"
 
 using namespace abft;
@@ -261,4 +263,27 @@ int ref_inject_eb_table(int8_t* rows, size_t R, size_t d, const uint64_t* offset
     });
 }
 
+
+int ref_requantize(const int32_t* c, size_t m, size_t n, int with_cs, const int32_t* rs, const int32_t* cs,
+                   const double* prm, uint64_t k, uint8_t* out) {
+    return guard([&] {
+        quant::IntermediateMatrix im;
+        const size_t cols = n + (with_cs ? 1 : 0);
+        im.data = MatI32(m, cols, std::vector<int32_t>(c, c + m * cols));
+        im.hasChecksumColumn = with_cs != 0;
+        quant::RequantParams p{prm[0], prm[1], prm[2], prm[3], prm[4], prm[5], static_cast<std::size_t>(k)};
+        quant::QuantU8 q = quant::requantize(im, std::vector<int32_t>(rs, rs + m), std::vector<int32_t>(cs, cs + n), p);
+        std::memcpy(out, q.data.data().data(), m * n);
+    });
+}
+
+void ref_row_sums_u8(const uint8_t* a, size_t m, size_t k, int32_t* out) {
+    auto v = quant::row_sums(MatU8(m, k, std::vector<uint8_t>(a, a + m * k)));
+    std::memcpy(out, v.data(), m * 4);
+}
+
+void ref_col_sums_i8(const int8_t* b, size_t k, size_t n, int32_t* out) {
+    auto v = quant::col_sums(MatI8(k, n, std::vector<int8_t>(b, b + k * n)));
+    std::memcpy(out, v.data(), n * 4);
+}
 }  // extern "C"

@@ -22,6 +22,7 @@ from .fault_lab import (BitRange, Campaign, CampaignReport, FaultModel, FaultRec
                         inject_eb_table, inject_intermediate_C, inject_weight_B, run_campaign)
 from .gemm import (AbftGemmResult, IntermediateMatrix, PackedEncodedWeight, WeightChecksum,  # noqa: F401
                    abft_gemm, compute_row_checksums, kChecksumMod, mod127, plain_gemm, verify_checksums)
+from .quant import RequantParams, abft_gemm_requant, col_sums, requantize, row_sums  # noqa: F401
 from .rng import SplitMix64  # noqa: F401
 
 __version__ = "0.1.0"

@@ -62,6 +62,12 @@ class BenchResult(C.Structure):
     _fields_ = [("baseline_ns", f64), ("abft_ns", f64), ("overhead_fraction", f64)]
 
 
+class RequantParams(C.Structure):
+    """abftlp_requant_params (RequantParams, P:src/quant.hpp:24-32)."""
+    _fields_ = [("scaleA", C.c_double), ("biasA", C.c_double), ("scaleB", C.c_double), ("biasB", C.c_double),
+                ("scaleC", C.c_double), ("biasC", C.c_double), ("k", C.c_uint64)]
+
+
 class Fault(C.Structure):
     _fields_ = [("active", i32), ("row", u64), ("col", u64), ("bit", u32)]
 
@@ -103,6 +109,10 @@ _SIGS = {
     "abftlp_eb_table_row_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_checked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp, vp, vp, vp, vp]),
     "abftlp_eb_unchecked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp]),
+    "abftlp_gemm_checked_requant": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),
+    "abftlp_requantize": (i32, [vp, u64, u64, u64, vp, vp, vp, vp, u64, vp]),
+    "abftlp_row_sums_u8": (i32, [vp, u64, u64, u64, vp, vp]),
+    "abftlp_gemm_weight_col_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_checked_scatter": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, u64, u64, vp, vp, vp]),
     "abftlp_flip_bit": (i32, [vp, u32, u64, u32, vp]),
     "abftlp_gemm_weight_flip_bit": (i32, [vp, u64, u64, u32, vp]),

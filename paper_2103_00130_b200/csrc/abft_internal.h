@@ -54,6 +54,11 @@ constexpr unsigned long long kRowAccCountMask = 0xFFFull;
 constexpr unsigned long long kRowAccResMask = (1ull << kRowAccCountShift) - 1;
 constexpr int kMaxCheckedNTiles = 4095;
 
+// RequantParams (P:src/quant.hpp:24-32) as the device sees it (k as a double, as the reference casts it).
+struct RequantDev {
+    double sA, bA, sB, bB, sC, bC, k;
+};
+
 struct GemmParams {
     int m, n, k;       // logical sizes (n excludes the checksum column)
     int k_blocks;      // 128-byte K blocks
@@ -72,6 +77,12 @@ struct GemmParams {
     // self-resetting per-stream workspace
     unsigned long long* row_acc;  // [m] see kRowAcc*: A*cs share sum | tile arrivals | residue sum
     unsigned long long* err_pack; // [1] (finished rows) << 32 | (flagged rows so far)
+    // fused requantization (rq_out != nullptr): u8 C_I = requantize(C') with the checksum column excluded
+    const int32_t* rq_row_sum_a;  // [m]
+    const int32_t* rq_col_sum_b;  // [n]
+    uint8_t* rq_out;
+    int64_t rq_ld;
+    RequantDev rq;
     // in-epilogue fault hook (P:src/fault_lab.cpp:192-195 semantics): flip `bit` of C'(row, col)
     int fault_active, fault_row, fault_col, fault_bit;
     unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA

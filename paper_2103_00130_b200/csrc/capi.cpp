@@ -319,6 +319,74 @@ abftlp_status abftlp_gemm_checked(const uint8_t* d_a, uint64_t m, uint64_t lda, 
     });
 }
 
+static abftk::RequantDev to_dev(const abftlp_requant_params* p) {
+    abftk::RequantDev q{};
+    q.sA = p->scaleA;
+    q.bA = p->biasA;
+    q.sB = p->scaleB;
+    q.bB = p->biasB;
+    q.sC = p->scaleC;
+    q.bC = p->biasC;
+    q.k = static_cast<double>(p->k);
+    return q;
+}
+
+abftlp_status abftlp_gemm_checked_requant(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w,
+                                          int32_t* d_c, uint64_t ldc, int32_t* d_csum, uint64_t csum_ld,
+                                          uint8_t* d_row_flags, uint32_t* d_err_count, const abftlp_fault* fault,
+                                          const int32_t* d_row_sum_a, const int32_t* d_col_sum_b,
+                                          const abftlp_requant_params* params, uint8_t* d_out, uint64_t ld_out,
+                                          abftlp_stream stream) {
+    if (!w || !params) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::Fault f;
+        if (fault && fault->active) {
+            f.active = true;
+            f.row = static_cast<int64_t>(fault->row);
+            f.col = static_cast<int64_t>(fault->col);
+            f.bit = fault->bit;
+        }
+        abftk::RequantArgs rq;
+        rq.row_sum_a = d_row_sum_a;
+        rq.col_sum_b = d_col_sum_b;
+        rq.params = to_dev(params);
+        rq.out = d_out;
+        rq.ld_out = static_cast<int64_t>(ld_out);
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    true, d_csum, static_cast<int64_t>(csum_ld), d_row_flags, d_err_count, &f, as_stream(stream),
+                    nullptr, &rq);
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_requantize(const int32_t* d_c, uint64_t ldc, uint64_t m, uint64_t n, const int32_t* d_row_sum_a,
+                                const int32_t* d_col_sum_b, const abftlp_requant_params* params, uint8_t* d_out,
+                                uint64_t ld_out, abftlp_stream stream) {
+    if (!params) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::requantize(d_c, static_cast<int64_t>(ldc), static_cast<int64_t>(m), static_cast<int64_t>(n), d_row_sum_a,
+                          d_col_sum_b, to_dev(params), d_out, static_cast<int64_t>(ld_out), as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_row_sums_u8(const uint8_t* d_a, uint64_t m, uint64_t k, uint64_t lda, int32_t* d_out,
+                                 abftlp_stream stream) {
+    return guarded([&] {
+        abftk::row_sums_u8(d_a, static_cast<int64_t>(m), static_cast<int64_t>(k), static_cast<int64_t>(lda), d_out,
+                           as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_weight_col_sums(const abftlp_gemm_weight* w, int32_t* d_out, abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::weight_col_sums(*w->w, d_out, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_gemm_unchecked(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w,
                                     int32_t* d_c, uint64_t ldc, abftlp_stream stream) {
     if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");

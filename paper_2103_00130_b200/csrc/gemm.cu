@@ -26,6 +26,7 @@
 
 #include "abft_internal.h"
 #include "ptx.cuh"
+#include "requant.cuh"
 
 namespace abftk {
 
@@ -327,6 +328,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
                         if (p.fault_col == col0 + j) v[j] ^= 1u << p.fault_bit;
+                }
+                if (p.rq_out != nullptr && row < p.m) {
+                    // fused requantization of this row's 32 columns (the checksum column is never part
+                    // of C, so it is excluded by construction), after any injected C' fault
+                    const RequantConsts rk = requant_consts(p.rq);
+                    const int32_t rsa = p.rq_row_sum_a[row];
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4) pk[q4] = 0u;
+#pragma unroll 4
+                    for (int j = 0; j < 32; ++j)
+                        if (col0 + j < p.n)
+                            pk[j >> 2] |= requant_one(static_cast<int32_t>(v[j]), rsa, __ldg(p.rq_col_sum_b + col0 + j), rk)
+                                          << (8 * (j & 3));
+                    uint8_t* dst = p.rq_out + static_cast<int64_t>(row) * p.rq_ld + col0;
+                    if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        reinterpret_cast<uint4*>(dst)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    } else {
+                        for (int j = 0; j < 32 && col0 + j < p.n; ++j)
+                            dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
+                    }
                 }
                 if constexpr (CHECKED) {
                     if (col0 + 32 <= p.n) {

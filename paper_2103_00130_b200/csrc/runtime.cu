@@ -236,9 +236,14 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
 
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
-          cudaStream_t st, const GemmTiling* force) {
+          cudaStream_t st, const GemmTiling* force, const RequantArgs* rq) {
     if (m < 0) throw std::invalid_argument("abft_gemm: negative m");
-    if (m > 0 && (!d_a || !d_c)) throw std::invalid_argument("null argument");
+    if (m > 0 && (!d_a || (!d_c && !rq))) throw std::invalid_argument("null argument");
+    if (rq) {
+        check_requant_params(rq->params);
+        if (m > 0 && (!rq->row_sum_a || !rq->col_sum_b || !rq->out)) throw std::invalid_argument("null argument");
+        if (rq->ld_out < w.n) throw std::invalid_argument("requantize: ld_out < n");
+    }
     if (lda < w.k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
     if (ldc < w.n) throw std::invalid_argument("abft_gemm: ldc < n");
     if (checked && (!d_err_count || (m > 0 && (!d_csum || !d_flags)))) throw std::invalid_argument("null argument");
@@ -275,9 +280,10 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
                    "cudaMemcpy2DAsync(A repack)");
         a = ws.scratch;
     }
-    const bool c_tma_ok = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0;
+    const bool c_tma_ok = d_c && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0;
     GemmTiling t = force ? *force : choose_tiling(m, w.n, w.k_pad, checked, c_tma_ok, has_fault);
     if (!c_tma_ok && t.epi != kEpiNone) t.epi = kEpiDirect;
+    if (!d_c) t.epi = kEpiNone;  // requantized output only
 
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
@@ -307,6 +313,13 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.row_acc = ws.row_acc;
     p.err_pack = reinterpret_cast<unsigned long long*>(ws.small + 8);
     p.trace = g_trace;
+    if (rq) {
+        p.rq_row_sum_a = rq->row_sum_a;
+        p.rq_col_sum_b = rq->col_sum_b;
+        p.rq_out = rq->out;
+        p.rq_ld = rq->ld_out;
+        p.rq = rq->params;
+    }
     if (has_fault) {
         p.fault_active = 1;
         p.fault_row = static_cast<int>(fault->row);
@@ -323,6 +336,32 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     const int pairs = static_cast<int>(std::min<int64_t>(p.num_tiles, std::max(1, device_sm_count() / 2)));
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
+}
+
+void check_requant_params(const RequantDev& q) {
+    if (!(q.sC > 0.0)) throw std::invalid_argument("requantize: scaleC must be positive");
+}
+
+void requantize(const int32_t* d_c, int64_t ldc, int64_t m, int64_t n, const int32_t* d_row_sum_a,
+                const int32_t* d_col_sum_b, const RequantDev& q, uint8_t* d_out, int64_t ld_out, cudaStream_t st) {
+    check_requant_params(q);
+    if (m < 0 || n < 0) throw std::invalid_argument("requantize: negative size");
+    if (m == 0 || n == 0) return;
+    if (!d_c || !d_row_sum_a || !d_col_sum_b || !d_out) throw std::invalid_argument("null argument");
+    if (ldc < n || ld_out < n) throw std::invalid_argument("requantize: leading dimension < n");
+    cuda_check(launch_requantize(d_c, ldc, m, n, d_row_sum_a, d_col_sum_b, q, d_out, ld_out, st), "requantize_kernel");
+}
+
+void row_sums_u8(const uint8_t* d_a, int64_t m, int64_t k, int64_t lda, int32_t* d_out, cudaStream_t st) {
+    if (m < 0 || k < 0 || lda < k) throw std::invalid_argument("row_sums: bad dimensions");
+    if (m == 0) return;
+    if (!d_a || !d_out) throw std::invalid_argument("null argument");
+    cuda_check(launch_row_sums_u8(d_a, m, k, lda, d_out, st), "row_sums_u8_kernel");
+}
+
+void weight_col_sums(const GemmWeight& w, int32_t* d_out, cudaStream_t st) {
+    if (!d_out) throw std::invalid_argument("null argument");
+    cuda_check(launch_col_sums(w, d_out, st), "col_sums_kernel");
 }
 
 void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum_ld, int64_t m, int64_t n,

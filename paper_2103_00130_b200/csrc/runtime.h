@@ -25,9 +25,22 @@ void set_checksums(GemmWeight& w, const int8_t* d_cs, cudaStream_t st);
 void free_weight(GemmWeight* w);
 GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault);
 // checked == false: plain GEMM (csum/flags/err_count ignored).
+// Fused requantization of the GEMM output (P:src/quant.cpp:77-102): u8 out = requantize(C').
+struct RequantArgs {
+    const int32_t* row_sum_a = nullptr;  // [m]
+    const int32_t* col_sum_b = nullptr;  // [n]
+    RequantDev params{};
+    uint8_t* out = nullptr;
+    int64_t ld_out = 0;
+};
+void check_requant_params(const RequantDev& q);
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
-          cudaStream_t st, const GemmTiling* force = nullptr);
+          cudaStream_t st, const GemmTiling* force = nullptr, const RequantArgs* rq = nullptr);
+void requantize(const int32_t* d_c, int64_t ldc, int64_t m, int64_t n, const int32_t* d_row_sum_a,
+                const int32_t* d_col_sum_b, const RequantDev& q, uint8_t* d_out, int64_t ld_out, cudaStream_t st);
+void row_sums_u8(const uint8_t* d_a, int64_t m, int64_t k, int64_t lda, int32_t* d_out, cudaStream_t st);
+void weight_col_sums(const GemmWeight& w, int32_t* d_out, cudaStream_t st);
 void verify(const int32_t* d_c, int64_t ldc, const int32_t* d_csum, int64_t csum_ld, int64_t m, int64_t n,
             uint8_t* d_flags, uint32_t* d_err_count, cudaStream_t st);
 
@@ -77,6 +90,10 @@ cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t 
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,
                           uint8_t* flags, uint32_t* err_count, uint32_t* ws_acc, uint32_t* ws_blocks, cudaStream_t st);
 cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st);
+cudaError_t launch_requantize(const int32_t* c, int64_t ldc, int64_t m, int64_t n, const int32_t* rs, const int32_t* cs,
+                              const RequantDev& q, uint8_t* out, int64_t ld_out, cudaStream_t st);
+cudaError_t launch_row_sums_u8(const uint8_t* a, int64_t m, int64_t k, int64_t lda, int32_t* out, cudaStream_t st);
+cudaError_t launch_col_sums(const GemmWeight& w, int32_t* out, cudaStream_t st);
 cudaError_t launch_eb_pack(const uint8_t* data, int64_t rows, int64_t row_bytes, int64_t row_stride, const void* meta,
                            int64_t meta_bytes, int64_t meta_off, int64_t rec_stride, uint8_t* packed, cudaStream_t st);
 cudaError_t launch_flip_cells(uint8_t* a, int64_t sa, uint8_t* b, int64_t sb, const int64_t* rows, const int64_t* cols,

@@ -241,3 +241,32 @@ def fnv1a64(arr: np.ndarray) -> str:
 def sha256(arr: np.ndarray) -> str:
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(arr).view(np.uint8).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- requantization (P:src/quant.cpp:77-118)
+def requantize(c, n, row_sum_a, col_sum_b, prm, k):
+    """C' (m x ldc int32, only the first n columns read) -> u8 m x n; raises ValueError on scaleC <= 0."""
+    c = np.ascontiguousarray(c, np.int32)
+    m, ldc = c.shape
+    rs = np.ascontiguousarray(row_sum_a, np.int32)
+    cs = np.ascontiguousarray(col_sum_b, np.int32)
+    p = np.ascontiguousarray(prm, np.float64)
+    out = np.empty((m, n), np.uint8)
+    rc = orc().orc_requantize(P(c), sz(ldc), sz(m), sz(n), P(rs), P(cs), P(p), C.c_uint64(int(k)), P(out), sz(n))
+    if rc != 0:
+        raise ValueError("requantize: scaleC must be positive")
+    return out
+
+
+def row_sums_u8(a):
+    a = np.ascontiguousarray(a, np.uint8)
+    out = np.empty(a.shape[0], np.int32)
+    orc().orc_row_sums_u8(P(a), sz(a.shape[0]), sz(a.shape[1]), sz(a.shape[1]), P(out))
+    return out
+
+
+def col_sums_i8(b):
+    b = np.ascontiguousarray(b, np.int8)
+    out = np.empty(b.shape[1], np.int32)
+    orc().orc_col_sums_i8(P(b), sz(b.shape[0]), sz(b.shape[1]), sz(b.shape[1]), P(out))
+    return out

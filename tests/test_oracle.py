@@ -287,3 +287,48 @@ def test_oracle_matches_reference_random(ref):
         assert np.array_equal(rs.view(np.uint64), rs_ref.view(np.uint64))
         assert np.array_equal(cs.view(np.uint64), cs_ref.view(np.uint64))
         assert np.array_equal(er, e_ref)
+
+
+# ---------------------------------------------------------------- requantization
+def _requant_case(seed):
+    from golden_cases import requant_inputs
+    return requant_inputs(seed)
+
+
+def test_requant_known_answers():  # P:tests/test_quant.cpp:125-144, 186-202
+    z = O.requantize(np.zeros((2, 2), np.int32), 2, [0, 0], [0, 0], [1, 0, 1, 0, 1, 0], 2)
+    assert not z.any()
+    assert O.requantize(np.zeros((1, 1), np.int32), 1, [0], [0], [1, 0, 1, 0, 1, -300.2], 1)[0, 0] == 255
+    with pytest.raises(ValueError):
+        O.requantize(np.zeros((2, 2), np.int32), 2, [0, 0], [0, 0], [1, 0, 1, 0, 0.0, 0], 1)
+    rng = np.random.default_rng(606)
+    no_cs = rng.integers(-100000, 100000, (3, 4)).astype(np.int32)
+    with_cs = np.concatenate([no_cs, rng.integers(-2 ** 31, 2 ** 31, (3, 1), dtype=np.int64).astype(np.int32)], 1)
+    prm = [0.01, 0.2, 0.02, -0.1, 0.5, -3.0]
+    a = O.requantize(no_cs, 4, [10, 20, 30], [1, 2, 3, 4], prm, 7)
+    b = O.requantize(with_cs, 4, [10, 20, 30], [1, 2, 3, 4], prm, 7)
+    assert np.array_equal(a, b)
+
+
+def test_requant_golden():
+    g = json.loads((GOLD / "requant.json").read_text())
+    for case in g["cases"]:
+        m, n, k, c, rs, cs, prm = _requant_case(case["seed"])
+        assert (m, n, k) == (case["m"], case["n"], case["k"])
+        out = O.requantize(c, n, rs, cs, prm, k)
+        assert out.reshape(-1).tolist() == case["out"], case["seed"]
+
+
+def test_row_col_sums_match_reference_semantics():
+    rng = np.random.default_rng(7)
+    a = rng.integers(0, 256, (9, 300)).astype(np.uint8)
+    b = rng.integers(-128, 128, (300, 11)).astype(np.int8)
+    assert np.array_equal(O.row_sums_u8(a), a.astype(np.int64).sum(1))
+    assert np.array_equal(O.col_sums_i8(b), b.astype(np.int64).sum(0))
+    R = O.ref()
+    if R is not None:
+        rr = np.empty(9, np.int32)
+        R.ref_row_sums_u8(O.P(a), O.sz(9), O.sz(300), O.P(rr))
+        cc = np.empty(11, np.int32)
+        R.ref_col_sums_i8(O.P(b), O.sz(300), O.sz(11), O.P(cc))
+        assert np.array_equal(rr, O.row_sums_u8(a)) and np.array_equal(cc, O.col_sums_i8(b))
