@@ -132,8 +132,23 @@ struct PairCfg {
 #endif
     static constexpr int KS = BN == 64 ? ABFT_KS64 : BN == 128 ? ABFT_KS128 : ABFT_KS256;
     static constexpr int kStagingBufs = ABFT_STAGING_BUFS;  // per epilogue warp
-    static constexpr int kProducers = 3;                   // TMA issuing warps: A lo, A hi, B'
-    static_assert(KS % 2 == 0, "the A stage is split in two K halves");
+#ifndef ABFT_NA64
+#define ABFT_NA64 2
+#endif
+#ifndef ABFT_NB64
+#define ABFT_NB64 1
+#endif
+#ifndef ABFT_NA
+#define ABFT_NA 2
+#endif
+#ifndef ABFT_NB
+#define ABFT_NB 1
+#endif
+    static constexpr int NA = BN == 64 ? ABFT_NA64 : ABFT_NA;  // TMA warps loading A (K split)
+    static constexpr int NB = BN == 64 ? ABFT_NB64 : ABFT_NB;  // TMA warps loading B' (K split)
+    static constexpr int kProducers = NA + NB;
+    static constexpr int kThreads = 32 * (5 + kProducers);   // producer 0, MMA, 4 epilogue, producers 1..
+    static_assert(KS % NA == 0 && KS % NB == 0, "producer warps split the stage's k-blocks evenly");
     static constexpr int kABytes = kBM * kBK;                // per CTA per k-block (its 128 rows of A)
     static constexpr int kBBytes = (BN / 2) * kBK;           // per CTA per k-block (its half of the B' tile)
     static constexpr int kStageBytes = KS * (kABytes + kBBytes);
@@ -148,7 +163,7 @@ struct PairCfg {
 };
 
 template <int BN, bool CHECKED, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
     using Cfg = PairCfg<BN>;
@@ -200,10 +215,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int rot = nt % kb_steps;
         for (int ks0 = 0; ks0 < pre; ++ks0) {
             const int ks = (ks0 + rot) % kb_steps;
-            if (role < 2)
-                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * (KS / 2));
+            if (role < Cfg::NA)
+                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * (KS / Cfg::NA));
             else
-                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS);
+                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2),
+                                   ks * KS + (role - Cfg::NA) * (KS / Cfg::NB));
         }
     }
     uint32_t tmem = 0;
@@ -227,10 +243,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         // scripts/pipe_bench9.cu), so the stage is split over three warps issuing in parallel:
         // A k-blocks [0, KS/2), A k-blocks [KS/2, KS), and the B' slab.
         if (lane == 0) {
-            const int role = warp == 0 ? 0 : warp - 5;  // 0, 1: A halves; 2: B'
+            const int role = warp == 0 ? 0 : warp - 5;  // [0, NA): A k-block groups; [NA, NA+NB): B' groups
             const uint64_t pol = policy_evict_last();   // A is re-read by every N tile, B' by every call
-            constexpr int KH = KS / 2;
-            constexpr uint32_t bytes[3] = {KH * Cfg::kABytes, (KS - KH) * Cfg::kABytes, KS * Cfg::kBBytes};
+            constexpr int KA = KS / Cfg::NA, KB = KS / Cfg::NB;
+            const bool is_a = role < Cfg::NA;
+            const int grp = is_a ? role : role - Cfg::NA;
+            const uint32_t bytes = is_a ? KA * Cfg::kABytes : KB * Cfg::kBBytes;
             int it = 0;
             for (int t = pair; t < p.num_tiles; t += npairs) {
                 const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
@@ -244,13 +262,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
-                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes[role]);
-                    if (role < 2)
-                        tma_load_3d_pair(st + role * KH * Cfg::kABytes, &tmA, &full[s], 0,
-                                         mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * KH, pol);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+                    if (is_a)
+                        tma_load_3d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
+                                         mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + grp * KA, pol);
                     else
-                        tma_load_3d_pair(st + KS * Cfg::kABytes, &tmB, &full[s], 0,
-                                         nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS, pol);
+                        tma_load_3d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, &tmB, &full[s], 0,
+                                         nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS + grp * KB, pol);
                 }
             }
         }
@@ -337,8 +355,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     uint32_t pk[8];
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) pk[q4] = 0u;
-#pragma unroll 4
-                    for (int j = 0; j < 32; ++j)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)  // fully unrolled: v[] and pk[] must stay in registers
                         if (col0 + j < p.n)
                             pk[j >> 2] |= requant_one(static_cast<int32_t>(v[j]), rsa, __ldg(p.rq_col_sum_b + col0 + j), rk)
                                           << (8 * (j & 3));
@@ -347,8 +365,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                         reinterpret_cast<uint4*>(dst)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         reinterpret_cast<uint4*>(dst)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                     } else {
-                        for (int j = 0; j < 32 && col0 + j < p.n; ++j)
-                            dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col0 + j < p.n) dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
                     }
                 }
                 if constexpr (CHECKED) {
@@ -532,7 +551,7 @@ static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap
     static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(Cfg::kThreads);
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -567,6 +586,14 @@ cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const C
 }
 
 int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }
+int gemm_box_a(int bn) {  // k-blocks per A request
+    return bn == 256 ? PairCfg<256>::KS / PairCfg<256>::NA : bn == 128 ? PairCfg<128>::KS / PairCfg<128>::NA
+                                                                    : PairCfg<64>::KS / PairCfg<64>::NA;
+}
+int gemm_box_b(int bn) {  // k-blocks per B' request
+    return bn == 256 ? PairCfg<256>::KS / PairCfg<256>::NB : bn == 128 ? PairCfg<128>::KS / PairCfg<128>::NB
+                                                                    : PairCfg<64>::KS / PairCfg<64>::NB;
+}
 
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st) {
     int64_t blocks = (w.k * (w.n + 1) + 255) / 256;

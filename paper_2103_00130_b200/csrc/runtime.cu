@@ -117,6 +117,8 @@ static unsigned long long* g_eb_trace = nullptr;  // debug: per-warp EmbeddingBa
 void set_eb_trace(unsigned long long* d_trace) { g_eb_trace = d_trace; }
 
 int gemm_ks(int bn);
+int gemm_box_a(int bn);
+int gemm_box_b(int bn);
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
 
 // 3D view {128 bytes of a k-block, rows, k-blocks} of a K-contiguous byte matrix. `row_bytes` is
@@ -164,7 +166,7 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
     cuda_check(launch_encode_weight(d_b, k, n, ldb, w, st), "encode_weight_kernel");
     for (int bn : {64, 128, 256})
         w.map_b[bn_index(bn)] = make_map_kblocks(w.bt, static_cast<uint64_t>(n_pad), static_cast<uint64_t>(k_pad / kBK),
-                                                 kBK, static_cast<uint64_t>(n_pad * kBK), bn / 2, gemm_ks(bn));
+                                                 kBK, static_cast<uint64_t>(n_pad * kBK), bn / 2, gemm_box_b(bn));
 }
 
 GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
@@ -328,7 +330,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     }
     // box = half a stage's k-blocks: two producer warps load the two halves in parallel
     const CUtensorMap map_a = make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
-                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_ks(t.bn) / 2);
+                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_box_a(t.bn));
     CUtensorMap map_c;
     std::memset(&map_c, 0, sizeof(map_c));
     if (t.epi == kEpiTmaStore)
