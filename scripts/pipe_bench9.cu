@@ -28,7 +28,7 @@ __device__ __forceinline__ void tma3d_mc(void* dst, const CUtensorMap* m, uint64
 }
 
 __global__ void __launch_bounds__(512, 1) stream(const __grid_constant__ CUtensorMap tm, int rows, int kbs, int stages,
-                                                 int iters, int lanes, int nreq, int spin, unsigned long long* out) {
+                                                 int iters, int lanes, int nreq, int spin, int same, unsigned long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem0 = (uint8_t*)(((uintptr_t)raw + 1023) & ~uintptr_t(1023));
     const int sb = rows * 128 * kbs;
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(512, 1) stream(const __grid_constant__ CUtenso
     }
     __syncthreads();
     unsigned long long t0 = globaltimer();
-    const int region = (blockIdx.x * lanes + lane_id) % 32;
+    const int region = same ? lane_id % 4 : (blockIdx.x * lanes + lane_id) % 32;
     if (threadIdx.x % 64 == 0) {
         for (int i = 0; i < iters; ++i) {
             const int s = i % stages;
@@ -89,7 +89,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&d, 4096 * 8);
     for (int ai = 1; ai + 4 < argc + 1 && ai < argc; ai += 5) {
         const int rows = atoi(argv[ai]), kbs = atoi(argv[ai + 1]), stages = atoi(argv[ai + 2]), lanes = atoi(argv[ai + 3]),
-                  nreq = atoi(argv[ai + 4]) % 10, spin = atoi(argv[ai + 4]) / 10;
+                  nreq = atoi(argv[ai + 4]) % 10, spin = (atoi(argv[ai + 4]) / 10) % 10, same = atoi(argv[ai + 4]) / 100;
         CUtensorMap m;
         memset(&m, 0, sizeof m);
         cuuint64_t dims[3] = {128, rows_total, kbt}, str[2] = {128, rows_total * 128};
@@ -101,7 +101,7 @@ int main(int argc, char** argv) {
         const int ctas = 148;
         cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         const int iters = 1024 * 1024 * 16 / sb;
-        for (int rep = 0; rep < 2; ++rep) stream<<<ctas, 64 * lanes, smem>>>(m, rows, kbs, stages, iters, lanes, nreq, spin, d);
+        for (int rep = 0; rep < 2; ++rep) stream<<<ctas, 64 * lanes, smem>>>(m, rows, kbs, stages, iters, lanes, nreq, spin, same, d);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h[256];
         cudaMemcpy(h, d, ctas * 8, cudaMemcpyDeviceToHost);
@@ -109,7 +109,7 @@ int main(int argc, char** argv) {
         for (int i = 0; i < ctas; ++i) avg += h[i];
         avg /= ctas;
         const double per_sm = (double)sb * iters * lanes / avg;
-        printf("spin %d lanes %d req %6d B x %d per stage, stages %d: %5.0f ns/stage/lane, %6.1f GB/s/SM, %5.2f TB/s  %s\n", spin, lanes,
+        printf("same %d spin %d lanes %d req %6d B x %d per stage, stages %d: %5.0f ns/stage/lane, %6.1f GB/s/SM, %5.2f TB/s  %s\n", same, spin, lanes,
                sb / nreq, nreq, stages, avg / iters, per_sm, per_sm * ctas / 1e3, cudaGetErrorString(e));
     }
 }
