@@ -65,6 +65,13 @@ struct GemmParams {
     int n_tiles;       // N tiles of BN columns
     int m_tiles;       // 256-row pair tiles
     int num_tiles;     // m_tiles * n_tiles
+    // split-K over two units per tile (small-m shapes, one wave): unit u < num_tiles computes k-blocks
+    // [kb_half, k_blocks) of tile u and publishes its partial tile; unit num_tiles + t computes
+    // [0, kb_half) of tile t, adds the partial and runs the epilogue. split == 1: one unit per tile.
+    int split;
+    int kb_half;
+    int32_t* partial;     // [num_tiles][2 CTAs][BN/32][32][128] int32 (split only)
+    uint32_t* part_flag;  // [num_tiles * 2], self-resetting
     int32_t* c;
     int64_t ldc;
     const uint8_t* a;  // A (u8, row-major, lda % 16 == 0) for the checksum GEMV
@@ -94,6 +101,7 @@ enum EpiMode { kEpiTmaStore = 0, kEpiStg = 1, kEpiDirect = 2, kEpiNone = 4 };
 
 struct GemmTiling {
     int bn, epi;
+    int split = 1;  // 2: split-K over two co-resident units per tile (GemmParams::split)
 };
 
 // ------------------------------------------------------------------ EmbeddingBag

@@ -176,12 +176,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* xbar = tempty + 2;  // split-K: the partner's partial tile landed in shared memory
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int pair = static_cast<int>(cluster_id_x()), npairs = static_cast<int>(nclusters_x());
-    const int kb_steps = (p.k_blocks + KS - 1) / KS;
+    const int num_units = p.num_tiles * p.split;
+    // unit -> (tile, k range); see GemmParams::split
+    struct Unit {
+        int tile, mt, nt, kh, kb0, steps;
+    };
+    auto unit_of = [&](int u) {
+        Unit x;
+        x.kh = (p.split == 2 && u < p.num_tiles) ? 1 : 0;
+        x.tile = p.split == 2 && !x.kh ? u - p.num_tiles : u;
+        x.mt = x.tile / p.n_tiles;
+        x.nt = x.tile - x.mt * p.n_tiles;
+        x.kb0 = x.kh ? p.kb_half : 0;
+        const int cnt = p.split == 2 ? (x.kh ? p.k_blocks - p.kb_half : p.kb_half) : p.k_blocks;
+        x.steps = (cnt + KS - 1) / KS;
+        return x;
+    };
     unsigned long long* trace = p.trace ? p.trace + 16ull * blockIdx.x : nullptr;
     if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
@@ -194,6 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
         }
+        mbar_init(xbar, 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -208,18 +225,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     if (trace && threadIdx.x == 0) trace[1] = globaltimer();
     // warm L2 with this pair's first stages while the previous grid finishes (before griddep_wait:
     // prefetches only touch L2, the point of coherence); one producer warp per operand part
-    if ((warp == 0 || warp >= 6) && lane == 0 && pair < p.num_tiles) {
+    if ((warp == 0 || warp >= 6) && lane == 0 && pair < num_units) {
         const int role = warp == 0 ? 0 : warp - 5;
-        const int mt = pair / p.n_tiles, nt = pair - mt * p.n_tiles;
-        const int pre = kb_steps < STAGES ? kb_steps : STAGES;
-        const int rot = nt % kb_steps;
+        const Unit x = unit_of(pair);
+        const int pre = x.steps < STAGES ? x.steps : STAGES;
+        const int rot = x.nt % x.steps;
         for (int ks0 = 0; ks0 < pre; ++ks0) {
-            const int ks = (ks0 + rot) % kb_steps;
+            const int kb = x.kb0 + ((ks0 + rot) % x.steps) * KS;
             if (role < Cfg::NA)
-                tma_prefetch_l2_3d(&tmA, 0, mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + role * (KS / Cfg::NA));
+                tma_prefetch_l2_3d(&tmA, 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA));
             else
-                tma_prefetch_l2_3d(&tmB, 0, nt * BN + static_cast<int>(rank) * (BN / 2),
-                                   ks * KS + (role - Cfg::NA) * (KS / Cfg::NB));
+                tma_prefetch_l2_3d(&tmB, 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
+                                   kb + (role - Cfg::NA) * (KS / Cfg::NB));
         }
     }
     uint32_t tmem = 0;
@@ -250,14 +267,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             const int grp = is_a ? role : role - Cfg::NA;
             const uint32_t bytes = is_a ? KA * Cfg::kABytes : KB * Cfg::kBBytes;
             int it = 0;
-            for (int t = pair; t < p.num_tiles; t += npairs) {
-                const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+            for (int u = pair; u < num_units; u += npairs) {
+                const Unit x = unit_of(u);
                 // Tiles of one M block read the same A rows; starting each tile at a different K step
                 // spreads those reads over all of A's L2 lines instead of hammering one k-block's lines
                 // (integer accumulation is exact, so the K order does not change the result).
-                const int rot = nt % kb_steps;
-                for (int ks0 = 0; ks0 < kb_steps; ++ks0, ++it) {
-                    const int ks = ks0 + rot < kb_steps ? ks0 + rot : ks0 + rot - kb_steps;
+                const int rot = x.nt % x.steps;
+                for (int ks0 = 0; ks0 < x.steps; ++ks0, ++it) {
+                    const int ks = ks0 + rot < x.steps ? ks0 + rot : ks0 + rot - x.steps;
+                    const int kb = x.kb0 + ks * KS;
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
@@ -265,10 +283,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
                     if (is_a)
                         tma_load_3d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
-                                         mt * kPairM + static_cast<int>(rank) * kBM, ks * KS + grp * KA, pol);
+                                         x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, pol);
                     else
                         tma_load_3d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, &tmB, &full[s], 0,
-                                         nt * BN + static_cast<int>(rank) * (BN / 2), ks * KS + grp * KB, pol);
+                                         x.nt * BN + static_cast<int>(rank) * (BN / 2), kb + grp * KB, pol);
                 }
             }
         }
@@ -277,19 +295,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         if (rank == 0 && lane == 0) {
             constexpr uint32_t idesc = idesc_u8s8(kPairM, BN);
             int it = 0, local = 0;
-            for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
+            for (int u = pair; u < num_units; u += npairs, ++local) {
+                const int steps = unit_of(u).steps;
                 const int acc = local & 1;
                 const uint32_t aph = (local >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
-                for (int ks = 0; ks < kb_steps; ++ks, ++it) {
+                for (int ks = 0; ks < steps; ++ks, ++it) {
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     if (trace && local == 0 && ks == 0) trace[2] = globaltimer();
-                    if (trace && local == 0 && ks >= 1 && ks <= 7) trace[8 + ks] = globaltimer();  // stage arrivals
+                    if (trace && local == 0 && ks >= 1 && ks <= 3) trace[8 + ks] = globaltimer();  // stage arrivals
                     const uint32_t a0 = smem_u32(smem + s * Cfg::kStageBytes);
                     const uint32_t b0 = a0 + KS * Cfg::kABytes;
 #pragma unroll
@@ -314,8 +333,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         const int q = warp & 3;                  // TMEM lane quarter this warp may access
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         int local = 0, chunk_ctr = 0;
-        for (int t = pair; t < p.num_tiles; t += npairs, ++local) {
-            const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        for (int u = pair; u < num_units; u += npairs, ++local) {
+            const Unit x = unit_of(u);
+            const int mt = x.mt, nt = x.nt;
             const int acc = local & 1;
             const uint32_t aph = (local >> 1) & 1;
             const int row0 = mt * kPairM + static_cast<int>(rank) * kBM + q * 32;  // first row of this warp
@@ -323,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             // This tile's share of the checksum column C'[row][n] = sum_p A[row][p]*cs[p]: K blocks
             // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
             uint32_t cs_part = 0;
-            if constexpr (CHECKED) {
+            if (CHECKED && x.kh == 0) {
                 const int kb0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
                 const int kb1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
                 if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, row, kb0 * kBK, min(kb1 * kBK, p.k));
@@ -333,6 +353,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
             const int n0 = nt * BN;
             const uint32_t t_row = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+            // split-K exchange slot of this CTA's half tile (BN*128 int32): [BN/32 chunks][8 column quads]
+            // [128 rows][4], so a warp moves 512 contiguous bytes per 16-byte access, in global memory (the
+            // upper-K unit's stores) and in shared memory (the lower-K unit's conflict-free reads)
+            const int64_t part_base = (static_cast<int64_t>(x.tile) * 2 + rank) * (BN * kBM);
+            uint32_t* pflag = p.split == 2 ? p.part_flag + x.tile * 2 + rank : nullptr;
+            const int prow = q * 32 + lane;
+            if (x.kh == 1) {
+                // upper-K unit: publish the partial tile through L2 and hand the tile to its partner
+                uint4* part = reinterpret_cast<uint4*>(p.partial + part_base);
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(t_row + c * 32, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4)
+                        part[(c * 8 + j4) * kBM + prow] = make_uint4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (rank == 0)
+                        mbar_arrive_local(&tempty[acc]);
+                    else
+                        mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc * 8));
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (threadIdx.x == 64) {
+                    st_release_gpu(pflag, 1u);
+                    if (trace) trace[14] = globaltimer();
+                }
+                continue;
+            }
+            const uint4* spart = nullptr;
+            if (p.split == 2) {
+                // lower-K unit: wait for the partner's partial (it was scheduled first and never waits),
+                // then pull it into the now idle pipeline buffers with bulk copies (one L2 round trip)
+                if (threadIdx.x == 64) {
+                    while (ld_acquire_gpu(pflag) == 0u) {
+                    }
+                    if (trace) trace[12] = globaltimer();
+                    fence_proxy_async_global();
+                    constexpr uint32_t kBytes = BN * kBM * 4;
+                    mbar_arrive_expect_tx(xbar, kBytes);
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.partial + part_base);
+#pragma unroll
+                    for (uint32_t o = 0; o < kBytes; o += 16384) bulk_load_1d(smem + o, src + o, 16384, xbar);
+                }
+                mbar_wait(xbar, 0);  // one split unit per CTA (units <= pairs), so phase 0
+                if (trace && threadIdx.x == 64) trace[13] = globaltimer();
+                spart = reinterpret_cast<const uint4*>(smem);
+            }
             const bool fault_here = p.fault_active && row == p.fault_row && p.fault_col < p.n;
             long long rsum = 0;
 #pragma unroll 1
@@ -342,6 +415,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(t_row + c * 32, v);
                 tmem_wait_ld();
+                if (spart != nullptr) {
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const uint4 w = spart[(c * 8 + j4) * kBM + prow];
+                        v[4 * j4] += w.x;
+                        v[4 * j4 + 1] += w.y;
+                        v[4 * j4 + 2] += w.z;
+                        v[4 * j4 + 3] += w.w;
+                    }
+                }
                 if (fault_here) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
@@ -435,6 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 }
             }
             if (trace && local == 0 && threadIdx.x == 64) trace[7] = globaltimer();
+            if (pflag != nullptr && threadIdx.x == 64) *pflag = 0u;  // self-resetting for the next call
             // accumulator drained: let the MMA warp reuse it
             tc_fence_before();
             __syncwarp();

@@ -73,6 +73,10 @@ struct Workspace {
     int device = 0;
     unsigned long long* row_acc = nullptr;  // GEMM: per-row (A*cs share sum) << 32 | residue sum
     int64_t rows_cap = 0;
+    int32_t* partial = nullptr;  // GEMM split-K partial tiles
+    int64_t partial_cap = 0;
+    uint32_t* part_flag = nullptr;  // GEMM split-K hand-over flags (self-resetting)
+    int64_t part_flag_cap = 0;
     uint32_t* small = nullptr;  // [2] verify acc [3] verify blocks [4] eb flag acc [5] eb blocks [6..7] eb bag counter (u64) [8..9] GEMM err_pack (u64) [12] eb validate count
     uint8_t* scratch = nullptr;  // A repack buffer
     size_t scratch_cap = 0;
@@ -198,39 +202,54 @@ void free_weight(GemmWeight* w) {
     delete w;
 }
 
-// Pick the N tile of the CTA pair. Cost model (cycles, per pair): waves x max(MMA issue, per-SM
-// operand ingest) with MMA issue floors measured on B200 for cta_group::2 kind::i8 (N=64: 46 cycles,
-// N=128: 64, N=256: 128 per K=32 step) and ~128 B/clk of TMA ingest per SM; plus the epilogue drain
-// of the last tile (TMA store ~31 B/clk/SM).
+// Pick the pair tile (BN) and split-K. Cost model in SM cycles, from B200 measurements:
+// the mainloop is bound by shared-memory bandwidth (128 B/clk/SM): every byte of a k-block's A rows
+// (128 per CTA) and B' rows (BN/2) is written by TMA and read by the MMA, i.e. 2*(128 + BN/2) cycles per
+// k-block, vs the MMA issue floor 4 x {46, 64, 128} cycles (N = 64, 128, 256). Split-K (single wave only)
+// halves the k-blocks per unit but the partial-tile hand-over through L2 (publish, flag, poll, bulk
+// pull) measured ~4 us on G2 (trace_gemm.py), more than the 2 us it saves: charged as 8000 cycles, so
+// it is only picked where the mainloop saving is larger. The last tile's drain is ~BN*128*4 B at ~31 B/clk.
+static int64_t gemm_kb_split(int64_t kb, int ks) { return (kb + 1) / 2 + ks - 1 - ((kb + 1) / 2 + ks - 1) % ks; }
+
 GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault) {
     (void)fault;
+    (void)checked;  // checked and unchecked run the same MMA tiles (the checksum column is a GEMV)
     const int pairs = std::max(1, device_sm_count() / 2);
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t kb = k_pad / kBK;
-    (void)checked;  // checked and unchecked run the same MMA tiles (the checksum column is a GEMV)
-    const int64_t ncols = n;
     const int epi = c_tma_ok ? kEpiTmaStore : kEpiDirect;
-    if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn[,epi]" tuning override
-        int bn = 0, e = -1;
-        const int got = std::sscanf(env, "%d,%d", &bn, &e);
+    auto split_ok = [&](int bn, int64_t tiles) {
+        const int ks = gemm_ks(bn);
+        return tiles * 2 <= pairs && kb >= 4 * ks && gemm_kb_split(kb, ks) < kb;
+    };
+    if (const char* env = std::getenv("ABFTLP_GEMM_TILING")) {  // "bn[,epi[,split]]" tuning override
+        int bn = 0, e = -1, sp = 1;
+        const int got = std::sscanf(env, "%d,%d,%d", &bn, &e, &sp);
         if (got >= 1 && (bn == 64 || bn == 128 || bn == 256)) {
-            if (got == 2 && e == kEpiNone) return {bn, kEpiNone};
-            if (got == 2 && (e == kEpiTmaStore || e == kEpiStg) && c_tma_ok) return {bn, e};
-            return {bn, epi};
+            GemmTiling t{bn, epi, 1};
+            if (got >= 2 && e == kEpiNone) t.epi = kEpiNone;
+            if (got >= 2 && (e == kEpiTmaStore || e == kEpiStg) && c_tma_ok) t.epi = e;
+            const int64_t tiles = m_tiles * ((n + bn - 1) / bn);
+            if (got == 3 && sp == 2 && split_ok(bn, tiles)) t.split = 2;
+            return t;
         }
     }
-    GemmTiling best{64, epi};
+    GemmTiling best{64, epi, 1};
     double best_cost = 1e300;
     for (int bn : {256, 128, 64}) {
-        const int64_t tiles = m_tiles * ((ncols + bn - 1) / bn);
-        const int64_t waves = (tiles + pairs - 1) / pairs;
-        const double mma = double(kb) * 4 * (bn == 64 ? 46 : bn == 128 ? 64 : 128);
-        const double ingest = double(kb) * (kBM * kBK + (bn / 2) * kBK) / 128.0;
-        const double epi_drain = double(kBM) * bn * 4 / 31.0;
-        const double cost = waves * std::max(mma, ingest) + epi_drain;
-        if (cost < best_cost * 0.97) {
-            best_cost = cost;
-            best.bn = bn;
+        const int64_t tiles = m_tiles * ((n + bn - 1) / bn);
+        const double per_kb = std::max(2.0 * (kBM + bn / 2), 4.0 * (bn == 64 ? 46 : bn == 128 ? 64 : 128));
+        const double drain = double(kBM) * bn * 4 / 31.0;
+        for (int split : {1, 2}) {
+            if (split == 2 && !split_ok(bn, tiles)) continue;
+            const int64_t units = tiles * split;
+            const int64_t waves = (units + pairs - 1) / pairs;
+            const double kb_unit = split == 2 ? double(gemm_kb_split(kb, gemm_ks(bn))) : double(kb);
+            const double cost = waves * kb_unit * per_kb + (split == 2 ? 8000.0 + 8.0 * bn : 0.0) + drain;
+            if (cost < best_cost * 0.97) {
+                best_cost = cost;
+                best = {bn, epi, split};
+            }
         }
     }
     return best;
@@ -303,6 +322,14 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.n_tiles = static_cast<int>(n_tiles);
     p.m_tiles = static_cast<int>(m_tiles);
     p.num_tiles = static_cast<int>(m_tiles * n_tiles);
+    p.split = t.split;
+    if (t.split == 2) {
+        p.kb_half = static_cast<int>(gemm_kb_split(kb, gemm_ks(t.bn)));
+        grow(ws.partial, ws.partial_cap, m_tiles * n_tiles * 2 * t.bn * kBM, st);
+        grow(ws.part_flag, ws.part_flag_cap, m_tiles * n_tiles * 2, st);
+        p.partial = ws.partial;
+        p.part_flag = ws.part_flag;
+    }
     p.c = d_c;
     p.ldc = ldc;
     p.csum = d_csum;
@@ -335,7 +362,8 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     std::memset(&map_c, 0, sizeof(map_c));
     if (t.epi == kEpiTmaStore)
         map_c = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_INT32, d_c, w.n, m, ldc * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    const int pairs = static_cast<int>(std::min<int64_t>(p.num_tiles, std::max(1, device_sm_count() / 2)));
+    const int pairs = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.num_tiles) * p.split,
+                                                         std::max(1, device_sm_count() / 2)));
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
 }

@@ -93,7 +93,8 @@ def test_shapes_bit_exact(G, m, n, k):
     assert check_against_oracle(G, a, b).errCount == 0
 
 
-@pytest.mark.parametrize("tiling", ["256", "128", "64", "256,2", "128,2", "64,2", "256,1", "128,1", "64,1"])
+@pytest.mark.parametrize("tiling", ["256", "128", "64", "256,2", "128,2", "64,2", "256,1", "128,1", "64,1",
+                                    "128,0,2", "256,0,2", "256,1,2", "128,2,2"])
 def test_g2_tilings_bit_exact(G, tiling, monkeypatch):
     """Every N-tile / split-K / epilogue variant gives the identical C' and verdicts."""
     monkeypatch.setenv("ABFTLP_GEMM_TILING", tiling)
@@ -105,6 +106,24 @@ def test_g2_tilings_bit_exact(G, tiling, monkeypatch):
     assert O.sha256(ct) == gold["ctemp_sha"]
     assert int(ct.astype(np.int64).sum()) == gold["ctemp_sum"]
     assert res.errCount == 0
+
+
+@pytest.mark.parametrize("m,n,k,tiling", [(64, 512, 512, "128,0,2"), (130, 300, 1200, "128,0,2"),
+                                          (256, 1000, 777, "64,0,2"), (33, 2049, 4096, "256,0,2"),
+                                          (256, 4096, 4096, "128,0,2")])
+def test_split_k_bit_exact_with_faults(G, m, n, k, tiling, monkeypatch):
+    """Split-K units (partial tile handed over through L2) give the identical C', checksum column and
+    verdicts, including the in-epilogue fault hook on both sides of the checksum column."""
+    monkeypatch.setenv("ABFTLP_GEMM_TILING", tiling)
+    a, b = rnd(m + 11 * n + k, m, n, k)
+    pb = G.PackedEncodedWeight(b)
+    for _ in range(2):  # the hand-over flags are self-resetting: a second call must see fresh partials
+        res = G.abft_gemm(a, pb)
+        ct, fl, err = O.abft_gemm(a, b)
+        assert np.array_equal(res.cTemp.data.cpu().numpy(), ct) and res.errCount == err == 0
+    for col in (n // 2, n):
+        bad = G.abft_gemm(a, pb, fault=(m - 1, col, 30))
+        assert bad.errCount == 1 and int(bad.rowFlags[m - 1].item()) == 1
 
 
 def test_device_api_aligned_layout_matches_ctemp(G):
