@@ -86,6 +86,35 @@ abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t ld
                                        int32_t* csum, uint8_t* row_flags, uint32_t* err_count,
                                        abftlp_stream stream);
 
+/* ------------------------------------------------------------------ batched GEMM (many small problems) */
+/* Encode `batch` independent weights of one shape: weight b is B_b = d_b + b*stride_b (k x n, ld ldb).
+ * The batched handle serves abftlp_gemm_*_batched; per-weight accessors (checksums, read, flip, col sums)
+ * need a single weight and return ABFTLP_ERR_INVALID_ARGUMENT on it. */
+abftlp_status abftlp_gemm_encode_batched(const int8_t* d_b, uint64_t batch, uint64_t k, uint64_t n,
+                                         uint64_t ldb, uint64_t stride_b, abftlp_stream stream,
+                                         abftlp_gemm_weight** out);
+typedef struct {
+    int32_t active;
+    uint64_t batch; /* problem index */
+    uint64_t row;
+    uint64_t col;   /* col == n: the checksum column */
+    uint32_t bit;
+} abftlp_batch_fault;
+/* `batch` checked GEMMs of one shape in ONE launch (e.g. the reference's 100 seeded trials of config 0):
+ * problem b multiplies A_b = d_a + b*stride_a (bytes; 16-byte multiple) by weight b of a batched weight
+ * (or the single weight of a plain handle) and writes C_b = d_c + b*stride_c, csum at d_csum +
+ * b*stride_csum (int32 elements), flags at d_row_flags + b*stride_flags and d_err_count[b]. Each problem's
+ * result is bit-identical to abftlp_gemm_checked on it. */
+abftlp_status abftlp_gemm_checked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                          uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c,
+                                          uint64_t ldc, uint64_t stride_c, int32_t* d_csum, uint64_t csum_ld,
+                                          uint64_t stride_csum, uint8_t* d_row_flags, uint64_t stride_flags,
+                                          uint32_t* d_err_count, const abftlp_batch_fault* fault,
+                                          abftlp_stream stream);
+abftlp_status abftlp_gemm_unchecked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                            uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c,
+                                            uint64_t ldc, uint64_t stride_c, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ requantization */
 /* RequantParams (P:src/quant.hpp:24-32): out = clamp(round_half_away((cf - biasC) / scaleC), 0, 255) with
  * cf = scaleA*scaleB*C + scaleA*biasB*rowSumA[i] + scaleB*biasA*colSumB[j] + k*biasA*biasB, all in

@@ -68,6 +68,12 @@ class RequantParams(C.Structure):
                 ("scaleC", C.c_double), ("biasC", C.c_double), ("k", C.c_uint64)]
 
 
+class BatchFault(C.Structure):
+    """abftlp_batch_fault."""
+    _fields_ = [("active", C.c_int32), ("batch", C.c_uint64), ("row", C.c_uint64), ("col", C.c_uint64),
+                ("bit", C.c_uint32)]
+
+
 class Fault(C.Structure):
     _fields_ = [("active", i32), ("row", u64), ("col", u64), ("bit", u32)]
 
@@ -109,6 +115,9 @@ _SIGS = {
     "abftlp_eb_table_row_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_checked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp, vp, vp, vp, vp]),
     "abftlp_eb_unchecked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp]),
+    "abftlp_gemm_encode_batched": (i32, [vp, u64, u64, u64, u64, u64, vp, vp]),
+    "abftlp_gemm_checked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, vp]),
+    "abftlp_gemm_unchecked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp]),
     "abftlp_gemm_checked_requant": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),
     "abftlp_requantize": (i32, [vp, u64, u64, u64, vp, vp, vp, vp, u64, vp]),
     "abftlp_row_sums_u8": (i32, [vp, u64, u64, u64, vp, vp]),

@@ -39,7 +39,9 @@ struct GemmWeight {
     int8_t* cs = nullptr;          // k_pad (WeightChecksum::values, each in [0,126]; zero pad)
     bool owns = true;
     size_t bt_cap = 0, cs_cap = 0;  // allocation capacities (campaign scratch re-encodes in place)
-    CUtensorMap map_b[3]{};         // 3D box {128, BN/2, KS} for BN = 64, 128, 256
+    int64_t batch = 1;              // independent weights stored back to back (batched GEMM)
+    int64_t bt_bstride = 0, cs_bstride = 0;  // bytes between consecutive weights' bt / cs
+    CUtensorMap map_b[3]{};         // 4D {128 B, rows, k-blocks, batch}, box {128, BN/2, KS/NB, 1}, BN = 64, 128, 256
     // device pointer of logical element (i, j) of [B | cs], j <= n
     int8_t* element(int64_t i, int64_t j) const {
         return j == n ? cs + i : bt + ((i / kBK) * n_pad * kBK + j * kBK + (i % kBK));
@@ -64,7 +66,17 @@ struct GemmParams {
     int k_blocks;      // 128-byte K blocks
     int n_tiles;       // N tiles of BN columns
     int m_tiles;       // 256-row pair tiles
-    int num_tiles;     // m_tiles * n_tiles
+    int num_tiles;     // batch * m_tiles * n_tiles
+    // batched GEMM (independent problems of one shape, one launch): tile t belongs to problem
+    // t / (m_tiles * n_tiles); per-problem strides below (batch == 1: all zero)
+    int batch;
+    int b_shared;          // 1: every problem uses weight 0
+    int64_t a_bstride;     // bytes
+    int64_t cs_bstride;    // bytes (checksum vector of problem b)
+    int64_t c_bstride;     // int32 elements
+    int64_t csum_bstride;  // int32 elements
+    int64_t flags_bstride; // bytes
+    int fault_batch;
     // split-K over two units per tile (small-m shapes, one wave): unit u < num_tiles computes k-blocks
     // [kb_half, k_blocks) of tile u and publishes its partial tile; unit num_tiles + t computes
     // [0, kb_half) of tile t, adds the partial and runs the epilogue. split == 1: one unit per tile.

@@ -262,6 +262,18 @@ abftlp_status abftlp_gemm_encode(const int8_t* d_b, uint64_t k, uint64_t n, uint
     });
 }
 
+abftlp_status abftlp_gemm_encode_batched(const int8_t* d_b, uint64_t batch, uint64_t k, uint64_t n, uint64_t ldb,
+                                         uint64_t stride_b, abftlp_stream stream, abftlp_gemm_weight** out) {
+    if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::GemmWeight* w = abftk::encode_weight(d_b, static_cast<int64_t>(k), static_cast<int64_t>(n),
+                                                    static_cast<int64_t>(ldb), as_stream(stream),
+                                                    static_cast<int64_t>(batch), static_cast<int64_t>(stride_b));
+        *out = new abftlp_gemm_weight_s{w};
+        return ABFTLP_OK;
+    });
+}
+
 void abftlp_gemm_weight_free(abftlp_gemm_weight* w) {
     if (!w) return;
     abftk::free_weight(w->w);
@@ -278,6 +290,7 @@ abftlp_status abftlp_gemm_weight_dims(const abftlp_gemm_weight* w, uint64_t* k, 
 abftlp_status abftlp_gemm_weight_checksums(const abftlp_gemm_weight* w, int8_t* d_cs, abftlp_stream stream) {
     if (!w || !d_cs) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
+        if (w->w->batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
         ABFT_CUDA(cudaMemcpyAsync(d_cs, w->w->cs, static_cast<size_t>(w->w->k), cudaMemcpyDeviceToDevice,
                                   as_stream(stream)));
         return ABFTLP_OK;
@@ -287,6 +300,7 @@ abftlp_status abftlp_gemm_weight_checksums(const abftlp_gemm_weight* w, int8_t* 
 abftlp_status abftlp_gemm_weight_set_checksums(abftlp_gemm_weight* w, const int8_t* d_cs, abftlp_stream stream) {
     if (!w || !d_cs) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
+        if (w->w->batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
         abftk::set_checksums(*w->w, d_cs, as_stream(stream));
         return ABFTLP_OK;
     });
@@ -295,6 +309,7 @@ abftlp_status abftlp_gemm_weight_set_checksums(abftlp_gemm_weight* w, const int8
 abftlp_status abftlp_gemm_weight_read(const abftlp_gemm_weight* w, int8_t* d_out, abftlp_stream stream) {
     if (!w || !d_out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
+        if (w->w->batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
         abftk::read_encoded(*w->w, d_out, as_stream(stream));
         return ABFTLP_OK;
     });
@@ -382,7 +397,51 @@ abftlp_status abftlp_row_sums_u8(const uint8_t* d_a, uint64_t m, uint64_t k, uin
 abftlp_status abftlp_gemm_weight_col_sums(const abftlp_gemm_weight* w, int32_t* d_out, abftlp_stream stream) {
     if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
+        if (w->w->batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
         abftk::weight_col_sums(*w->w, d_out, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_checked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                          uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
+                                          uint64_t stride_c, int32_t* d_csum, uint64_t csum_ld, uint64_t stride_csum,
+                                          uint8_t* d_row_flags, uint64_t stride_flags, uint32_t* d_err_count,
+                                          const abftlp_batch_fault* fault, abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::Fault f;
+        abftk::GemmBatch bt;
+        bt.batch = static_cast<int64_t>(batch);
+        bt.a_bstride = static_cast<int64_t>(stride_a);
+        bt.c_bstride = static_cast<int64_t>(stride_c);
+        bt.csum_bstride = static_cast<int64_t>(stride_csum);
+        bt.flags_bstride = static_cast<int64_t>(stride_flags);
+        if (fault && fault->active) {
+            f.active = true;
+            f.row = static_cast<int64_t>(fault->row);
+            f.col = static_cast<int64_t>(fault->col);
+            f.bit = fault->bit;
+            bt.fault_batch = static_cast<int64_t>(fault->batch);
+        }
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    true, d_csum, static_cast<int64_t>(csum_ld), d_row_flags, d_err_count, &f, as_stream(stream),
+                    nullptr, nullptr, &bt);
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_unchecked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                            uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
+                                            uint64_t stride_c, abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::GemmBatch bt;
+        bt.batch = static_cast<int64_t>(batch);
+        bt.a_bstride = static_cast<int64_t>(stride_a);
+        bt.c_bstride = static_cast<int64_t>(stride_c);
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    false, nullptr, 0, nullptr, nullptr, nullptr, as_stream(stream), nullptr, nullptr, &bt);
         return ABFTLP_OK;
     });
 }
@@ -539,6 +598,7 @@ abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uin
                                           abftlp_stream stream) {
     if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {
+        if (w->w->batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
         const abftk::GemmWeight& W = *w->w;
         if (i >= static_cast<uint64_t>(W.k) || j > static_cast<uint64_t>(W.n))
             throw std::out_of_range("inject_weight_B: coordinates out of range");

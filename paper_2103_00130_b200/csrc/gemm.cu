@@ -91,8 +91,9 @@ __global__ void read_encoded_kernel(const int8_t* __restrict__ bt, const int8_t*
 // ============================================================ checksum GEMV share
 // sum_{p in [k0, k1)} A[row][p] * cs[p], exact in 32 bits (A <= 255, cs <= 126, k < 65793 as the
 // reference's int32 accumulation). 16-byte loads (lda % 16 == 0), four u8 x u8 dot products per dp4a.
-__device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int row, int k0, int k1) {
-    const uint8_t* arow = p.a + static_cast<int64_t>(row) * p.lda;
+__device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int b, int row, int k0, int k1) {
+    const uint8_t* arow = p.a + b * p.a_bstride + static_cast<int64_t>(row) * p.lda;
+    const int8_t* cs = p.cs + b * p.cs_bstride;
     uint32_t s = 0;
     int kk = k0;
     for (; kk + 128 <= k1; kk += 128) {
@@ -101,14 +102,14 @@ __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int row, int
         for (int u = 0; u < 8; ++u) av[u] = __ldg(reinterpret_cast<const uint4*>(arow + kk + 16 * u));
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(p.cs + kk + 16 * u));
+            const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cs + kk + 16 * u));
             s = __dp4a(av[u].x, cv.x, s);
             s = __dp4a(av[u].y, cv.y, s);
             s = __dp4a(av[u].z, cv.z, s);
             s = __dp4a(av[u].w, cv.w, s);
         }
     }
-    for (; kk < k1; ++kk) s += static_cast<uint32_t>(arow[kk]) * static_cast<uint32_t>(static_cast<uint8_t>(p.cs[kk]));
+    for (; kk < k1; ++kk) s += static_cast<uint32_t>(arow[kk]) * static_cast<uint32_t>(static_cast<uint8_t>(cs[kk]));
     return s;
 }
 
@@ -185,14 +186,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     const int num_units = p.num_tiles * p.split;
     // unit -> (tile, k range); see GemmParams::split
     struct Unit {
-        int tile, mt, nt, kh, kb0, steps;
+        int tile, b, mt, nt, kh, kb0, steps;
     };
+    const int tiles_per_problem = p.m_tiles * p.n_tiles;
     auto unit_of = [&](int u) {
         Unit x;
         x.kh = (p.split == 2 && u < p.num_tiles) ? 1 : 0;
         x.tile = p.split == 2 && !x.kh ? u - p.num_tiles : u;
-        x.mt = x.tile / p.n_tiles;
-        x.nt = x.tile - x.mt * p.n_tiles;
+        x.b = x.tile / tiles_per_problem;
+        const int tl = x.tile - x.b * tiles_per_problem;
+        x.mt = tl / p.n_tiles;
+        x.nt = tl - x.mt * p.n_tiles;
         x.kb0 = x.kh ? p.kb_half : 0;
         const int cnt = p.split == 2 ? (x.kh ? p.k_blocks - p.kb_half : p.kb_half) : p.k_blocks;
         x.steps = (cnt + KS - 1) / KS;
@@ -233,10 +237,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         for (int ks0 = 0; ks0 < pre; ++ks0) {
             const int kb = x.kb0 + ((ks0 + rot) % x.steps) * KS;
             if (role < Cfg::NA)
-                tma_prefetch_l2_3d(&tmA, 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA));
+                tma_prefetch_l2_4d(&tmA, 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA), x.b);
             else
-                tma_prefetch_l2_3d(&tmB, 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
-                                   kb + (role - Cfg::NA) * (KS / Cfg::NB));
+                tma_prefetch_l2_4d(&tmB, 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
+                                   kb + (role - Cfg::NA) * (KS / Cfg::NB), p.b_shared ? 0 : x.b);
         }
     }
     uint32_t tmem = 0;
@@ -282,11 +286,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     uint8_t* st = smem + s * Cfg::kStageBytes;
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
                     if (is_a)
-                        tma_load_3d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
-                                         x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, pol);
+                        tma_load_4d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
+                                         x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, x.b, pol);
                     else
-                        tma_load_3d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, &tmB, &full[s], 0,
-                                         x.nt * BN + static_cast<int>(rank) * (BN / 2), kb + grp * KB, pol);
+                        tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, &tmB, &full[s], 0,
+                                         x.nt * BN + static_cast<int>(rank) * (BN / 2), kb + grp * KB,
+                                         p.b_shared ? 0 : x.b, pol);
                 }
             }
         }
@@ -346,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             if (CHECKED && x.kh == 0) {
                 const int kb0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
                 const int kb1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
-                if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, row, kb0 * kBK, min(kb1 * kBK, p.k));
+                if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, x.b, row, kb0 * kBK, min(kb1 * kBK, p.k));
             }
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
@@ -406,7 +411,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 if (trace && threadIdx.x == 64) trace[13] = globaltimer();
                 spart = reinterpret_cast<const uint4*>(smem);
             }
-            const bool fault_here = p.fault_active && row == p.fault_row && p.fault_col < p.n;
+            const bool fault_problem = p.fault_active && x.b == p.fault_batch;
+            const bool fault_here = fault_problem && row == p.fault_row && p.fault_col < p.n;
+            int32_t* const cb = p.c + x.b * p.c_bstride;  // this problem's C
             long long rsum = 0;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
@@ -477,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (row0 < p.m) tma_store_2d(&tmC, buf, col0, row0);
+                        if (row0 < p.m) tma_store_3d(&tmC, buf, col0, row0, x.b);
                         bulk_commit();
                     }
                     ++chunk_ctr;
@@ -498,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                         const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 128 + ((cq ^ (r & 7)) << 4));
                         const int grow = row0 + r;
                         if (grow < p.m && gcol < p.n) {
-                            int32_t* dst = p.c + static_cast<int64_t>(grow) * p.ldc + gcol;
+                            int32_t* dst = cb + static_cast<int64_t>(grow) * p.ldc + gcol;
                             if (gcol + 3 < p.n) {
                                 *reinterpret_cast<uint4*>(dst) = val;
                             } else {
@@ -510,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     __syncwarp();
                 } else if constexpr (EPI == kEpiDirect) {
                     if (row < p.m) {
-                        int32_t* crow = p.c + static_cast<int64_t>(row) * p.ldc;
+                        int32_t* crow = cb + static_cast<int64_t>(row) * p.ldc;
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (col0 + j < p.n) crow[col0 + j] = static_cast<int32_t>(v[j]);
@@ -540,17 +547,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     const unsigned long long add = (static_cast<unsigned long long>(cs_part) << 32) |
                                                    (1ull << kRowAccCountShift) |
                                                    static_cast<unsigned long long>(mod127(rsum));
-                    const unsigned long long v = atomicAdd(&p.row_acc[row], add) + add;
+                    unsigned long long* racc = p.row_acc + static_cast<int64_t>(x.b) * p.m + row;
+                    const unsigned long long v = atomicAdd(racc, add) + add;
                     if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.n_tiles)) {
                         fin = 1;
                         int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
-                        if (p.fault_active && row == p.fault_row && p.fault_col == p.n)
+                        if (fault_problem && row == p.fault_row && p.fault_col == p.n)
                             csv ^= static_cast<int32_t>(1u << p.fault_bit);  // fault in C'[:, n]
                         const uint32_t res = static_cast<uint32_t>(v & kRowAccResMask) % 127u;
                         flag = static_cast<int32_t>(res) != mod127(csv);
-                        p.flags[row] = static_cast<uint8_t>(flag);
-                        p.csum[static_cast<int64_t>(row) * p.csum_ld] = csv;
-                        p.row_acc[row] = 0ull;  // self-resetting workspace
+                        p.flags[x.b * p.flags_bstride + row] = static_cast<uint8_t>(flag);
+                        p.csum[x.b * p.csum_bstride + static_cast<int64_t>(row) * p.csum_ld] = csv;
+                        *racc = 0ull;  // self-resetting workspace
                     }
                 }
                 if (trace && local == 0 && threadIdx.x == 64) trace[8] = globaltimer();
@@ -558,10 +566,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 const uint32_t nflag = __popc(__ballot_sync(0xffffffffu, flag));
                 if (lane == 0 && nfin) {
                     // (finished rows) << 32 | (flagged rows); the call's last finished row publishes
-                    const unsigned long long prev = atomicAdd(p.err_pack, (static_cast<unsigned long long>(nfin) << 32) | nflag);
+                    const unsigned long long prev =
+                        atomicAdd(p.err_pack + x.b, (static_cast<unsigned long long>(nfin) << 32) | nflag);
                     if ((prev >> 32) + nfin == static_cast<unsigned long long>(p.m)) {
-                        *p.err_count = static_cast<uint32_t>(prev) + nflag;
-                        *p.err_pack = 0ull;
+                        p.err_count[x.b] = static_cast<uint32_t>(prev) + nflag;
+                        p.err_pack[x.b] = 0ull;
                     }
                 }
             }

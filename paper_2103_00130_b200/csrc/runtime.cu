@@ -51,20 +51,6 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 2D row-major tensor: `inner` elements per row (contiguous), `outer` rows, `row_bytes` pitch.
-static CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
-                               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof(map));
-    const cuuint64_t dims[2] = {inner, outer};
-    const cuuint64_t strides[1] = {row_bytes};
-    const cuuint32_t box[2] = {box_inner, box_outer};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (code " + std::to_string(int(r)) + ")");
-    return map;
-}
 
 // ------------------------------------------------------------------ per-stream workspace
 // Scratch that must not live in the shared immutable weight/table handles: kernels
@@ -77,7 +63,9 @@ struct Workspace {
     int64_t partial_cap = 0;
     uint32_t* part_flag = nullptr;  // GEMM split-K hand-over flags (self-resetting)
     int64_t part_flag_cap = 0;
-    uint32_t* small = nullptr;  // [2] verify acc [3] verify blocks [4] eb flag acc [5] eb blocks [6..7] eb bag counter (u64) [8..9] GEMM err_pack (u64) [12] eb validate count
+    unsigned long long* err_pack = nullptr;  // GEMM per-problem (rows finished, rows flagged)
+    int64_t err_pack_cap = 0;
+    uint32_t* small = nullptr;  // [2] verify acc [3] verify blocks [4] eb flag acc [5] eb blocks [6..7] eb bag counter (u64) [12] eb validate count
     uint8_t* scratch = nullptr;  // A repack buffer
     size_t scratch_cap = 0;
     std::mutex mu;
@@ -125,32 +113,56 @@ int gemm_box_a(int bn);
 int gemm_box_b(int bn);
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
 
-// 3D view {128 bytes of a k-block, rows, k-blocks} of a K-contiguous byte matrix. `row_bytes` is
-// the row pitch, `kb_bytes` the step between k-blocks (128 for row-major A; n_pad*128 for B').
+// 4D view {128 bytes of a k-block, rows, k-blocks, batch} of K-contiguous byte matrices. `row_bytes` is
+// the row pitch, `kb_bytes` the step between k-blocks (128 for row-major A; n_pad*128 for B'),
+// `batch_bytes` the step between problems (unused when batch == 1).
 static CUtensorMap make_map_kblocks(const void* base, uint64_t rows, uint64_t kblocks, uint64_t row_bytes,
-                                    uint64_t kb_bytes, uint32_t box_rows, uint32_t box_kb) {
+                                    uint64_t kb_bytes, uint32_t box_rows, uint32_t box_kb, uint64_t batch = 1,
+                                    uint64_t batch_bytes = 0) {
     CUtensorMap map;
     std::memset(&map, 0, sizeof(map));
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kBK), rows, kblocks};
-    const cuuint64_t strides[2] = {row_bytes, kb_bytes};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), box_rows, box_kb};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+    if (batch <= 1) batch_bytes = kb_bytes * kblocks + row_bytes * rows;  // any valid stride for a unit dim
+    batch_bytes = (batch_bytes + 15) / 16 * 16;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(kBK), rows, kblocks, batch < 1 ? 1 : batch};
+    const cuuint64_t strides[3] = {row_bytes, kb_bytes, batch_bytes};
+    const cuuint32_t box[4] = {static_cast<cuuint32_t>(kBK), box_rows, box_kb, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(3d) failed (code " + std::to_string(int(r)) + ")");
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(4d) failed (code " + std::to_string(int(r)) + ")");
+    return map;
+}
+
+// 3D view {columns, rows, batch} of int32 C matrices, 32x32 boxes (TMA-store epilogue).
+static CUtensorMap make_map_c(const void* base, uint64_t n, uint64_t m, uint64_t ldc, uint64_t batch, uint64_t bstride) {
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    const uint64_t bb = batch <= 1 ? ldc * 4 * m : bstride * 4;
+    const cuuint64_t dims[3] = {n, m, batch < 1 ? 1 : batch};
+    const cuuint64_t strides[2] = {ldc * 4, (bb + 15) / 16 * 16};
+    const cuuint32_t box[3] = {32, 32, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(C) failed (code " + std::to_string(int(r)) + ")");
     return map;
 }
 
 static int bn_index(int bn) { return bn == 64 ? 0 : bn == 128 ? 1 : 2; }
 
-void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
+void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st,
+                        int64_t batch, int64_t b_bstride) {
     if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
     if (!d_b) throw std::invalid_argument("null argument");
     if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
+    if (batch < 1) throw std::invalid_argument("abftlp_gemm_encode: batch < 1");
+    if (batch > 1 && b_bstride < ldb * (k - 1) + n) throw std::invalid_argument("abftlp_gemm_encode: batch stride too small");
     const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, kRowAlign);
-    const size_t need_bt = static_cast<size_t>(n_pad * k_pad);
-    if (!w.bt || need_bt > w.bt_cap || static_cast<size_t>(k_pad) > w.cs_cap) {
+    const size_t per_bt = static_cast<size_t>(n_pad * k_pad);
+    const size_t need_bt = per_bt * static_cast<size_t>(batch), need_cs = static_cast<size_t>(k_pad * batch);
+    if (!w.bt || need_bt > w.bt_cap || need_cs > w.cs_cap) {
         if (w.bt) {
             cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
             cudaFree(w.bt);
@@ -159,25 +171,35 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
             w.cs = nullptr;
         }
         cuda_check(cudaMalloc(&w.bt, need_bt), "cudaMalloc(B')");
-        cuda_check(cudaMalloc(&w.cs, static_cast<size_t>(k_pad)), "cudaMalloc(cs)");
+        cuda_check(cudaMalloc(&w.cs, need_cs), "cudaMalloc(cs)");
         w.bt_cap = need_bt;
-        w.cs_cap = static_cast<size_t>(k_pad);
+        w.cs_cap = need_cs;
     }
     w.k = k;
     w.n = n;
     w.k_pad = k_pad;
     w.n_pad = n_pad;
-    cuda_check(launch_encode_weight(d_b, k, n, ldb, w, st), "encode_weight_kernel");
+    w.batch = batch;
+    w.bt_bstride = static_cast<int64_t>(per_bt);
+    w.cs_bstride = k_pad;
+    for (int64_t b = 0; b < batch; ++b) {
+        GemmWeight one = w;
+        one.bt = w.bt + b * w.bt_bstride;
+        one.cs = w.cs + b * w.cs_bstride;
+        cuda_check(launch_encode_weight(d_b + b * b_bstride, k, n, ldb, one, st), "encode_weight_kernel");
+    }
     for (int bn : {64, 128, 256})
         w.map_b[bn_index(bn)] = make_map_kblocks(w.bt, static_cast<uint64_t>(n_pad), static_cast<uint64_t>(k_pad / kBK),
-                                                 kBK, static_cast<uint64_t>(n_pad * kBK), bn / 2, gemm_box_b(bn));
+                                                 kBK, static_cast<uint64_t>(n_pad * kBK), bn / 2, gemm_box_b(bn),
+                                                 static_cast<uint64_t>(batch), static_cast<uint64_t>(w.bt_bstride));
 }
 
-GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st) {
+GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st, int64_t batch,
+                          int64_t b_bstride) {
     if (k <= 0 || n <= 0) throw std::invalid_argument("compute_row_checksums: empty matrix");
     auto* w = new GemmWeight();
     try {
-        encode_weight_into(*w, d_b, k, n, ldb, st);
+        encode_weight_into(*w, d_b, k, n, ldb, st, batch, b_bstride);
     } catch (...) {
         free_weight(w);
         throw;
@@ -257,7 +279,15 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
 
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
-          cudaStream_t st, const GemmTiling* force, const RequantArgs* rq) {
+          cudaStream_t st, const GemmTiling* force, const RequantArgs* rq, const GemmBatch* batch) {
+    const GemmBatch one{};
+    const GemmBatch& bt = batch ? *batch : one;
+    const int64_t nb = bt.batch;
+    if (nb < 1) throw std::invalid_argument("abft_gemm: batch < 1");
+    if (nb > 1 && w.batch != 1 && w.batch != nb) throw std::invalid_argument("abft_gemm: weight batch mismatch");
+    if (nb == 1 && w.batch != 1) throw std::invalid_argument("abft_gemm: batched weight needs a batched call");
+    if (nb > 1 && (rq || (bt.a_bstride % 16) != 0 || bt.a_bstride < lda * (m - 1) + w.k))
+        throw std::invalid_argument("abft_gemm: unsupported batch layout");
     if (m < 0) throw std::invalid_argument("abft_gemm: negative m");
     if (m > 0 && (!d_a || (!d_c && !rq))) throw std::invalid_argument("null argument");
     if (rq) {
@@ -272,23 +302,25 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     const bool has_fault = fault && fault->active;
     if (has_fault) {
         if (!checked) throw std::invalid_argument("abft_gemm: fault hook needs the checked kernel");
-        if (fault->row < 0 || fault->row >= m || fault->col < 0 || fault->col > w.n || fault->bit > 31)
+        if (fault->row < 0 || fault->row >= m || fault->col < 0 || fault->col > w.n || fault->bit > 31 ||
+            bt.fault_batch < 0 || bt.fault_batch >= nb)
             throw std::out_of_range("abft_gemm: fault coordinates out of range");
     }
     if (m == 0) {
-        if (checked) cuda_check(cudaMemsetAsync(d_err_count, 0, sizeof(uint32_t), st), "cudaMemsetAsync");
+        if (checked) cuda_check(cudaMemsetAsync(d_err_count, 0, sizeof(uint32_t) * nb, st), "cudaMemsetAsync");
         return;
     }
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
 
-    // A is read through a 3D view {128 B, rows, k-blocks}: base and pitch must be 16-byte aligned and
-    // the last (partial) k-block must stay inside the allocation. Otherwise repack into scratch.
+    // A is read through a 4D view {128 B, rows, k-blocks, batch}: base and pitch must be 16-byte aligned
+    // and the last (partial) k-block must stay inside the allocation. Otherwise repack into scratch.
     const uint8_t* a = d_a;
-    int64_t a_ld = lda;
+    int64_t a_ld = lda, a_bstride = bt.a_bstride;
     if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0 || (w.k % kBK != 0 && lda < w.k_pad)) {
         a_ld = w.k_pad;
-        const size_t need = static_cast<size_t>(a_ld * m);
+        a_bstride = a_ld * m;
+        const size_t need = static_cast<size_t>(a_ld * m * nb);
         if (need > ws.scratch_cap) {
             if (ws.scratch) {
                 cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
@@ -297,22 +329,29 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
             cuda_check(cudaMalloc(&ws.scratch, need), "cudaMalloc(A scratch)");
             ws.scratch_cap = need;
         }
-        cuda_check(cudaMemcpy2DAsync(ws.scratch, a_ld, d_a, lda, w.k, m, cudaMemcpyDeviceToDevice, st),
-                   "cudaMemcpy2DAsync(A repack)");
+        for (int64_t b = 0; b < nb; ++b)
+            cuda_check(cudaMemcpy2DAsync(ws.scratch + b * a_bstride, a_ld, d_a + b * bt.a_bstride, lda, w.k, m,
+                                         cudaMemcpyDeviceToDevice, st),
+                       "cudaMemcpy2DAsync(A repack)");
         a = ws.scratch;
     }
-    const bool c_tma_ok = d_c && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0;
-    GemmTiling t = force ? *force : choose_tiling(m, w.n, w.k_pad, checked, c_tma_ok, has_fault);
+    const bool c_tma_ok = d_c && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(d_c) % 16) == 0 &&
+                          (nb == 1 || (bt.c_bstride % 4) == 0);
+    GemmTiling t = force ? *force : choose_tiling(nb * round_up(m, kPairM), w.n, w.k_pad, checked, c_tma_ok, has_fault);
+    if (nb > 1) t.split = 1;
     if (!c_tma_ok && t.epi != kEpiNone) t.epi = kEpiDirect;
     if (!d_c) t.epi = kEpiNone;  // requantized output only
 
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
     const int64_t kb = w.k_pad / kBK;
-    if (m_tiles * n_tiles > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
+    if (nb * m_tiles * n_tiles * t.split > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
 
     if (checked && n_tiles > kMaxCheckedNTiles) throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
-    if (checked) grow(ws.row_acc, ws.rows_cap, m, st);
+    if (checked) {
+        grow(ws.row_acc, ws.rows_cap, m * nb, st);
+        grow(ws.err_pack, ws.err_pack_cap, nb, st);
+    }
 
     GemmParams p{};
     p.m = static_cast<int>(m);
@@ -321,7 +360,14 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.k_blocks = static_cast<int>(kb);
     p.n_tiles = static_cast<int>(n_tiles);
     p.m_tiles = static_cast<int>(m_tiles);
-    p.num_tiles = static_cast<int>(m_tiles * n_tiles);
+    p.num_tiles = static_cast<int>(nb * m_tiles * n_tiles);
+    p.batch = static_cast<int>(nb);
+    p.b_shared = w.batch == 1 ? 1 : 0;
+    p.a_bstride = a_bstride;
+    p.cs_bstride = w.batch == 1 ? 0 : w.cs_bstride;
+    p.c_bstride = bt.c_bstride;
+    p.csum_bstride = bt.csum_bstride;
+    p.flags_bstride = bt.flags_bstride;
     p.split = t.split;
     if (t.split == 2) {
         p.kb_half = static_cast<int>(gemm_kb_split(kb, gemm_ks(t.bn)));
@@ -340,7 +386,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.lda = a_ld;
     p.cs = w.cs;
     p.row_acc = ws.row_acc;
-    p.err_pack = reinterpret_cast<unsigned long long*>(ws.small + 8);
+    p.err_pack = ws.err_pack;
     p.trace = g_trace;
     if (rq) {
         p.rq_row_sum_a = rq->row_sum_a;
@@ -351,17 +397,20 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     }
     if (has_fault) {
         p.fault_active = 1;
+        p.fault_batch = static_cast<int>(bt.fault_batch);
         p.fault_row = static_cast<int>(fault->row);
         p.fault_col = static_cast<int>(fault->col);
         p.fault_bit = static_cast<int>(fault->bit);
     }
-    // box = half a stage's k-blocks: two producer warps load the two halves in parallel
+    // box = a stage's k-blocks split over the A producer warps
     const CUtensorMap map_a = make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
-                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_box_a(t.bn));
+                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_box_a(t.bn),
+                                               static_cast<uint64_t>(nb), static_cast<uint64_t>(a_bstride));
     CUtensorMap map_c;
     std::memset(&map_c, 0, sizeof(map_c));
     if (t.epi == kEpiTmaStore)
-        map_c = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_INT32, d_c, w.n, m, ldc * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+        map_c = make_map_c(d_c, static_cast<uint64_t>(w.n), static_cast<uint64_t>(m), static_cast<uint64_t>(ldc),
+                           static_cast<uint64_t>(nb), static_cast<uint64_t>(bt.c_bstride));
     const int pairs = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.num_tiles) * p.split,
                                                          std::max(1, device_sm_count() / 2)));
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),

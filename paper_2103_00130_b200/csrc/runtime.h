@@ -16,9 +16,12 @@ struct Fault {
 };
 
 // ---- GEMM (replaces P:src/gemm_abft.hpp:23-74)
-GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st);
+// batch > 1: `batch` independent weights, weight b at d_b + b * b_bstride (batched GEMM).
+GemmWeight* encode_weight(const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st, int64_t batch = 1,
+                          int64_t b_bstride = 0);
 // Re-encode into an existing handle, growing its buffers only when needed (campaign scratch).
-void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st);
+void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, int64_t ldb, cudaStream_t st,
+                        int64_t batch = 1, int64_t b_bstride = 0);
 // Logical k x (n+1) [B | cs] matrix, row-major (PackedEncodedWeight::at contract).
 void read_encoded(const GemmWeight& w, int8_t* d_out, cudaStream_t st);
 void set_checksums(GemmWeight& w, const int8_t* d_cs, cudaStream_t st);
@@ -34,9 +37,21 @@ struct RequantArgs {
     int64_t ld_out = 0;
 };
 void check_requant_params(const RequantDev& q);
+// Batched GEMM: `batch` problems of one shape in one launch; problem b reads A at + b*a_bstride bytes and
+// weight b of a batched weight (or weight 0 of a single one) and writes C/csum/flags at its strides and
+// err_count[b]. Fault (if any) applies to problem fault_batch.
+struct GemmBatch {
+    int64_t batch = 1;
+    int64_t a_bstride = 0;     // bytes
+    int64_t c_bstride = 0;     // int32 elements
+    int64_t csum_bstride = 0;  // int32 elements
+    int64_t flags_bstride = 0; // bytes
+    int64_t fault_batch = 0;
+};
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
-          cudaStream_t st, const GemmTiling* force = nullptr, const RequantArgs* rq = nullptr);
+          cudaStream_t st, const GemmTiling* force = nullptr, const RequantArgs* rq = nullptr,
+          const GemmBatch* batch = nullptr);
 void requantize(const int32_t* d_c, int64_t ldc, int64_t m, int64_t n, const int32_t* d_row_sum_a,
                 const int32_t* d_col_sum_b, const RequantDev& q, uint8_t* d_out, int64_t ld_out, cudaStream_t st);
 void row_sums_u8(const uint8_t* d_a, int64_t m, int64_t k, int64_t lda, int32_t* d_out, cudaStream_t st);

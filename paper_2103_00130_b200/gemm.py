@@ -166,3 +166,56 @@ def verify_checksums(c: IntermediateMatrix, flags: torch.Tensor | None = None) -
     _lib.call("abftlp_gemm_verify", ptr(data) if m else None, cols, csum, cols, m, n, ptr(flags), ptr(err),
               stream_handle())
     return int(err.item())
+
+
+class PackedEncodedWeightBatch:
+    """`batch` independent encoded weights of one shape (abftlp_gemm_encode_batched): the operand of the
+    one-launch batched GEMM (e.g. the reference's seeded trials, each with its own A and B)."""
+
+    def __init__(self, b, stream=None):
+        bt = to_device(b, torch.int8)
+        if bt.dim() != 3:
+            raise ValueError("PackedEncodedWeightBatch: B must be [batch, k, n]")
+        self._batch, self._k, self._n = (int(s) for s in bt.shape)
+        self._h = C.c_void_p()
+        _lib.call("abftlp_gemm_encode_batched", ptr(bt), self._batch, self._k, self._n, self._n, self._k * self._n,
+                  stream_handle(stream), C.byref(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib.abftlp_gemm_weight_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def batch(self) -> int:
+        return self._batch
+
+    def k(self) -> int:
+        return self._k
+
+    def n(self) -> int:
+        return self._n
+
+
+def abft_gemm_batched(a, pb: PackedEncodedWeightBatch, fault: tuple[int, int, int, int] | None = None, stream=None):
+    """`batch` checked GEMMs in one launch: a is [batch, m, k] u8. Returns (cTemp [batch, m, n+1] int32 with
+    the checksum column last, errCount [batch] int32, rowFlags [batch, m] u8) as device tensors.
+    ``fault=(problem, row, col, bit)`` flips one bit of that problem's C' in the epilogue."""
+    at = to_device(a, torch.uint8)
+    if at.dim() != 3 or int(at.shape[0]) != pb.batch() or int(at.shape[2]) != pb.k():
+        raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "abft_gemm: dimension mismatch")
+    nb, m, k = (int(s) for s in at.shape)
+    n = pb.n()
+    dev = device()
+    ctemp = torch.zeros((nb, m, n + 1), dtype=torch.int32, device=dev)
+    flags = torch.zeros((nb, m), dtype=torch.uint8, device=dev)
+    err = torch.zeros(nb, dtype=torch.int32, device=dev)
+    f = C.byref(_lib.BatchFault(1, *fault)) if fault is not None else None
+    _lib.call("abftlp_gemm_checked_batched", ptr(at), nb, m, k, m * k, pb.handle, ptr(ctemp), n + 1, m * (n + 1),
+              C.c_void_p(ctemp.data_ptr() + 4 * n), n + 1, m * (n + 1), ptr(flags), m, ptr(err), f,
+              stream_handle(stream))
+    return ctemp, err, flags
