@@ -340,6 +340,8 @@ def run_gpu_arm(args, rank, world, dist):
     e2e_tops = world * e2e_runs * OPS / e2e_s / 1e12
 
     secondary = eb_secondary(L, dev, st, vp, pk) if (rank == 0 and not args.no_eb) else None
+    if rank == 0 and secondary is not None:
+        secondary["G1"] = g1_secondary(L, dev, st, vp, pk)
 
     L.lib.abftlp_gemm_weight_free(w)
     if rank != 0:
@@ -393,6 +395,82 @@ def run_gpu_arm(args, rank, world, dist):
         line["cpu_baseline"] = {"value": tops, "unit": "TOPS", "cores": threads, "kind": kind,
                                 "sample": f"{threads} concurrent G2 abft_gemm calls ({dt:.1f} s wall)"}
     print(json.dumps(line), flush=True)
+
+
+def g1_secondary(L, dev, st, vp, pk):
+    """BASELINE configs[0] (G1): 100 seeded checked GEMMs m=64 k=512 n=512 (each trial its own A and B,
+    the reference's draw protocol, stream t*4), half with one C' bit flip (stream t*4+1 draws) -- ONE
+    batched launch (abftlp_gemm_checked_batched) vs 100 single launches, both replayed as CUDA graphs."""
+    import torch
+    from paper_2103_00130_b200.rng import SplitMix64
+    nb, m, n, k = 100, 64, 512, 512
+    a = torch.empty((nb, m, k), dtype=torch.uint8, device=dev)
+    b = torch.empty((nb, k, n), dtype=torch.int8, device=dev)
+    for t in range(nb):
+        L.call("abftlp_generate", vp(a[t]), m * k, SEED, t * 4, 0, 0, 0.0, 0.0, 0, st)
+        L.call("abftlp_generate", vp(b[t]), k * n, SEED, t * 4, m * k, 1, 0.0, 0.0, 0, st)
+    wb = C.c_void_p()
+    L.call("abftlp_gemm_encode_batched", vp(b), nb, k, n, n, k * n, st, C.byref(wb))
+    ws = []
+    for t in range(nb):
+        w = C.c_void_p()
+        L.call("abftlp_gemm_encode", vp(b[t]), k, n, n, st, C.byref(w))
+        ws.append(w)
+    c = torch.empty((nb, m, n + 1), dtype=torch.int32, device=dev)
+    fl = torch.empty((nb, m), dtype=torch.uint8, device=dev)
+    err = torch.empty(nb, dtype=torch.int32, device=dev)
+    faults = []
+    for t in range(1, nb, 2):
+        r = SplitMix64(SEED, t * 4 + 1)
+        faults.append((t, r.next_below(m), r.next_below(n + 1), r.next_below(32)))
+
+    def batched(fault=None):
+        f = C.byref(L.BatchFault(1, *fault)) if fault else None
+        L.call("abftlp_gemm_checked_batched", vp(a), nb, m, k, m * k, wb, vp(c), n + 1, m * (n + 1),
+               C.c_void_p(c.data_ptr() + 4 * n), n + 1, m * (n + 1), vp(fl), m, vp(err), f, st)
+
+    def separate():
+        for t in range(nb):
+            L.call("abftlp_gemm_checked", vp(a[t]), m, k, ws[t], vp(c[t]), n + 1, C.c_void_p(c[t].data_ptr() + 4 * n),
+                   n + 1, vp(fl[t]), vp(err[t:t + 1]), None, st)
+
+    stream = torch.cuda.current_stream()
+    res = {}
+    for name, fn in (("batched", batched), ("separate", separate)):
+        fn()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(10):
+                g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3 / 10)
+        res[name] = statistics.median(ts)
+        del g
+    # verdict parity of the G1 protocol: every odd trial's single flip detected, no false positive
+    batched()
+    clean_ok = int(err.sum().item()) == 0
+    det = 0
+    for fault in faults:
+        batched(fault)
+        det += int(err[fault[0]].item() == 1 and int(err.sum().item()) == 1)
+    for w in ws:
+        L.lib.abftlp_gemm_weight_free(w)
+    L.lib.abftlp_gemm_weight_free(wb)
+    ops = 2 * m * n * k * nb
+    alg = nb * (m * k + k * (n + 1) + 4 * m * (n + 1) + m)
+    return {"trials": nb, "batched_us_per_100": res["batched"], "separate_us_per_100": res["separate"],
+            "batched_tops": ops / (res["batched"] * 1e-6) / 1e12, "alg_gbs": alg / (res["batched"] * 1e-6) / 1e9,
+            "hbm_frac": alg / (res["batched"] * 1e-6) / 1e9 / pk["hbm_gbs"], "clean_unflagged": clean_ok,
+            "faults_detected": f"{det}/{len(faults)}",
+            "note": "one abftlp_gemm_checked_batched launch for the 100 trials vs 100 abftlp_gemm_checked launches"}
 
 
 def eb_secondary(L, dev, st, vp, pk):
