@@ -342,6 +342,7 @@ def run_gpu_arm(args, rank, world, dist):
     secondary = eb_secondary(L, dev, st, vp, pk) if (rank == 0 and not args.no_eb) else None
     if rank == 0 and secondary is not None:
         secondary["G1"] = g1_secondary(L, dev, st, vp, pk)
+        secondary["D5_shard"] = d5_secondary(L, dev, st, vp, pk)
 
     L.lib.abftlp_gemm_weight_free(w)
     if rank != 0:
@@ -471,6 +472,97 @@ def g1_secondary(L, dev, st, vp, pk):
             "hbm_frac": alg / (res["batched"] * 1e-6) / 1e9 / pk["hbm_gbs"], "clean_unflagged": clean_ok,
             "faults_detected": f"{det}/{len(faults)}",
             "note": "one abftlp_gemm_checked_batched launch for the 100 trials vs 100 abftlp_gemm_checked launches"}
+
+
+def d5_secondary(L, dev, st, vp, pk, G=8):
+    """BASELINE configs[4] (D5), ONE GPU's share at G=8 (table-wise EB shards, MLP split by N): 64/G = 8
+    int8-rowwise tables of 1M x 128 (fp32 scale/bias), batch 8192, Zipf(1.05) pooling 80, checked lookups
+    written by the scatter kernel straight into the all-to-all send buffer [G][B/G][8][128]; plus the checked
+    MLP GEMMs m=8192 with (k, n/G) for (k, n) in {512,1024,2048}^2. Synthetic seeded data."""
+    import torch
+    T_loc, R, d, B, pool = 64 // G, 1_000_000, 128, 8192, 80
+    rng = np.random.default_rng(5)
+    ranks = np.arange(1, R + 1, dtype=np.float64)
+    cdf = np.cumsum(ranks ** -1.05)
+    cdf /= cdf[-1]
+    tabs, rows_keep, bags = [], [], []
+    for t in range(T_loc):
+        rows = torch.randint(-128, 128, (R, d), dtype=torch.int8, device=dev)
+        sc = torch.rand(R, device=dev) * 9e-3 + 1e-3
+        bi = torch.rand(R, device=dev) * 2 - 1
+        h = C.c_void_p()
+        L.call("abftlp_eb_table_create", 0, vp(rows), R, d, d, 0, vp(sc), vp(bi), None, st, C.byref(h))
+        perm = rng.permutation(R)
+        idx = perm[np.searchsorted(cdf, rng.random(B * pool))].astype(np.int64)
+        off = torch.arange(0, B * pool + 1, pool, dtype=torch.int64, device=dev)
+        tabs.append(h)
+        rows_keep.append((rows, sc, bi))
+        bags.append((off, torch.from_numpy(idx).to(dev)))
+    Bg = B // G
+    send = torch.empty((G, Bg, T_loc, d), dtype=torch.float32, device=dev)
+    send_f = torch.empty((G, Bg, T_loc), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    dests = []
+    for slot in range(T_loc):
+        o = torch.tensor([send[g, 0, slot].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
+        f = torch.tensor([send_f[g, 0, slot:].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
+        dests.append((o, f))
+
+    def eb_step():
+        for slot in range(T_loc):
+            off, ix = bags[slot]
+            o, f = dests[slot]
+            L.call("abftlp_eb_checked_scatter", tabs[slot], vp(off), vp(ix), B, None, vp(o), T_loc * d, vp(f), T_loc,
+                   Bg, vp(cnt), None, st)
+
+    shapes = [(k, n // G) for k in (512, 1024, 2048) for n in (512, 1024, 2048)]
+    mlp = []
+    m = 8192
+    for k, n in shapes:
+        bw = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev)
+        w = C.c_void_p()
+        L.call("abftlp_gemm_encode", vp(bw), k, n, n, st, C.byref(w))
+        a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device=dev)
+        c = torch.empty((m, n), dtype=torch.int32, device=dev)
+        cs = torch.empty(m, dtype=torch.int32, device=dev)
+        fl = torch.empty(m, dtype=torch.uint8, device=dev)
+        er = torch.empty(1, dtype=torch.int32, device=dev)
+        mlp.append((k, n, w, a, c, cs, fl, er, bw))
+
+    def mlp_step():
+        for k, n, w, a, c, cs, fl, er, _ in mlp:
+            L.call("abftlp_gemm_checked", vp(a), m, k, w, vp(c), n, vp(cs), 1, vp(fl), vp(er), None, st)
+
+    def timed(fn, reps=8):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        return statistics.median(ts)
+
+    eb_us = timed(eb_step)
+    mlp_us = timed(mlp_step)
+    lookups = T_loc * B * pool
+    alg = lookups * (d + 4 + 4 + 4 + 8) + T_loc * (8 * (B + 1) + 4 * B * d + B)
+    ops = sum(2 * m * n * k for k, n, *_ in mlp)
+    for k, n, w, *_ in mlp:
+        L.lib.abftlp_gemm_weight_free(w)
+    for h in tabs:
+        L.lib.abftlp_eb_table_free(h)
+    return {"workload": f"D5 per-GPU share at G={G}: {T_loc} tables x 1M x 128 int8, batch {B}, pooling {pool}, "
+                        "Zipf(1.05); 9 checked MLP GEMMs m=8192 (k, n/G)",
+            "eb_us": eb_us, "eb_lookups": lookups, "eb_alg_gbs": alg / (eb_us * 1e-6) / 1e9,
+            "eb_hbm_frac": alg / (eb_us * 1e-6) / 1e9 / pk["hbm_gbs"],
+            "alltoall_send_bytes": int(send.numel() * 4 + send_f.numel()),
+            "mlp_us": mlp_us, "mlp_tops": ops / (mlp_us * 1e-6) / 1e12,
+            "note": "EB outputs land in the all-to-all send buffer via abftlp_eb_checked_scatter; at N=1 the "
+                    "exchange itself is not run (multi-rank path: paper_2103_00130_b200/sharded.py)"}
 
 
 def eb_secondary(L, dev, st, vp, pk):
