@@ -165,6 +165,7 @@ struct EbParams {
     uint32_t* ws_block_cnt;
     unsigned long long* ws_bag_ctr;  // persistent kernels' next-bag counter (self-resetting)
     unsigned long long* trace;       // debug: per-warp timeline (16 slots), nullptr = off
+    float neg_zero;                  // -0.0f, passed at run time (see f2_fma in eb.cu)
     // scatter mode (table-wise sharded exchange fused into the lookups): when out_dest is set, bag b
     // writes out_dest[b / bags_per_dest] + (b % bags_per_dest) * ld_out and its flag to
     // flag_dest[b / bags_per_dest][(b % bags_per_dest) * flag_ld] (pointers may be NVLink peer memory)

@@ -395,6 +395,47 @@ __device__ __forceinline__ float decode_fast(W w, int c) {
         return splice_u2f(static_cast<uint32_t>(w >> (4 * c)) & 0xFu, 8388608.0f);
 }
 
+// Packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2): two columns per instruction with IEEE round-to-
+// nearest on each lane, i.e. bit-identical to the scalar ops. A product is formed as fma(a, b, nz) with nz
+// = -0.0 supplied at RUN time: round(a*b + -0) == round(a*b) for every a, b, and because ptxas cannot see
+// that nz is -0 it cannot contract the product with the following add (it does contract a plain
+// mul.rn.f32x2 + add.rn.f32x2 pair into one FFMA2, which would change the rounding).
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// Columns c, c+1 of a lane word as spliced floats (before the magic subtraction).
+template <int ELEM, typename W>
+__device__ __forceinline__ unsigned long long decode_pair_bits(W w, int c) {
+    uint32_t lo, hi;
+    if constexpr (ELEM == kEbU4) {
+        lo = static_cast<uint32_t>(w >> (4 * c)) & 0xFu;
+        hi = static_cast<uint32_t>(w >> (4 * c + 4)) & 0xFu;
+    } else {
+        lo = static_cast<uint32_t>(w >> (8 * c)) & 0xFFu;
+        hi = static_cast<uint32_t>(w >> (8 * c + 8)) & 0xFFu;
+        if constexpr (ELEM == kEbS8) {
+            lo ^= 0x80u;
+            hi ^= 0x80u;
+        }
+    }
+    return static_cast<unsigned long long>(0x4B000000u | lo) | (static_cast<unsigned long long>(0x4B000000u | hi) << 32);
+}
+
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
 __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
@@ -457,6 +498,12 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
         float acc[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) acc[c] = 0.0f;
+        unsigned long long acc2[CPL / 2 > 0 ? CPL / 2 : 1];  // packed column pairs (CPL >= 2)
+#pragma unroll
+        for (int c = 0; c < (CPL / 2 > 0 ? CPL / 2 : 1); ++c) acc2[c] = 0ull;  // (+0.0, +0.0)
+        const unsigned long long nz2 = f2_pack(p.neg_zero, p.neg_zero);
+        const unsigned long long magic2 = f2_pack(-8388608.0f - (ELEM == kEbS8 ? 128.0f : 0.0f),
+                                                  -8388608.0f - (ELEM == kEbS8 ? 128.0f : 0.0f));
         double csum = 0.0;
         bool oob = false;
         const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
@@ -534,11 +581,23 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
                 smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
                 const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
                 const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
+                if constexpr (CPL >= 2) {
+                    const unsigned long long s2 = f2_pack(s, s), b2 = f2_pack(b, b);
+                    const unsigned long long w2 = f2_pack(w, w);
 #pragma unroll
-                for (int c = 0; c < CPL; ++c) {
-                    float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(word, c)), b);
-                    if constexpr (WEIGHTED) x = __fmul_rn(w, x);
-                    acc[c] = __fadd_rn(acc[c], x);
+                    for (int c = 0; c < CPL; c += 2) {
+                        const unsigned long long q2 = f2_add(decode_pair_bits<ELEM>(word, c), magic2);
+                        unsigned long long x2 = f2_add(f2_fma(s2, q2, nz2), b2);
+                        if constexpr (WEIGHTED) x2 = f2_fma(w2, x2, nz2);
+                        acc2[c / 2] = f2_add(acc2[c / 2], x2);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < CPL; ++c) {
+                        float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(word, c)), b);
+                        if constexpr (WEIGHTED) x = __fmul_rn(w, x);
+                        acc[c] = __fadd_rn(acc[c], x);
+                    }
                 }
             }
             if constexpr (CHECKED) {
@@ -552,6 +611,10 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
             __syncwarp();  // slot `sl` may be refilled by a later issue
         }
         cp_async_wait<0>();  // drain the (empty) trailing groups before the ring is reused
+        if constexpr (CPL >= 2) {
+#pragma unroll
+            for (int c = 0; c < CPL; c += 2) f2_unpack(acc2[c / 2], acc[c], acc[c + 1]);
+        }
         csum = __shfl_sync(0xffffffffu, csum, 0);
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
         float* dst = out_row(p, bag) + slice * 32 * CPL + lane * CPL;

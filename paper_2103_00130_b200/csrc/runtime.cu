@@ -605,6 +605,7 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     p.ws_block_cnt = ws.small + 5;
     p.ws_bag_ctr = reinterpret_cast<unsigned long long*>(ws.small + 6);
     p.trace = g_eb_trace;
+    p.neg_zero = -0.0f;
     if (scatter) {
         p.out_dest = scatter->out_dest;
         p.flag_dest = checked ? scatter->flag_dest : nullptr;

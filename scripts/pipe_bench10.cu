@@ -39,6 +39,31 @@ __global__ void gather(const uint4* __restrict__ tab, const long long* __restric
     if (acc == 0x9e3779b9u) *sink = acc;
 }
 
+// cp.async variant: each 16-B piece lands in shared memory (the EmbeddingBag kernel's path)
+template <int U>
+__global__ void gather_cpasync(const uint4* __restrict__ tab, const long long* __restrict__ idx, long long n, int rec16,
+                               unsigned* sink) {
+    __shared__ __align__(16) uint4 buf[256 * U];
+    const int lanes_per_rec = rec16;
+    const long long groups_total = ((long long)gridDim.x * blockDim.x) / lanes_per_rec;
+    const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / lanes_per_rec;
+    const int part = threadIdx.x % lanes_per_rec;
+    unsigned acc = 0;
+    for (long long base = g0; base < n; base += groups_total * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long e = base + u * groups_total;
+            const long long r = e < n ? idx[e] : 0;
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(&buf[threadIdx.x * U + u]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(tab + r * rec16 + part) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc ^= buf[threadIdx.x * U + u].x;
+    }
+    if (acc == 0x9e3779b9u) *sink = acc;
+}
+
 int main(int argc, char** argv) {
     const int rec = atoi(argv[1]);
     const long long rows = atoll(argv[2]), n = atoll(argv[3]);
@@ -69,7 +94,11 @@ int main(int argc, char** argv) {
         flush<<<148 * 8, 256>>>(fb, (256 << 20) / 16, (int*)sink);
         cudaEventRecord(e0);
         const int blocks = 148 * 8;
-        if (U == 1) gather<1><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        const bool cpa = argc > 5 && atoi(argv[5]) == 1;
+        if (cpa) {
+            if (U == 4) gather_cpasync<4><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+            else gather_cpasync<8><<<blocks, 256>>>(tab, idx, n, rec16, sink);
+        } else if (U == 1) gather<1><<<blocks, 256>>>(tab, idx, n, rec16, sink);
         else if (U == 2) gather<2><<<blocks, 256>>>(tab, idx, n, rec16, sink);
         else if (U == 4) gather<4><<<blocks, 256>>>(tab, idx, n, rec16, sink);
         else gather<8><<<blocks, 256>>>(tab, idx, n, rec16, sink);
