@@ -83,3 +83,74 @@ def test_fused_epilogue_matches_oracle(Q, m, n, k, tiling, monkeypatch):
     assert np.array_equal(out2.cpu().numpy(), O.requantize(bad, n, rs, cs, prm, k))
     assert res2.errCount == 1 and int(res2.rowFlags[r].item()) == 1
     assert not res2.cTemp.data[:, :n].any()  # int32 C' skipped
+
+
+def test_dependent_chain_under_pdl_and_graph(Q):
+    """GEMM i+1 consumes GEMM i's requantized u8 output as its A on the same stream, all enqueued without
+    host synchronisation: the kernels overlap prologue/tail under programmatic dependent launch, so this
+    checks that nothing reads A before griddepcontrol.wait. Run eagerly and as a replayed CUDA graph;
+    every layer bit-exact vs the oracle."""
+    import ctypes as C
+    from paper_2103_00130_b200 import _lib
+    from paper_2103_00130_b200 import gemm as G
+    m, dims = 256, [512, 1024, 768, 512]
+    rng = np.random.default_rng(77)
+    a0 = rng.integers(0, 256, (m, dims[0])).astype(np.uint8)
+    ws = [rng.integers(-128, 128, (dims[i], dims[i + 1])).astype(np.int8) for i in range(len(dims) - 1)]
+    prm = [0.01, 0.1, 0.02, -0.05, 40.0, -20.0]
+    pbs = [G.PackedEncodedWeight(w) for w in ws]
+    css = [torch.from_numpy(O.col_sums_i8(w)).cuda() for w in ws]
+    dev = torch.device("cuda")
+    xs = [torch.from_numpy(a0).cuda()] + [torch.empty((m, dims[i + 1]), dtype=torch.uint8, device=dev)
+                                          for i in range(len(ws))]
+    cts = [torch.empty((m, dims[i + 1] + 1), dtype=torch.int32, device=dev) for i in range(len(ws))]
+    rss = [torch.empty(m, dtype=torch.int32, device=dev) for _ in ws]
+    fls = [torch.empty(m, dtype=torch.uint8, device=dev) for _ in ws]
+    errs = torch.empty(len(ws) + 1, dtype=torch.int32, device=dev)
+    prms = [_params(Q, prm, dims[i])._c() for i in range(len(ws))]
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    # a last plain checked GEMM reads the final requantized output directly: a GEMM -> GEMM PDL pair
+    w_last = rng.integers(-128, 128, (dims[-1], 300)).astype(np.int8)
+    pb_last = G.PackedEncodedWeight(w_last)
+    ct_last = torch.empty((m, 301), dtype=torch.int32, device=dev)
+    fl_last = torch.empty(m, dtype=torch.uint8, device=dev)
+
+    def chain(st):
+        for i, pb in enumerate(pbs):
+            k, n = dims[i], dims[i + 1]
+            _lib.call("abftlp_row_sums_u8", vp(xs[i]), m, k, k, vp(rss[i]), st)
+            _lib.call("abftlp_gemm_checked_requant", vp(xs[i]), m, k, pb.handle, vp(cts[i]), n + 1,
+                      C.c_void_p(cts[i].data_ptr() + 4 * n), n + 1, vp(fls[i]), C.c_void_p(errs.data_ptr() + 4 * i),
+                      None, vp(rss[i]), vp(css[i]), C.byref(prms[i]), vp(xs[i + 1]), n, st)
+        _lib.call("abftlp_gemm_checked", vp(xs[-1]), m, dims[-1], pb_last.handle, vp(ct_last), 301,
+                  C.c_void_p(ct_last.data_ptr() + 4 * 300), 301, vp(fl_last), C.c_void_p(errs.data_ptr() + 4 * len(ws)),
+                  None, st)
+
+    ref_x = a0
+    refs = []
+    for i, w in enumerate(ws):
+        ct, _, _ = O.abft_gemm(ref_x, w)
+        ref_x = O.requantize(ct, w.shape[1], O.row_sums_u8(ref_x), O.col_sums_i8(w), prm, dims[i])
+        refs.append((ct, ref_x))
+
+    def check():
+        torch.cuda.synchronize()
+        for i, (ct, rx) in enumerate(refs):
+            assert np.array_equal(cts[i].cpu().numpy(), ct), i
+            assert np.array_equal(xs[i + 1].cpu().numpy(), rx), i
+        assert np.array_equal(ct_last.cpu().numpy(), O.abft_gemm(refs[-1][1], w_last)[0])
+        assert not errs.any()
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        chain(C.c_void_p(s.cuda_stream))
+    check()
+    for t in xs[1:] + cts + [ct_last]:
+        t.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        chain(C.c_void_p(s.cuda_stream))
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            g.replay()
+    check()
