@@ -77,6 +77,7 @@ struct GemmParams {
     int64_t csum_bstride;  // int32 elements
     int64_t flags_bstride; // bytes
     int fault_batch;
+    int a_exact;  // 1: A map is the exact-extent 3D {k, rows, batch} view (one k-block per request)
     // split-K over two units per tile (small-m shapes, one wave): unit u < num_tiles computes k-blocks
     // [kb_half, k_blocks) of tile u and publishes its partial tile; unit num_tiles + t computes
     // [0, kb_half) of tile t, adds the partial and runs the epilogue. split == 1: one unit per tile.

@@ -236,7 +236,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         const int rot = x.nt % x.steps;
         for (int ks0 = 0; ks0 < pre; ++ks0) {
             const int kb = x.kb0 + ((ks0 + rot) % x.steps) * KS;
-            if (role < Cfg::NA)
+            if (role < Cfg::NA && p.a_exact)
+                tma_prefetch_l2_3d(&tmA, (kb + role * (KS / Cfg::NA)) * kBK, x.mt * kPairM + static_cast<int>(rank) * kBM, x.b);
+            else if (role < Cfg::NA)
                 tma_prefetch_l2_4d(&tmA, 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA), x.b);
             else
                 tma_prefetch_l2_4d(&tmB, 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
@@ -285,7 +287,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
-                    if (is_a)
+                    if (is_a && p.a_exact) {
+#pragma unroll
+                        for (int q = 0; q < KA; ++q)  // exact-extent view: one k-block per request
+                            tma_load_3d_pair(st + (grp * KA + q) * Cfg::kABytes, &tmA, &full[s], (kb + grp * KA + q) * kBK,
+                                             x.mt * kPairM + static_cast<int>(rank) * kBM, x.b, pol);
+                    } else if (is_a)
                         tma_load_4d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
                                          x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, x.b, pol);
                     else

@@ -134,6 +134,24 @@ static CUtensorMap make_map_kblocks(const void* base, uint64_t rows, uint64_t kb
     return map;
 }
 
+// 3D exact-extent view {k bytes, rows, batch} of row-major A, box {128 B, 128 rows, 1}: one k-block per
+// request, TMA zero-fills past k (no reads beyond a row's k bytes).
+static CUtensorMap make_map_rows(const void* base, uint64_t k, uint64_t rows, uint64_t lda, uint64_t batch,
+                                 uint64_t bstride) {
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    const uint64_t bb = batch <= 1 ? lda * rows : bstride;
+    const cuuint64_t dims[3] = {k, rows, batch < 1 ? 1 : batch};
+    const cuuint64_t strides[2] = {lda, (bb + 15) / 16 * 16};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(kBM), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled(rows) failed (code " + std::to_string(int(r)) + ")");
+    return map;
+}
+
 // 3D view {columns, rows, batch} of int32 C matrices, 32x32 boxes (TMA-store epilogue).
 static CUtensorMap make_map_c(const void* base, uint64_t n, uint64_t m, uint64_t ldc, uint64_t batch, uint64_t bstride) {
     CUtensorMap map;
@@ -313,11 +331,48 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> g(ws.mu);
 
-    // A is read through a 4D view {128 B, rows, k-blocks, batch}: base and pitch must be 16-byte aligned
-    // and the last (partial) k-block must stay inside the allocation. Otherwise repack into scratch.
+    // Small-m problems (the GEMV class of P:data/shapes.txt): stream B' once on CUDA cores (gemv.cu).
+    const int64_t gemv_rows = std::getenv("ABFTLP_GEMV_MAX_ROWS") ? std::atoll(std::getenv("ABFTLP_GEMV_MAX_ROWS"))
+                                                                  : kGemvMaxRows;
+    const int mr = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : m <= 8 ? 8 : 16;
+    if (nb == 1 && !rq && !force && m <= gemv_rows && m <= 16 && d_c &&
+        mr * w.k_pad + 8 * mr * 32 * 4 <= 160 * 1024 && (w.n + 31) / 32 <= kMaxCheckedNTiles) {
+        if (checked) {
+            grow(ws.row_acc, ws.rows_cap, m, st);
+            grow(ws.err_pack, ws.err_pack_cap, 1, st);
+        }
+        GemmParams p{};
+        p.m = static_cast<int>(m);
+        p.n = static_cast<int>(w.n);
+        p.k = static_cast<int>(w.k);
+        p.k_blocks = static_cast<int>(w.k_pad / kBK);
+        p.batch = 1;
+        p.c = d_c;
+        p.ldc = ldc;
+        p.csum = d_csum;
+        p.csum_ld = csum_ld;
+        p.flags = d_flags;
+        p.err_count = d_err_count;
+        p.a = d_a;
+        p.lda = lda;
+        p.cs = w.cs;
+        p.row_acc = ws.row_acc;
+        p.err_pack = ws.err_pack;
+        if (has_fault) {
+            p.fault_active = 1;
+            p.fault_row = static_cast<int>(fault->row);
+            p.fault_col = static_cast<int>(fault->col);
+            p.fault_bit = static_cast<int>(fault->bit);
+        }
+        cuda_check(launch_gemv(p, w, checked, st), "gemv_checked_kernel");
+        return;
+    }
+    // A is read through a 4D view {128 B, rows, k-blocks, batch} (several k-blocks per request) when k is a
+    // multiple of 128, else through an exact-extent 3D view {k, rows, batch} (one k-block per request, the
+    // tail zero-filled by TMA). Base and pitch must be 16-byte aligned; otherwise repack into scratch.
     const uint8_t* a = d_a;
     int64_t a_ld = lda, a_bstride = bt.a_bstride;
-    if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0 || (w.k % kBK != 0 && lda < w.k_pad)) {
+    if ((lda % 16) != 0 || (reinterpret_cast<uintptr_t>(d_a) % 16) != 0) {
         a_ld = w.k_pad;
         a_bstride = a_ld * m;
         const size_t need = static_cast<size_t>(a_ld * m * nb);
@@ -402,10 +457,15 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         p.fault_col = static_cast<int>(fault->col);
         p.fault_bit = static_cast<int>(fault->bit);
     }
-    // box = a stage's k-blocks split over the A producer warps
-    const CUtensorMap map_a = make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
-                                               static_cast<uint64_t>(a_ld), kBK, kBM, gemm_box_a(t.bn),
-                                               static_cast<uint64_t>(nb), static_cast<uint64_t>(a_bstride));
+    // box = a stage's k-blocks split over the A producer warps (exact-extent view: one k-block)
+    p.a_exact = (w.k % kBK) != 0 ? 1 : 0;
+    const CUtensorMap map_a = p.a_exact
+                                  ? make_map_rows(a, static_cast<uint64_t>(w.k), static_cast<uint64_t>(m),
+                                                  static_cast<uint64_t>(a_ld), static_cast<uint64_t>(nb),
+                                                  static_cast<uint64_t>(a_bstride))
+                                  : make_map_kblocks(a, static_cast<uint64_t>(m), static_cast<uint64_t>(kb),
+                                                     static_cast<uint64_t>(a_ld), kBK, kBM, gemm_box_a(t.bn),
+                                                     static_cast<uint64_t>(nb), static_cast<uint64_t>(a_bstride));
     CUtensorMap map_c;
     std::memset(&map_c, 0, sizeof(map_c));
     if (t.epi == kEpiTmaStore)

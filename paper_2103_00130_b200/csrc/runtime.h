@@ -105,6 +105,8 @@ cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t 
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,
                           uint8_t* flags, uint32_t* err_count, uint32_t* ws_acc, uint32_t* ws_blocks, cudaStream_t st);
 cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked, cudaStream_t st);
+constexpr int64_t kGemvMaxRows = 16;  // m <= this: the small-m (GEMV class) path
+cudaError_t launch_gemv(const GemmParams& p, const GemmWeight& w, bool checked, cudaStream_t st);
 cudaError_t launch_requantize(const int32_t* c, int64_t ldc, int64_t m, int64_t n, const int32_t* rs, const int32_t* cs,
                               const RequantDev& q, uint8_t* out, int64_t ld_out, cudaStream_t st);
 cudaError_t launch_row_sums_u8(const uint8_t* a, int64_t m, int64_t k, int64_t lda, int32_t* out, cudaStream_t st);
