@@ -5,9 +5,10 @@ Headline workload = BASELINE.json configs[1] ("G2"): checked int8 GEMM m=256, k=
 A u8 U[0,255], B s8 U[-128,127] (SplitMix64, the reference's draw protocol), B encoded ONCE and
 reused for a job of 1000 GEMMs with distinct A matrices; 1% of the runs inject one random bit
 flip (half into B' after encoding, half into C' through the epilogue hook) and every injected
-run must be flagged. One step = one such job, replayed as a CUDA graph of the 1000 launches (the
-kernels use programmatic dependent launch, so each GEMM's prologue overlaps the previous one's tail);
-L2 is flushed between steps (a 256 MiB read).
+run must be flagged. The runs are independent problems against one weight, so they are issued as
+GROUPED launches (one problem per run: its own A, C', checksum column, flags and count; the C' faults
+ride in the launch's fault list); a run with a B' fault runs alone between a flip and an unflip of B'.
+One step = one such job, replayed as a CUDA graph; L2 is flushed between steps (a 256 MiB read).
 metric = checked int8 GEMM TOPS (2*m*n*k per GEMM, checksum column excluded).
 
 Secondary lines in the same JSON object: ABFT overhead vs the same kernel with checking compiled
@@ -38,13 +39,14 @@ sys.path.insert(0, str(REPO))
 
 M, N, K = 256, 4096, 4096
 JOB = 1000
+GROUP_MAX = 1000  # runs per grouped launch
 SEED = 20260823
 OPS = 2 * M * N * K
 ALG_BYTES = M * K + K * (N + 1) + 4 * M * (N + 1) + M  # A, B' (incl. checksum column), C', flags
 
 
 def peaks():
-    p = {"hbm_gbs": 6446.6, "bf16_tflops": 1674.8, "source": "fallback (B200_PROFILING.md)"}
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
     f = REPO / "MEASURED_PEAKS.json"
     if f.exists():
         d = json.loads(f.read_text())
@@ -180,8 +182,7 @@ def run_gpu_arm(args, rank, world, dist):
     L.call("abftlp_gemm_encode", vp(b), K, N, N, st, C.byref(w))
     a_pool = torch.empty((JOB, M, K), dtype=torch.uint8, device=dev)
     L.call("abftlp_generate", vp(a_pool), JOB * M * K, SEED, 0, 0, 0, 0.0, 0.0, 0, st)
-    n_cbuf = 8
-    c_ring = torch.empty((n_cbuf, M, N), dtype=torch.int32, device=dev)
+    c_all = torch.empty((JOB, M, N), dtype=torch.int32, device=dev)  # every run keeps its C' (4.3 GB)
     csum = torch.empty((JOB, M), dtype=torch.int32, device=dev)
     flags = torch.empty((JOB, M), dtype=torch.uint8, device=dev)
     errs = torch.zeros(JOB, dtype=torch.int32, device=dev)
@@ -198,27 +199,59 @@ def run_gpu_arm(args, rank, world, dist):
         else:
             plan[run] = ("C", rng.next_below(M), rng.next_below(N + 1), rng.next_below(32))
 
-    def job(checked=True):
-        """Issues the whole job on `st`; returns the number of kernels it launches."""
+    # The job's runs are independent GEMMs against the one encoded weight, so they are issued as GROUPED
+    # launches (abftlp_gemm_checked_batched_faults: problem b = run b, its own A, C', csum, flags and count;
+    # the C' faults of the group ride in the launch's fault list). A run with a B' fault must see the
+    # corrupted weight alone, so it is its own launch between a flip and an unflip of B'.
+    segments = []  # ("group", first, count, [faults]) | ("B", run, p, j, bit)
+    start = 0
+    for run in sorted(r for r, f in plan.items() if f[0] == "B") + [JOB]:
+        i = start
+        while i < run:
+            cnt = min(run - i, GROUP_MAX)
+            fl = [(r - i, plan[r]) for r in range(i, i + cnt) if r in plan and plan[r][0] == "C"]
+            segments.append(("group", i, cnt, fl))
+            i += cnt
+        if run < JOB:
+            segments.append(("B", run) + plan[run][1:])
+        start = run + 1
+    assert all(len(sg[3]) <= 8 for sg in segments if sg[0] == "group")
+
+    def launch_group(i0, cnt, fl, checked):
+        if checked:
+            arr = (L.BatchFault * max(1, len(fl)))()
+            for q, (b_, f) in enumerate(fl):
+                arr[q] = L.BatchFault(1, b_, f[1], f[2], f[3])
+            L.call("abftlp_gemm_checked_batched_faults", vp(a_pool[i0]), cnt, M, K, M * K, w, vp(c_all[i0]), N,
+                   M * N, vp(csum[i0]), 1, M, vp(flags[i0]), M, vp(errs[i0:]), arr, len(fl), st)
+        else:
+            L.call("abftlp_gemm_unchecked_batched", vp(a_pool[i0]), cnt, M, K, M * K, w, vp(c_all[i0]), N, M * N, st)
+
+    def job(checked=True, events=None):
+        """Issues the whole job on `st`; returns the number of kernels it launches. With `events`, the grouped
+        launches are bracketed by CUDA events (the roofline's per-launch durations; not used when timing)."""
         n = 0
-        for i in range(JOB):
-            f = plan.get(i)
-            fault = None
-            if f and f[0] == "B":
-                L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
+        for sg in segments:
+            if sg[0] == "group":
+                _, i0, cnt, fl = sg
+                if events is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                launch_group(i0, cnt, fl, checked)
+                if events is not None:
+                    e1.record(stream)
+                    events.append((cnt, e0, e1))
                 n += 1
-            elif f and f[0] == "C" and checked:
-                fault = C.byref(L.Fault(1, f[1], f[2], f[3]))
-            c = c_ring[i % n_cbuf]
+                continue
+            _, run, pp, jj, bit = sg
+            L.call("abftlp_gemm_weight_flip_bit", w, pp, jj, bit, st)
             if checked:
-                L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c), N, vp(csum[i]), 1, vp(flags[i]),
-                       vp(errs[i:i + 1]), fault, st)
+                L.call("abftlp_gemm_checked", vp(a_pool[run]), M, K, w, vp(c_all[run]), N, vp(csum[run]), 1,
+                       vp(flags[run]), vp(errs[run:run + 1]), None, st)
             else:
-                L.call("abftlp_gemm_unchecked", vp(a_pool[i]), M, K, w, vp(c), N, st)
-            n += 1
-            if f and f[0] == "B":
-                L.call("abftlp_gemm_weight_flip_bit", w, f[1], f[2], f[3], st)
-                n += 1
+                L.call("abftlp_gemm_unchecked", vp(a_pool[run]), M, K, w, vp(c_all[run]), N, st)
+            L.call("abftlp_gemm_weight_flip_bit", w, pp, jj, bit, st)
+            n += 3
         return n
 
     def barrier():
@@ -284,23 +317,54 @@ def run_gpu_arm(args, rank, world, dist):
     # unchecked baseline (same kernel, checking compiled out) for the ABFT overhead
     u_total, _ = timed(graphs[False].replay, args.steps)
 
-    # ---- per-launch duration of the checked kernel (events around each launch, no graph, L2 warm
-    # with B'; distinct A per launch as in the job): the roofline's denominator
+    # ---- the roofline's kernel: the grouped checked launch. Its launches are bracketed by CUDA events on the
+    # job stream in one eager pass of the job (after an L2 flush; events outside the timed region).
+    L.call("abftlp_l2_flush", vp(flush_buf), flush_buf.numel(), 77, st)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(4_000_000)  # ~2 ms: the host enqueues the job before the GPU reaches it
+    ev = []
+    job(True, ev)
+    torch.cuda.synchronize()
+    grp_gemms = sum(c for c, _, _ in ev)
+    grp_ms = sum(a.elapsed_time(b) for _, a, b in ev)
+    kernel_us = grp_ms * 1e3 / len(ev)  # average grouped-launch duration
+    gemms_per_launch = grp_gemms / len(ev)
+
+    # ---- one m=256 GEMM per launch (no grouping): isolated launch latency, and the job as a CUDA graph of
+    # 1000 single launches (programmatic dependent launch between them) -- what grouping is compared with
+    c1 = torch.empty((M, N), dtype=torch.int32, device=dev)
+    cs1 = torch.empty(M, dtype=torch.int32, device=dev)
+    f1 = torch.empty(M, dtype=torch.uint8, device=dev)
+    e1_ = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def single(i, c=None):
+        L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c1 if c is None else c), N, vp(cs1), 1, vp(f1),
+               vp(e1_), None, st)
     per_launch = []
     torch.cuda.synchronize()
-    torch.cuda._sleep(4_000_000)  # ~2 ms: the host enqueues every launch below before the GPU reaches them
+    torch.cuda._sleep(4_000_000)
     for i in range(60):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        L.call("abftlp_gemm_checked", vp(a_pool[i]), M, K, w, vp(c_ring[i % n_cbuf]), N, vp(csum[i]), 1,
-               vp(flags[i]), vp(errs[i:i + 1]), None, st)
+        single(i)
         e1.record(stream)
         per_launch.append((e0, e1))
     torch.cuda.synchronize()
     single_launch_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in per_launch[10:])
-    # the roofline's launch duration: the timed region's device time per checked GEMM launch (the
-    # launches overlap prologue/tail under PDL, so per-launch events would break what they measure)
-    kernel_us = t_total * 1e3 / (args.steps * JOB)
+    # grouped results are bit-identical to single launches (spot check on a clean run)
+    clean_run = next(i for i in range(JOB) if i not in plan)
+    single(clean_run)
+    torch.cuda.synchronize()
+    grouped_eq_single = bool(torch.equal(c1, c_all[clean_run]) and torch.equal(cs1, csum[clean_run]))
+    g1k = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g1k, stream=stream):
+        for i in range(JOB):
+            single(i, c_all[i])
+    torch.cuda.set_stream(stream)
+    g1k.replay()
+    ungrouped_total, _ = timed(g1k.replay, max(1, min(3, args.steps)))
+    ungrouped_tops = world * max(1, min(3, args.steps)) * JOB * OPS / (ungrouped_total * 1e-3) / 1e12
+    del g1k
 
     # ---- cold single GEMM (L2 flushed before each launch), kernel-only
     cold = []
@@ -308,8 +372,7 @@ def run_gpu_arm(args, rank, world, dist):
         L.call("abftlp_l2_flush", vp(flush_buf), flush_buf.numel(), 100 + s, st)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        L.call("abftlp_gemm_checked", vp(a_pool[s]), M, K, w, vp(c_ring[0]), N, vp(csum[0]), 1, vp(flags[0]),
-               vp(errs[0:1]), None, st)
+        single(s)
         e1.record(stream)
         torch.cuda.synchronize()
         cold.append(e0.elapsed_time(e1) * 1e3)
@@ -349,12 +412,14 @@ def run_gpu_arm(args, rank, world, dist):
         return
     value = world * args.steps * JOB * OPS / (t_total * 1e-3) / 1e12
     # DRAM traffic of the checked kernel from the committed ncu --set full capture (profiles/)
+    # DRAM traffic of the grouped checked kernel from the committed ncu --set full capture (profiles/),
+    # recorded per GEMM and scaled to this run's GEMMs per launch
     traffic, traffic_src = None, None
-    caps = sorted(REPO.glob("profiles/r*/ncu_gemm_g2_*.json"))
+    caps = sorted(REPO.glob("profiles/r*/ncu_gemm_g2grouped_*.json"))
     if caps:
         cap = json.loads(caps[-1].read_text())
-        traffic, traffic_src = cap.get("traffic_bytes_per_launch"), str(caps[-1].relative_to(REPO))
-    achieved = OPS / (kernel_us * 1e-6) / 1e12
+        traffic, traffic_src = cap["traffic_bytes_per_gemm"] * gemms_per_launch, str(caps[-1].relative_to(REPO))
+    achieved = grp_gemms * OPS / (grp_ms * 1e-3) / 1e12
     line = {
         "metric": "checked int8 GEMM TOPS", "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -363,7 +428,7 @@ def run_gpu_arm(args, rank, world, dist):
         "config": {"workload": "G2 = BASELINE configs[1]: checked GEMM m=256 k=4096 n=4096, B encoded once, "
                                f"job of {JOB} GEMMs with distinct A, 1% fault runs (B' and C' bit flips)",
                    "step": f"one {JOB}-GEMM job", "l2": "flushed between steps (256 MiB read, untimed); the job's 1 GB of A exceeds L2",
-                   "launch": "CUDA graph of the job's launches, programmatic dependent launch between GEMMs",
+                   "launch": "CUDA graph of the job: grouped launches (runs share the encoded B', one problem per run) split at B'-fault runs, which run alone between a flip and an unflip of B'",
                    "parallelism": f"N-column shard per GPU (n={N} per rank), verdicts OR-reduced",
                    "gemm_kernel": "tcgen05 cta_group::2 int8, TMEM accumulators, fused mod-127 row check"},
         "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": M * K * e2e_runs,
@@ -372,19 +437,23 @@ def run_gpu_arm(args, rank, world, dist):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["int8_tops"], "unit": "TOP/s",
                      "frac": achieved / pk["int8_tops"], "traffic": traffic, "traffic_unit": "bytes/launch",
                      "traffic_source": traffic_src,
-                     "kernel": "gemm_pair_kernel (checked)", "kernel_us": kernel_us,
-                     "kernel_us_how": "timed-region device time / checked GEMM launches (CUDA events, max over ranks)",
-                     "single_launch_us": single_launch_us,
-                     "single_launch_how": "median CUDA-event duration of an isolated checked launch (no PDL overlap; includes launch latency)",
-                     "ops_per_launch": OPS, "alg_bytes_per_launch": ALG_BYTES,
-                     "peak_source": f"2 x bf16 burst from {pk['source']}",
-                     "note": "B' stays L2-resident across the job, so the per-launch bound is tensor, not HBM"},
+                     "kernel": "gemm_pair_kernel<256, checked> (grouped launch)", "kernel_us": kernel_us,
+                     "kernel_us_how": "mean CUDA-event duration of the job's grouped checked launches (job stream, eager pass after an L2 flush)",
+                     "gemms_per_launch": gemms_per_launch, "ops_per_launch": gemms_per_launch * OPS,
+                     "alg_bytes_per_launch": gemms_per_launch * ALG_BYTES,
+                     "peak_source": f"2 x bf16 dense burst from {pk['source']} (int8 dense = 2x bf16 on B200; no driver-measured int8 peak)",
+                     "note": "B' (16.8 MB) stays L2-resident across the job and A/C' stream through HBM at ~1.8 TB/s, so the bound is the tensor pipe"},
+        "per_gemm_launch": {"single_launch_us": single_launch_us,
+                            "single_launch_how": "median CUDA-event duration of an isolated m=256 checked launch",
+                            "ungrouped_job_tops": ungrouped_tops,
+                            "ungrouped_how": "the same 1000 GEMMs as a CUDA graph of 1000 single launches (PDL)"},
         "cold_gemm": {"us_median": statistics.median(cold), "alg_gbs": ALG_BYTES / (statistics.median(cold) * 1e-6) / 1e9,
                       "hbm_frac": ALG_BYTES / (statistics.median(cold) * 1e-6) / 1e9 / pk["hbm_gbs"],
                       "note": "single checked GEMM with L2 flushed (B' from HBM)"},
         "abft_overhead_pct": 100.0 * (t_total - u_total) / u_total,
         "parity": {"clean_runs_unflagged": bool(ok_clean), "c_faults_flagged": bool(ok_c),
-                   "b_faults_flagged": bool(ok_b), "fault_runs": len(plan)},
+                   "b_faults_flagged": bool(ok_b), "fault_runs": len(plan),
+                   "grouped_eq_single_launch": grouped_eq_single},
         "gpu_launches": launches_timed,
         "clocks": clk,
     }

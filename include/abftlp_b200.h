@@ -111,6 +111,14 @@ abftlp_status abftlp_gemm_checked_batched(const uint8_t* d_a, uint64_t batch, ui
                                           uint64_t stride_csum, uint8_t* d_row_flags, uint64_t stride_flags,
                                           uint32_t* d_err_count, const abftlp_batch_fault* fault,
                                           abftlp_stream stream);
+/* Same, with a list of C' faults (entries with active == 0 are skipped; at most 8 active per call): the
+ * form a grouped job uses when several of its runs carry an injected fault. */
+abftlp_status abftlp_gemm_checked_batched_faults(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                                 uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c,
+                                                 uint64_t ldc, uint64_t stride_c, int32_t* d_csum, uint64_t csum_ld,
+                                                 uint64_t stride_csum, uint8_t* d_row_flags, uint64_t stride_flags,
+                                                 uint32_t* d_err_count, const abftlp_batch_fault* faults,
+                                                 uint64_t nfaults, abftlp_stream stream);
 abftlp_status abftlp_gemm_unchecked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
                                             uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c,
                                             uint64_t ldc, uint64_t stride_c, abftlp_stream stream);

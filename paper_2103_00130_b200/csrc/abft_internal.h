@@ -61,6 +61,8 @@ struct RequantDev {
     double sA, bA, sB, bB, sC, bC, k;
 };
 
+constexpr int kMaxGemmFaults = 8;  // C' faults one launch can inject (grouped jobs)
+
 struct GemmParams {
     int m, n, k;       // logical sizes (n excludes the checksum column)
     int k_blocks;      // 128-byte K blocks
@@ -76,7 +78,6 @@ struct GemmParams {
     int64_t c_bstride;     // int32 elements
     int64_t csum_bstride;  // int32 elements
     int64_t flags_bstride; // bytes
-    int fault_batch;
     int a_exact;  // 1: A map is the exact-extent 3D {k, rows, batch} view (one k-block per request)
     // split-K over two units per tile (small-m shapes, one wave): unit u < num_tiles computes k-blocks
     // [kb_half, k_blocks) of tile u and publishes its partial tile; unit num_tiles + t computes
@@ -103,8 +104,10 @@ struct GemmParams {
     uint8_t* rq_out;
     int64_t rq_ld;
     RequantDev rq;
-    // in-epilogue fault hook (P:src/fault_lab.cpp:192-195 semantics): flip `bit` of C'(row, col)
-    int fault_active, fault_row, fault_col, fault_bit;
+    // in-epilogue fault hook (P:src/fault_lab.cpp:192-195 semantics): fault f flips bit fault_bit[f] of
+    // C'(fault_row[f], fault_col[f]) of problem fault_b[f] (col == n: the checksum column), before the check
+    int nfaults;
+    int fault_b[kMaxGemmFaults], fault_row[kMaxGemmFaults], fault_col[kMaxGemmFaults], fault_bit[kMaxGemmFaults];
     unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
 };
 

@@ -431,6 +431,37 @@ abftlp_status abftlp_gemm_checked_batched(const uint8_t* d_a, uint64_t batch, ui
     });
 }
 
+abftlp_status abftlp_gemm_checked_batched_faults(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
+                                                 uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c,
+                                                 uint64_t ldc, uint64_t stride_c, int32_t* d_csum, uint64_t csum_ld,
+                                                 uint64_t stride_csum, uint8_t* d_row_flags, uint64_t stride_flags,
+                                                 uint32_t* d_err_count, const abftlp_batch_fault* faults,
+                                                 uint64_t nfaults, abftlp_stream stream) {
+    if (!w || (nfaults && !faults)) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::BatchFault fl[abftk::kMaxGemmFaults];
+        int64_t nf = 0;
+        for (uint64_t i = 0; i < nfaults; ++i) {
+            if (!faults[i].active) continue;
+            if (nf == abftk::kMaxGemmFaults) throw std::invalid_argument("abft_gemm: too many faults for one call");
+            fl[nf++] = abftk::BatchFault{static_cast<int64_t>(faults[i].batch), static_cast<int64_t>(faults[i].row),
+                                         static_cast<int64_t>(faults[i].col), faults[i].bit};
+        }
+        abftk::GemmBatch bt;
+        bt.batch = static_cast<int64_t>(batch);
+        bt.a_bstride = static_cast<int64_t>(stride_a);
+        bt.c_bstride = static_cast<int64_t>(stride_c);
+        bt.csum_bstride = static_cast<int64_t>(stride_csum);
+        bt.flags_bstride = static_cast<int64_t>(stride_flags);
+        bt.faults = fl;
+        bt.nfaults = nf;
+        abftk::gemm(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                    true, d_csum, static_cast<int64_t>(csum_ld), d_row_flags, d_err_count, nullptr, as_stream(stream),
+                    nullptr, nullptr, &bt);
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_gemm_unchecked_batched(const uint8_t* d_a, uint64_t batch, uint64_t m, uint64_t lda,
                                             uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* d_c, uint64_t ldc,
                                             uint64_t stride_c, abftlp_stream stream) {

@@ -418,8 +418,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 if (trace && threadIdx.x == 64) trace[13] = globaltimer();
                 spart = reinterpret_cast<const uint4*>(smem);
             }
-            const bool fault_problem = p.fault_active && x.b == p.fault_batch;
-            const bool fault_here = fault_problem && row == p.fault_row && p.fault_col < p.n;
+            bool fault_here = false;  // some injected fault hits a data column of this row
+            for (int f = 0; f < p.nfaults; ++f)
+                fault_here |= x.b == p.fault_b[f] && row == p.fault_row[f] && p.fault_col[f] < p.n;
             int32_t* const cb = p.c + x.b * p.c_bstride;  // this problem's C
             long long rsum = 0;
 #pragma unroll 1
@@ -440,9 +441,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     }
                 }
                 if (fault_here) {
+                    for (int f = 0; f < p.nfaults; ++f) {
+                        if (x.b != p.fault_b[f] || row != p.fault_row[f]) continue;
+                        const int fc = p.fault_col[f];
+                        const uint32_t fm = 1u << p.fault_bit[f];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (p.fault_col == col0 + j) v[j] ^= 1u << p.fault_bit;
+                        for (int j = 0; j < 32; ++j)
+                            if (fc == col0 + j) v[j] ^= fm;
+                    }
                 }
                 if (p.rq_out != nullptr && row < p.m) {
                     // fused requantization of this row's 32 columns (the checksum column is never part
@@ -559,8 +565,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.n_tiles)) {
                         fin = 1;
                         int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
-                        if (fault_problem && row == p.fault_row && p.fault_col == p.n)
-                            csv ^= static_cast<int32_t>(1u << p.fault_bit);  // fault in C'[:, n]
+                        for (int f = 0; f < p.nfaults; ++f)
+                            if (x.b == p.fault_b[f] && row == p.fault_row[f] && p.fault_col[f] == p.n)
+                                csv ^= static_cast<int32_t>(1u << p.fault_bit[f]);  // fault in C'[:, n]
                         const uint32_t res = static_cast<uint32_t>(v & kRowAccResMask) % 127u;
                         flag = static_cast<int32_t>(res) != mod127(csv);
                         p.flags[x.b * p.flags_bstride + row] = static_cast<uint8_t>(flag);

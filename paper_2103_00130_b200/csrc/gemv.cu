@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(32 * kGemvWarps) gemv_checked_kernel(const Gem
     for (int i = warp; i < MR && i < p.m; i += kGemvWarps) {
         uint32_t v = 0u;
         for (int r = 0; r < ks; ++r) v += static_cast<uint32_t>(xin[(r * MR + i) * 32 + lane]);
-        if (p.fault_active && i == p.fault_row && p.fault_col == j && j < p.n) v ^= 1u << p.fault_bit;
+        for (int f = 0; f < p.nfaults; ++f)
+            if (i == p.fault_row[f] && p.fault_col[f] == j && j < p.n) v ^= 1u << p.fault_bit[f];
         if (j < p.n && p.c) p.c[static_cast<int64_t>(i) * p.ldc + j] = static_cast<int32_t>(v);
         if constexpr (CHECKED) {
             long long rs = j < p.n ? static_cast<int32_t>(v) : 0;
@@ -137,8 +138,9 @@ __global__ void __launch_bounds__(32 * kGemvWarps) gemv_checked_kernel(const Gem
                 const unsigned long long acc64 = atomicAdd(&p.row_acc[i], add) + add;
                 if (((acc64 >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(ncg)) {
                     int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(acc64 >> 32));
-                    if (p.fault_active && i == p.fault_row && p.fault_col == p.n)
-                        csv ^= static_cast<int32_t>(1u << p.fault_bit);  // fault in C'[:, n]
+                    for (int f = 0; f < p.nfaults; ++f)
+                        if (i == p.fault_row[f] && p.fault_col[f] == p.n)
+                            csv ^= static_cast<int32_t>(1u << p.fault_bit[f]);  // fault in C'[:, n]
                     const uint32_t res = static_cast<uint32_t>(acc64 & kRowAccResMask) % 127u;
                     const int flag = static_cast<int32_t>(res) != mod127(csv);
                     p.flags[i] = static_cast<uint8_t>(flag);

@@ -317,13 +317,29 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (ldc < w.n) throw std::invalid_argument("abft_gemm: ldc < n");
     if (checked && (!d_err_count || (m > 0 && (!d_csum || !d_flags)))) throw std::invalid_argument("null argument");
     if (m > (int64_t{1} << 31) - 1 || w.n > (int64_t{1} << 31) - 2) throw std::invalid_argument("abft_gemm: too large");
-    const bool has_fault = fault && fault->active;
-    if (has_fault) {
-        if (!checked) throw std::invalid_argument("abft_gemm: fault hook needs the checked kernel");
-        if (fault->row < 0 || fault->row >= m || fault->col < 0 || fault->col > w.n || fault->bit > 31 ||
-            bt.fault_batch < 0 || bt.fault_batch >= nb)
+    // the call's C' faults: the single-fault form plus the batched list
+    BatchFault fl[kMaxGemmFaults];
+    int nf = 0;
+    if (bt.nfaults < 0 || (bt.nfaults > 0 && !bt.faults)) throw std::invalid_argument("abft_gemm: bad fault list");
+    if ((fault && fault->active ? 1 : 0) + bt.nfaults > kMaxGemmFaults)
+        throw std::invalid_argument("abft_gemm: too many faults for one call");
+    if (fault && fault->active) fl[nf++] = BatchFault{bt.fault_batch, fault->row, fault->col, fault->bit};
+    for (int64_t i = 0; i < bt.nfaults; ++i) fl[nf++] = bt.faults[i];
+    const bool has_fault = nf > 0;
+    if (has_fault && !checked) throw std::invalid_argument("abft_gemm: fault hook needs the checked kernel");
+    for (int i = 0; i < nf; ++i)
+        if (fl[i].row < 0 || fl[i].row >= m || fl[i].col < 0 || fl[i].col > w.n || fl[i].bit > 31 || fl[i].batch < 0 ||
+            fl[i].batch >= nb)
             throw std::out_of_range("abft_gemm: fault coordinates out of range");
-    }
+    auto set_faults = [&](GemmParams& p) {
+        p.nfaults = nf;
+        for (int i = 0; i < nf; ++i) {
+            p.fault_b[i] = static_cast<int>(fl[i].batch);
+            p.fault_row[i] = static_cast<int>(fl[i].row);
+            p.fault_col[i] = static_cast<int>(fl[i].col);
+            p.fault_bit[i] = static_cast<int>(fl[i].bit);
+        }
+    };
     if (m == 0) {
         if (checked) cuda_check(cudaMemsetAsync(d_err_count, 0, sizeof(uint32_t) * nb, st), "cudaMemsetAsync");
         return;
@@ -358,12 +374,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         p.cs = w.cs;
         p.row_acc = ws.row_acc;
         p.err_pack = ws.err_pack;
-        if (has_fault) {
-            p.fault_active = 1;
-            p.fault_row = static_cast<int>(fault->row);
-            p.fault_col = static_cast<int>(fault->col);
-            p.fault_bit = static_cast<int>(fault->bit);
-        }
+        set_faults(p);
         cuda_check(launch_gemv(p, w, checked, st), "gemv_checked_kernel");
         return;
     }
@@ -450,13 +461,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         p.rq_ld = rq->ld_out;
         p.rq = rq->params;
     }
-    if (has_fault) {
-        p.fault_active = 1;
-        p.fault_batch = static_cast<int>(bt.fault_batch);
-        p.fault_row = static_cast<int>(fault->row);
-        p.fault_col = static_cast<int>(fault->col);
-        p.fault_bit = static_cast<int>(fault->bit);
-    }
+    set_faults(p);
     // box = a stage's k-blocks split over the A producer warps (exact-extent view: one k-block)
     p.a_exact = (w.k % kBK) != 0 ? 1 : 0;
     const CUtensorMap map_a = p.a_exact

@@ -14,6 +14,11 @@ struct Fault {
     int64_t row = 0, col = 0;
     uint32_t bit = 0;
 };
+// A C' fault of one problem of a batched call (grouped jobs carry several per launch).
+struct BatchFault {
+    int64_t batch = 0, row = 0, col = 0;
+    uint32_t bit = 0;
+};
 
 // ---- GEMM (replaces P:src/gemm_abft.hpp:23-74)
 // batch > 1: `batch` independent weights, weight b at d_b + b * b_bstride (batched GEMM).
@@ -46,7 +51,9 @@ struct GemmBatch {
     int64_t c_bstride = 0;     // int32 elements
     int64_t csum_bstride = 0;  // int32 elements
     int64_t flags_bstride = 0; // bytes
-    int64_t fault_batch = 0;
+    int64_t fault_batch = 0;            // problem of `fault` (single-fault form)
+    const BatchFault* faults = nullptr;  // further C' faults; at most kMaxGemmFaults per call in total
+    int64_t nfaults = 0;
 };
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,

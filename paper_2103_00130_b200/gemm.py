@@ -201,12 +201,16 @@ class PackedEncodedWeightBatch:
         return self._n
 
 
-def abft_gemm_batched(a, pb: PackedEncodedWeightBatch, fault: tuple[int, int, int, int] | None = None, stream=None):
-    """`batch` checked GEMMs in one launch: a is [batch, m, k] u8. Returns (cTemp [batch, m, n+1] int32 with
-    the checksum column last, errCount [batch] int32, rowFlags [batch, m] u8) as device tensors.
-    ``fault=(problem, row, col, bit)`` flips one bit of that problem's C' in the epilogue."""
+def abft_gemm_batched(a, pb, fault: tuple[int, int, int, int] | None = None, stream=None,
+                      faults: list[tuple[int, int, int, int]] | None = None):
+    """`batch` checked GEMMs in one launch: a is [batch, m, k] u8; ``pb`` is a PackedEncodedWeightBatch (one
+    weight per problem) or a single PackedEncodedWeight shared by every problem (a grouped job). Returns
+    (cTemp [batch, m, n+1] int32 with the checksum column last, errCount [batch] int32, rowFlags [batch, m]
+    u8) as device tensors. ``fault=(problem, row, col, bit)`` flips one bit of that problem's C' in the
+    epilogue; ``faults`` is a list of such tuples (at most 8 per call)."""
     at = to_device(a, torch.uint8)
-    if at.dim() != 3 or int(at.shape[0]) != pb.batch() or int(at.shape[2]) != pb.k():
+    nb_w = pb.batch() if isinstance(pb, PackedEncodedWeightBatch) else None
+    if at.dim() != 3 or (nb_w is not None and int(at.shape[0]) != nb_w) or int(at.shape[2]) != pb.k():
         raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "abft_gemm: dimension mismatch")
     nb, m, k = (int(s) for s in at.shape)
     n = pb.n()
@@ -214,8 +218,12 @@ def abft_gemm_batched(a, pb: PackedEncodedWeightBatch, fault: tuple[int, int, in
     ctemp = torch.zeros((nb, m, n + 1), dtype=torch.int32, device=dev)
     flags = torch.zeros((nb, m), dtype=torch.uint8, device=dev)
     err = torch.zeros(nb, dtype=torch.int32, device=dev)
-    f = C.byref(_lib.BatchFault(1, *fault)) if fault is not None else None
-    _lib.call("abftlp_gemm_checked_batched", ptr(at), nb, m, k, m * k, pb.handle, ptr(ctemp), n + 1, m * (n + 1),
-              C.c_void_p(ctemp.data_ptr() + 4 * n), n + 1, m * (n + 1), ptr(flags), m, ptr(err), f,
-              stream_handle(stream))
+    args = (ptr(at), nb, m, k, m * k, pb.handle, ptr(ctemp), n + 1, m * (n + 1),
+            C.c_void_p(ctemp.data_ptr() + 4 * n), n + 1, m * (n + 1), ptr(flags), m, ptr(err))
+    if faults is not None:
+        arr = (_lib.BatchFault * max(1, len(faults)))(*[_lib.BatchFault(1, *f) for f in faults])
+        _lib.call("abftlp_gemm_checked_batched_faults", *args, arr, len(faults), stream_handle(stream))
+    else:
+        f = C.byref(_lib.BatchFault(1, *fault)) if fault is not None else None
+        _lib.call("abftlp_gemm_checked_batched", *args, f, stream_handle(stream))
     return ctemp, err, flags

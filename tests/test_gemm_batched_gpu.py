@@ -47,3 +47,39 @@ def test_g1_trials_protocol_sum():
         _, e, _ = G.abft_gemm_batched(a, pb, fault=(t, i, j, bit))
         detected += int(e[t].item())
     assert detected == 50
+
+
+@pytest.mark.parametrize("nb,m,n,k", [(12, 256, 1024, 1024), (5, 200, 520, 384)])
+def test_grouped_shared_weight_with_fault_list(nb, m, n, k):
+    """Grouped job form (BASELINE config 1's 1000 runs against one encoded B): every problem shares ONE
+    PackedEncodedWeight, several C' faults (data and checksum columns, different problems, two in one
+    problem) ride in one launch's fault list; per problem, C' equals the oracle with the same bits flipped
+    post hoc and the counts equal the reference's verify on it."""
+    from paper_2103_00130_b200 import gemm as G
+    a = np.stack([O.gemm_inputs(20260823, t, m, n, k)[0] for t in range(nb)])
+    b = O.gemm_inputs(20260823, 0, m, n, k)[1]
+    pb = G.PackedEncodedWeight(b)
+    faults = [(1, 3, n, 7), (4, m - 1, n // 3, 31), (4, 0, 0, 0), (nb - 1, m // 2, n - 1, 12)]
+    ct, err, flags = G.abft_gemm_batched(a, pb, faults=faults)
+    ct, err, flags = ct.cpu().numpy(), err.cpu().numpy(), flags.cpu().numpy()
+    for t in range(nb):
+        ref, _, _ = O.abft_gemm(a[t], b)
+        ref = ref.copy()
+        for (p_, i, j, bit) in faults:
+            if p_ == t:
+                ref[i, j] = np.int32(np.uint32(ref[i, j].view(np.uint32) ^ np.uint32(1 << bit)).view(np.int32))
+        assert np.array_equal(ct[t], ref), t
+        e_ref, fl_ref = O.verify(ref)  # the reference's verify_checksums on the post-hoc faulted C'
+        assert err[t] == e_ref == len({i for (p_, i, _, _) in faults if p_ == t}), t
+        assert np.array_equal(flags[t], fl_ref), t
+
+
+def test_grouped_fault_list_limits():
+    from paper_2103_00130_b200 import _lib
+    from paper_2103_00130_b200 import gemm as G
+    a = np.zeros((2, 8, 128), np.uint8)
+    pb = G.PackedEncodedWeight(np.ones((128, 64), np.int8))
+    with pytest.raises(_lib.InvalidArgument):
+        G.abft_gemm_batched(a, pb, faults=[(0, 0, 0, 0)] * 9)
+    with pytest.raises(_lib.InvalidArgument):  # out_of_range -> ABFTLP_ERR_INVALID_ARGUMENT
+        G.abft_gemm_batched(a, pb, faults=[(2, 0, 0, 0)])
