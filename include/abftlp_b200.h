@@ -86,6 +86,18 @@ abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t ld
                                        int32_t* csum, uint8_t* row_flags, uint32_t* err_count,
                                        abftlp_stream stream);
 
+/* Host-buffer job (the "e2e" path of a grouped job): `batch` checked GEMMs against one encoded weight, A_b at
+ * a + b*stride_a (bytes, row pitch lda), C_b at c + b*stride_c (int32 elements, row pitch ldc), csum_b at
+ * csum + b*stride_csum (m int32), flags_b at row_flags + b*stride_flags, err_count[b]. Internally pipelined:
+ * chunks of runs are copied in on one stream, multiplied as grouped launches on `stream` and copied out on a
+ * third, so host->device, compute and device->host overlap (pinned host buffers make the copies
+ * asynchronous). Synchronous on return. Results are identical to abftlp_gemm_checked per run. */
+abftlp_status abftlp_gemm_checked_host_batched(const uint8_t* a, uint64_t batch, uint64_t m, uint64_t lda,
+                                               uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* c,
+                                               uint64_t ldc, uint64_t stride_c, int32_t* csum,
+                                               uint64_t stride_csum, uint8_t* row_flags, uint64_t stride_flags,
+                                               uint32_t* err_count, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ batched GEMM (many small problems) */
 /* Encode `batch` independent weights of one shape: weight b is B_b = d_b + b*stride_b (k x n, ld ldb).
  * The batched handle serves abftlp_gemm_*_batched; per-weight accessors (checksums, read, flip, col sums)

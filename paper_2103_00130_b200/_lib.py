@@ -117,6 +117,7 @@ _SIGS = {
     "abftlp_eb_unchecked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp]),
     "abftlp_gemm_encode_batched": (i32, [vp, u64, u64, u64, u64, u64, vp, vp]),
     "abftlp_gemm_checked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, vp]),
+    "abftlp_gemm_checked_host_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, vp, u64, vp, vp]),
     "abftlp_gemm_checked_batched_faults": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, u64, vp]),
     "abftlp_gemm_unchecked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp]),
     "abftlp_gemm_checked_requant": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),

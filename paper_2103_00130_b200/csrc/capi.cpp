@@ -86,6 +86,19 @@ struct HostStage {
     uint8_t* flags = nullptr;
     size_t flags_cap = 0;
     uint32_t* err = nullptr;
+    // pipelined host job (abftlp_gemm_checked_host_batched): copy-in / copy-out streams and per-slot events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t a_ready[3] = {}, c_done[3] = {}, out_done[3] = {};
+    uint8_t* ja = nullptr;
+    size_t ja_cap = 0;
+    int32_t* jc = nullptr;
+    size_t jc_cap = 0;
+    int32_t* jcs = nullptr;
+    size_t jcs_cap = 0;
+    uint8_t* jfl = nullptr;
+    size_t jfl_cap = 0;
+    uint32_t* jerr = nullptr;
+    size_t jerr_cap = 0;
 };
 std::mutex g_stage_mu;
 std::unordered_map<uint64_t, HostStage> g_stage;
@@ -525,6 +538,108 @@ abftlp_status abftlp_gemm_checked_host(const uint8_t* a, uint64_t m, uint64_t ld
         if (csum) ABFT_CUDA(cudaMemcpyAsync(csum, s.csum, m * 4, cudaMemcpyDeviceToHost, st));
         if (row_flags) ABFT_CUDA(cudaMemcpyAsync(row_flags, s.flags, m, cudaMemcpyDeviceToHost, st));
         if (err_count) ABFT_CUDA(cudaMemcpyAsync(err_count, s.err, 4, cudaMemcpyDeviceToHost, st));
+        ABFT_CUDA(cudaStreamSynchronize(st));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_checked_host_batched(const uint8_t* a, uint64_t batch, uint64_t m, uint64_t lda,
+                                               uint64_t stride_a, const abftlp_gemm_weight* w, int32_t* c,
+                                               uint64_t ldc, uint64_t stride_c, int32_t* csum,
+                                               uint64_t stride_csum, uint8_t* row_flags, uint64_t stride_flags,
+                                               uint32_t* err_count, abftlp_stream stream) {
+    if (!w || (batch && m && (!a || !c || !csum || !row_flags || !err_count)))
+        return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::GemmWeight& W = *w->w;
+        if (W.batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
+        const size_t n = static_cast<size_t>(W.n), k = static_cast<size_t>(W.k);
+        if (lda < k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
+        if (ldc < n) throw std::invalid_argument("abft_gemm: ldc < n");
+        if (batch > 1 && (stride_a < lda * (m - 1) + k || stride_c < ldc * m || stride_csum < m || stride_flags < m))
+            throw std::invalid_argument("abft_gemm: batch strides overlap");
+        if (batch == 0 || m == 0) {
+            for (uint64_t b = 0; b < batch; ++b) err_count[b] = 0;
+            return ABFTLP_OK;
+        }
+        cudaStream_t st = as_stream(stream);
+        int dev = 0;
+        ABFT_CUDA(cudaGetDevice(&dev));
+        const uint64_t key = (reinterpret_cast<uint64_t>(st) << 8) ^ static_cast<uint64_t>(dev);
+        std::lock_guard<std::mutex> g(g_stage_mu);
+        HostStage& s = g_stage[key];
+        if (!s.h2d) {
+            ABFT_CUDA(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+            ABFT_CUDA(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
+            for (int i = 0; i < 3; ++i) {
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.a_ready[i], cudaEventDisableTiming));
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.c_done[i], cudaEventDisableTiming));
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.out_done[i], cudaEventDisableTiming));
+            }
+        }
+        // chunk = runs per grouped launch: ~32 MB of C' per chunk, three slots in flight
+        const size_t dlda = (k + 15) / 16 * 16, dldc = (n + 3) / 4 * 4;
+        const size_t per_c = m * dldc * 4;
+        const uint64_t q = std::max<uint64_t>(1, std::min<uint64_t>(batch, (32u << 20) / std::max<size_t>(per_c, 1)));
+        ensure(s.ja, s.ja_cap, 3 * q * m * dlda);
+        ensure(s.jc, s.jc_cap, 3 * q * m * dldc);
+        ensure(s.jcs, s.jcs_cap, 3 * q * m);
+        ensure(s.jfl, s.jfl_cap, 3 * q * m);
+        ensure(s.jerr, s.jerr_cap, 3 * q);
+        // the caller's stream may have pending work the job depends on (e.g. the weight encode)
+        ABFT_CUDA(cudaEventRecord(s.c_done[0], st));
+        ABFT_CUDA(cudaStreamWaitEvent(s.h2d, s.c_done[0], 0));
+        const uint64_t chunks = (batch + q - 1) / q;
+        for (uint64_t i = 0; i < chunks; ++i) {
+            const int sl = static_cast<int>(i % 3);
+            const uint64_t b0 = i * q, nb = std::min<uint64_t>(q, batch - b0);
+            uint8_t* da = s.ja + sl * q * m * dlda;
+            int32_t* dc = s.jc + sl * q * m * dldc;
+            int32_t* dcs = s.jcs + sl * q * m;
+            uint8_t* dfl = s.jfl + sl * q * m;
+            uint32_t* derr = s.jerr + sl * q;
+            if (i >= 3) ABFT_CUDA(cudaStreamWaitEvent(s.h2d, s.c_done[sl], 0));  // slot's A no longer read
+            for (uint64_t b = 0; b < nb; ++b)
+                ABFT_CUDA(cudaMemcpy2DAsync(da + b * m * dlda, dlda, a + (b0 + b) * stride_a, lda, k, m,
+                                            cudaMemcpyHostToDevice, s.h2d));
+            ABFT_CUDA(cudaEventRecord(s.a_ready[sl], s.h2d));
+            ABFT_CUDA(cudaStreamWaitEvent(st, s.a_ready[sl], 0));
+            if (i >= 3) ABFT_CUDA(cudaStreamWaitEvent(st, s.out_done[sl], 0));  // slot's C' copied out
+            abftk::GemmBatch bt;
+            bt.batch = static_cast<int64_t>(nb);
+            bt.a_bstride = static_cast<int64_t>(m * dlda);
+            bt.c_bstride = static_cast<int64_t>(m * dldc);
+            bt.csum_bstride = static_cast<int64_t>(m);
+            bt.flags_bstride = static_cast<int64_t>(m);
+            abftk::gemm(da, static_cast<int64_t>(m), static_cast<int64_t>(dlda), W, dc, static_cast<int64_t>(dldc),
+                        true, dcs, 1, dfl, derr, nullptr, st, nullptr, nullptr, nb > 1 ? &bt : nullptr);
+            ABFT_CUDA(cudaEventRecord(s.c_done[sl], st));
+            ABFT_CUDA(cudaStreamWaitEvent(s.d2h, s.c_done[sl], 0));
+            if (stride_c == ldc * m && ldc == dldc) {
+                ABFT_CUDA(cudaMemcpyAsync(c + b0 * stride_c, dc, nb * m * dldc * 4, cudaMemcpyDeviceToHost, s.d2h));
+            } else if (stride_c == ldc * m) {
+                ABFT_CUDA(cudaMemcpy2DAsync(c + b0 * stride_c, ldc * 4, dc, dldc * 4, n * 4, nb * m,
+                                            cudaMemcpyDeviceToHost, s.d2h));
+            } else {
+                for (uint64_t b = 0; b < nb; ++b)
+                    ABFT_CUDA(cudaMemcpy2DAsync(c + (b0 + b) * stride_c, ldc * 4, dc + b * m * dldc, dldc * 4, n * 4, m,
+                                                cudaMemcpyDeviceToHost, s.d2h));
+            }
+            if (stride_csum == m && stride_flags == m) {
+                ABFT_CUDA(cudaMemcpyAsync(csum + b0 * m, dcs, nb * m * 4, cudaMemcpyDeviceToHost, s.d2h));
+                ABFT_CUDA(cudaMemcpyAsync(row_flags + b0 * m, dfl, nb * m, cudaMemcpyDeviceToHost, s.d2h));
+            } else {
+                for (uint64_t b = 0; b < nb; ++b) {
+                    ABFT_CUDA(cudaMemcpyAsync(csum + (b0 + b) * stride_csum, dcs + b * m, m * 4, cudaMemcpyDeviceToHost,
+                                              s.d2h));
+                    ABFT_CUDA(cudaMemcpyAsync(row_flags + (b0 + b) * stride_flags, dfl + b * m, m,
+                                              cudaMemcpyDeviceToHost, s.d2h));
+                }
+            }
+            ABFT_CUDA(cudaMemcpyAsync(err_count + b0, derr, nb * 4, cudaMemcpyDeviceToHost, s.d2h));
+            ABFT_CUDA(cudaEventRecord(s.out_done[sl], s.d2h));
+        }
+        ABFT_CUDA(cudaStreamSynchronize(s.d2h));
         ABFT_CUDA(cudaStreamSynchronize(st));
         return ABFTLP_OK;
     });

@@ -123,6 +123,21 @@ __device__ __forceinline__ double csum_term(float s, float b, int32_t rs, float 
 
 }  // namespace
 
+// Block completion without fences: one 64-bit atomic per block on the per-stream word {flags (low 32),
+// finished blocks (high 32)} (ws_flag_acc / ws_block_cnt, adjacent and 8-byte aligned). Atomics on one
+// address are totally ordered, so the block whose add brings the count to gridDim.x sees every other
+// block's flags in the returned value; it publishes the call's flag count and resets the per-stream words
+// (the bag counter's last use by any block returned its value before that block arrived here).
+__device__ __forceinline__ void eb_block_done(const EbParams& p, uint32_t blk_flags, bool reset_bag_ctr) {
+    unsigned long long* pack = reinterpret_cast<unsigned long long*>(p.ws_flag_acc);
+    const unsigned long long prev = atomicAdd(pack, (1ull << 32) | blk_flags);
+    if ((prev >> 32) == gridDim.x - 1) {
+        if (p.flag_count) *p.flag_count = static_cast<uint32_t>(prev) + blk_flags;
+        *pack = 0ull;
+        if (reset_bag_ctr) *p.ws_bag_ctr = 0ull;
+    }
+}
+
 constexpr int kGenericSlots = 8;
 constexpr int kChunk = 32;  // lookups gathered per round
 
@@ -142,7 +157,6 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
     __shared__ double part_sum[8];
     __shared__ int part_emax[8], part_umin[8];
     __shared__ uint32_t blk_flags;
-    __shared__ uint32_t is_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bag_local = warp / WPB, slice = warp % WPB;
@@ -296,17 +310,7 @@ __global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int lo
         }
         if (p.flag_count) {
             __syncthreads();
-            if (threadIdx.x == 0) {
-                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
-                __threadfence();
-                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
-            }
-            __syncthreads();
-            if (is_last && threadIdx.x == 0) {
-                __threadfence();
-                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
-                atomicExch(p.ws_block_cnt, 0u);
-            }
+            if (threadIdx.x == 0) eb_block_done(p, blk_flags, false);
         }
     }
 }
@@ -356,7 +360,7 @@ struct AsyncStage {
     uint4 meta[NST][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B); zero = neutral slot
     float w[NST][kChunk];
     int64_t off[kChunk];                  // row byte offsets of the chunk being issued, -1 = none
-    double term[kChunk];                  // cSum terms of the chunk, summed in order by lane 0
+    double term[kChunk];                  // cSum terms of the chunk being consumed
 };
 
 template <int SCALE>
@@ -449,14 +453,15 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
     __shared__ int part_emax[8], part_umin[8];
     __shared__ long long grp_bag[GROUPS];
     __shared__ uint32_t blk_flags;
-    __shared__ uint32_t is_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = warp / WPB, slice = warp % WPB;
     const int64_t slice_byte = static_cast<int64_t>(slice) * SLICE;
     const double dd = static_cast<double>(p.dim);
     if (threadIdx.x == 0) blk_flags = 0;
+    griddep_launch_dependents();  // the next kernel on the stream may start its prologue
     __syncthreads();
+    griddep_wait();  // inputs and the per-stream words are those the preceding grid left
     auto group_sync = [&]() {
         if constexpr (WPB > 1)
             named_bar_sync(1 + grp, 32 * WPB);
@@ -566,12 +571,13 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
             const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
             const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
             if constexpr (CHECKED) {
-                if (slice == 0) {  // neutral slots give an exact 0.0 term
+                if (slice == 0) {  // the chunk's cSum terms, lane-parallel (a neutral slot's term is +0.0)
                     float s, b;
                     int32_t rs;
                     smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
                     S.term[lane] = csum_term(s, b, rs, WEIGHTED ? S.w[sl][lane] : 1.0f, dd, WEIGHTED);
                 }
+                __syncwarp();
             }
             const int tmax = (cnt + 3) & ~3;  // slots cnt..tmax-1 are neutral
 #pragma unroll 4
@@ -580,6 +586,12 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
                 int32_t rs;
                 smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
                 const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
+                // cSum in the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), kept by every
+                // lane of the slice-0 warp (same terms, same order, same value) inside the lookup loop, so the
+                // dependent DADD chain overlaps the column arithmetic. A neutral slot's +0.0 term is an exact
+                // no-op (cSum starts at +0.0 and never becomes -0.0 in round-to-nearest).
+                if constexpr (CHECKED)
+                    if (slice == 0) csum = __dadd_rn(csum, S.term[t]);
                 const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
                 if constexpr (CPL >= 2) {
                     const unsigned long long s2 = f2_pack(s, s), b2 = f2_pack(b, b);
@@ -598,14 +610,6 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
                         if constexpr (WEIGHTED) x = __fmul_rn(w, x);
                         acc[c] = __fadd_rn(acc[c], x);
                     }
-                }
-            }
-            if constexpr (CHECKED) {
-                // the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), one lane
-                __syncwarp();
-                if (slice == 0 && lane == 0) {
-#pragma unroll 8
-                    for (int t = 0; t < cnt; ++t) csum = __dadd_rn(csum, S.term[t]);
                 }
             }
             __syncwarp();  // slot `sl` may be refilled by a later issue
@@ -685,19 +689,7 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
     }
     // last block out publishes the flag count and resets the per-stream counters
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (CHECKED && blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
-        __threadfence();
-        is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (is_last && threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t total = atomicExch(p.ws_flag_acc, 0u);
-        if (CHECKED && p.flag_count) *p.flag_count = total;
-        atomicExch(p.ws_block_cnt, 0u);
-        atomicExch(p.ws_bag_ctr, 0ull);
-    }
+    if (threadIdx.x == 0) eb_block_done(p, CHECKED ? blk_flags : 0u, true);
 }
 
 // Generic path (any d <= 256, unaligned rows): warp per bag, lane owns columns lane + 32*c, byte loads.
@@ -708,7 +700,6 @@ __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, i
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bag = static_cast<int64_t>(blockIdx.x) * 8 + warp;
     __shared__ uint32_t blk_flags;
-    __shared__ uint32_t is_last;
     if (threadIdx.x == 0) blk_flags = 0;
     __syncthreads();
     if (bag < p.num_bags) {
@@ -818,17 +809,7 @@ __global__ void __launch_bounds__(256) eb_bag_generic_kernel(const EbParams p, i
     if constexpr (CHECKED) {
         if (p.flag_count) {
             __syncthreads();
-            if (threadIdx.x == 0) {
-                if (blk_flags) atomicAdd(p.ws_flag_acc, blk_flags);
-                __threadfence();
-                is_last = atomicAdd(p.ws_block_cnt, 1u) == gridDim.x - 1;
-            }
-            __syncthreads();
-            if (is_last && threadIdx.x == 0) {
-                __threadfence();
-                *p.flag_count = atomicExch(p.ws_flag_acc, 0u);
-                atomicExch(p.ws_block_cnt, 0u);
-            }
+            if (threadIdx.x == 0) eb_block_done(p, blk_flags, false);
         }
     }
 }
@@ -922,8 +903,19 @@ static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t s
     const int64_t need = (p.num_bags + (8 / WPB) - 1) / (8 / WPB);
     const int64_t cap = static_cast<int64_t>(per_sm) * device_sm_count();
     const unsigned blocks = static_cast<unsigned>(need < cap ? need : cap);
-    kern<<<blocks, 256, smem, st>>>(p, log2d);
-    return cudaGetLastError();
+    // programmatic dependent launch: consecutive batches overlap launch and prologue with the tail
+    static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, p, log2d);
 }
 
 template <int ELEM, int SCALE, int CPL, int WPB>

@@ -14,6 +14,15 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "E3"
 checked = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 dev = torch.device("cuda")
+torch.cuda.init()
+if os.environ.get("L2FETCH"):  # cudaLimitMaxL2FetchGranularity (0x05) experiment
+    import glob
+    rt = C.CDLL(sorted(glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib", "libcudart.so*")))[0])
+    torch.zeros(1, device=dev)
+    r = rt.cudaDeviceSetLimit(5, C.c_size_t(int(os.environ["L2FETCH"])))
+    v = C.c_size_t()
+    rt.cudaDeviceGetLimit(C.byref(v), 5)
+    print("L2 fetch granularity set", r, "->", v.value)
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 rng = np.random.default_rng(3)
@@ -34,7 +43,14 @@ else:
     if cfg == "E4short":  # same total lookups in 4x as many 4x shorter bags
         nb = nb * 4
         lens = np.full(nb, int(round(lens.mean() / 4)))
+    if os.environ.get("NBAGS"):  # fixed-cost probe: fewer bags
+        nb = int(os.environ["NBAGS"])
+        lens = lens[:nb]
     idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
+    if cfg == "E4seq":  # gather cost probe: consecutive rows
+        idx = np.arange(int(lens.sum()), dtype=np.int64)
+    if cfg == "E4hot":  # L2-resident probe: 64K distinct rows
+        idx = rng.integers(0, 65536, int(lens.sum())).astype(np.int64)
     w = torch.from_numpy(rng.uniform(0, 1, int(lens.sum())).astype(np.float32)).to(dev)
     rb = d // 2
 rows = torch.randint(0, 256, (R, rb), dtype=torch.uint8, device=dev)
@@ -62,3 +78,28 @@ for i in range(iters):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1) * 1e3)
 print(cfg, "checked" if checked else "unchecked", "us:", [round(t, 1) for t in ts])
+# back-to-back launches (no flush in between): per-launch time in a stream of batches
+if os.environ.get("B2B"):
+    nrep = int(os.environ["B2B"])
+    torch.cuda.synchronize()
+    torch.cuda._sleep(2_000_000)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(nrep):
+        if checked:
+            L.call("abftlp_eb_checked", tab, vp(off), vp(ix), nb, vp(w) if w is not None else None, vp(o), d, vp(fl),
+                   None, None, None, None, st)
+        else:
+            L.call("abftlp_eb_unchecked", tab, vp(off), vp(ix), nb, vp(w) if w is not None else None, vp(o), d, None, st)
+    e1.record()
+    torch.cuda.synchronize()
+    print(cfg, "back-to-back x%d: %.2f us/launch" % (nrep, e0.elapsed_time(e1) * 1e3 / nrep))
+    # single launch queued behind a sleep (host latency excluded), L2 flushed first
+    L.call("abftlp_l2_flush", vp(fb), fb.numel(), 99, st)
+    torch.cuda._sleep(2_000_000)
+    e0.record()
+    L.call("abftlp_eb_checked", tab, vp(off), vp(ix), nb, vp(w) if w is not None else None, vp(o), d, vp(fl),
+           None, None, None, None, st)
+    e1.record()
+    torch.cuda.synchronize()
+    print(cfg, "queued single after flush: %.2f us" % (e0.elapsed_time(e1) * 1e3))

@@ -83,3 +83,29 @@ def test_grouped_fault_list_limits():
         G.abft_gemm_batched(a, pb, faults=[(0, 0, 0, 0)] * 9)
     with pytest.raises(_lib.InvalidArgument):  # out_of_range -> ABFTLP_ERR_INVALID_ARGUMENT
         G.abft_gemm_batched(a, pb, faults=[(2, 0, 0, 0)])
+
+
+@pytest.mark.parametrize("nb,m,n,k", [(21, 256, 512, 384), (3, 40, 130, 200), (1, 7, 64, 128)])
+def test_host_batched_job_matches_oracle(nb, m, n, k):
+    """abftlp_gemm_checked_host_batched (pinned host buffers, pipelined copy-in / grouped launch / copy-out):
+    every run's C', checksum column, flags and count equal the oracle's abft_gemm on that run."""
+    import ctypes as C
+    import torch
+    from paper_2103_00130_b200 import _lib
+    from paper_2103_00130_b200 import gemm as G
+    a = np.stack([O.gemm_inputs(20260823, t, m, n, k)[0] for t in range(nb)])
+    b = O.gemm_inputs(20260823, 0, m, n, k)[1]
+    pb = G.PackedEncodedWeight(b)
+    ah = torch.from_numpy(a).pin_memory()
+    ch = torch.zeros((nb, m, n), dtype=torch.int32).pin_memory()
+    csh = torch.zeros((nb, m), dtype=torch.int32).pin_memory()
+    flh = torch.ones((nb, m), dtype=torch.uint8).pin_memory()
+    eh = torch.full((nb,), 7, dtype=torch.int32).pin_memory()
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.call("abftlp_gemm_checked_host_batched", vp(ah), nb, m, k, m * k, pb.handle, vp(ch), n, m * n, vp(csh), m,
+              vp(flh), m, vp(eh), None)
+    for t in range(nb):
+        ref, fl, e = O.abft_gemm(a[t], b)
+        assert np.array_equal(ch[t].numpy(), ref[:, :n]), t
+        assert np.array_equal(csh[t].numpy(), ref[:, n]), t
+        assert not flh[t].numpy().any() and int(eh[t]) == e == 0, t
