@@ -351,7 +351,10 @@ struct AsyncRing {
 #ifndef ABFT_EB_NST64
 #define ABFT_EB_NST64 4
 #endif
-    static constexpr int NST = SLICE <= 32 ? ABFT_EB_NST32 : SLICE <= 64 ? ABFT_EB_NST64 : SLICE <= 128 ? 3 : 2;
+#ifndef ABFT_EB_NST128
+#define ABFT_EB_NST128 2  // measured: occupancy beats ring depth for 128-B slices (D5, E3)
+#endif
+    static constexpr int NST = SLICE <= 32 ? ABFT_EB_NST32 : SLICE <= 64 ? ABFT_EB_NST64 : SLICE <= 128 ? ABFT_EB_NST128 : 2;
 };
 template <int BPL>
 struct AsyncStage {
@@ -441,7 +444,7 @@ __device__ __forceinline__ unsigned long long decode_pair_bits(W w, int c) {
 }
 
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
-__global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int log2d) {
+__global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
     constexpr int SLICE = 32 * BPL;        // bytes of a row this warp needs
     constexpr int PIECES = SLICE / 16;     // 16-B copies per row slice
@@ -580,37 +583,72 @@ __global__ void __launch_bounds__(256) eb_bag_async_kernel(const EbParams p, int
                 __syncwarp();
             }
             const int tmax = (cnt + 3) & ~3;  // slots cnt..tmax-1 are neutral
-#pragma unroll 4
-            for (int t = 0; t < tmax; ++t) {
-                float s, b;
-                int32_t rs;
-                smem_meta<SCALE>(S.meta[sl][t], s, b, rs);
-                const float w = WEIGHTED ? S.w[sl][t] : 1.0f;
-                // cSum in the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), kept by every
-                // lane of the slice-0 warp (same terms, same order, same value) inside the lookup loop, so the
-                // dependent DADD chain overlaps the column arithmetic. A neutral slot's +0.0 term is an exact
-                // no-op (cSum starts at +0.0 and never becomes -0.0 in round-to-nearest).
-                if constexpr (CHECKED)
-                    if (slice == 0) csum = __dadd_rn(csum, S.term[t]);
-                const auto word = lds_word<BPL>(&S.rows[sl][t][lane * BPL]);
-                if constexpr (CPL >= 2) {
-                    const unsigned long long s2 = f2_pack(s, s), b2 = f2_pack(b, b);
-                    const unsigned long long w2 = f2_pack(w, w);
+            // Four lookups per step with the instruction-level parallelism spelled out: every shared-memory
+            // load of the four first, then their (independent) column values, then the accumulations in
+            // lookup order -- the only loop-carried chains are the per-column fp32 adds and the cSum DADD.
+            using Word = typename LaneWord<BPL>::T;
+            constexpr int NP = CPL >= 2 ? CPL / 2 : 1;
+#pragma unroll 1
+            for (int t0 = 0; t0 < tmax; t0 += 4) {
+                uint4 mt[4];
+                Word wd[4];
+                float wt[4];
+                double tm[4];
 #pragma unroll
-                    for (int c = 0; c < CPL; c += 2) {
-                        const unsigned long long q2 = f2_add(decode_pair_bits<ELEM>(word, c), magic2);
-                        unsigned long long x2 = f2_add(f2_fma(s2, q2, nz2), b2);
-                        if constexpr (WEIGHTED) x2 = f2_fma(w2, x2, nz2);
-                        acc2[c / 2] = f2_add(acc2[c / 2], x2);
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < CPL; ++c) {
-                        float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(word, c)), b);
-                        if constexpr (WEIGHTED) x = __fmul_rn(w, x);
-                        acc[c] = __fadd_rn(acc[c], x);
-                    }
+                for (int u = 0; u < 4; ++u) {
+                    mt[u] = S.meta[sl][t0 + u];
+                    wd[u] = lds_word<BPL>(&S.rows[sl][t0 + u][lane * BPL]);
+                    wt[u] = WEIGHTED ? S.w[sl][t0 + u] : 1.0f;
+                    if constexpr (CHECKED) tm[u] = S.term[t0 + u];
                 }
+                if constexpr (CPL >= 2) {
+                    unsigned long long xv[4][NP];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s, b;
+                        int32_t rs;
+                        smem_meta<SCALE>(mt[u], s, b, rs);
+                        const unsigned long long s2 = f2_pack(s, s), b2 = f2_pack(b, b);
+                        const unsigned long long w2 = f2_pack(wt[u], wt[u]);
+#pragma unroll
+                        for (int c = 0; c < CPL; c += 2) {
+                            const unsigned long long q2 = f2_add(decode_pair_bits<ELEM>(wd[u], c), magic2);
+                            unsigned long long x2 = f2_add(f2_fma(s2, q2, nz2), b2);
+                            if constexpr (WEIGHTED) x2 = f2_fma(w2, x2, nz2);
+                            xv[u][c / 2] = x2;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int c = 0; c < NP; ++c) acc2[c] = f2_add(acc2[c], xv[u][c]);
+                } else {
+                    float xv[4][CPL];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float s, b;
+                        int32_t rs;
+                        smem_meta<SCALE>(mt[u], s, b, rs);
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) {
+                            float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(wd[u], c)), b);
+                            if constexpr (WEIGHTED) x = __fmul_rn(wt[u], x);
+                            xv[u][c] = x;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int c = 0; c < CPL; ++c) acc[c] = __fadd_rn(acc[c], xv[u][c]);
+                }
+                // cSum in the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), kept by every
+                // lane of the slice-0 warp (same terms, same order, same value). A neutral slot's +0.0 term is
+                // an exact no-op (cSum starts at +0.0 and never becomes -0.0 in round-to-nearest).
+                if constexpr (CHECKED)
+                    if (slice == 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) csum = __dadd_rn(csum, tm[u]);
+                    }
             }
             __syncwarp();  // slot `sl` may be refilled by a later issue
         }
@@ -948,7 +986,13 @@ static cudaError_t launch_bag_generic(const EbParams& p, bool checked, int log2d
 
 // Warps per bag: enough warps to keep ~32 resident per SM when the batch is small.
 static int pick_wpb(int64_t num_bags, int64_t d_over_32, bool u4) {
-    const int64_t target = 148 * 32;
+    if (const char* e = std::getenv("ABFTLP_EB_WPB")) {  // tuning override (1, 2 or 4; must divide d/32)
+        const int f = std::atoi(e);
+        if ((f == 1 || f == 2 || f == 4) && d_over_32 % f == 0 && (!u4 || d_over_32 / f >= 2)) return f;
+    }
+    // Split a bag over several warps only for small batches: a warp that owns the whole row amortises the
+    // per-lookup metadata work over more columns, and occupancy (not per-bag latency) bounds the rest.
+    const int64_t target = 148 * 8;
     int wpb = 1;
     while (wpb < 4 && num_bags * wpb * 2 <= target && (d_over_32 % (wpb * 2)) == 0 &&
            (!u4 || (d_over_32 / (wpb * 2)) >= 2))

@@ -26,7 +26,18 @@ if os.environ.get("L2FETCH"):  # cudaLimitMaxL2FetchGranularity (0x05) experimen
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 rng = np.random.default_rng(3)
-if cfg == "E3":
+if cfg == "D5":  # one table of BASELINE configs[4]: 1M x 128 int8, fp32 scale/bias, 8192 bags x 80, Zipf(1.05)
+    R, d, nb, elem, sct = 1_000_000, 128, 8192, 0, 0
+    lens = np.full(nb, 80)
+    ranks = np.arange(1, R + 1, dtype=np.float64)
+    cdf = np.cumsum(ranks ** -1.05)
+    cdf /= cdf[-1]
+    idx = rng.permutation(R)[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+    if os.environ.get("UNIFORM"):
+        idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
+    w = None
+    rb = d
+elif cfg == "E3":
     R, d, nb, elem, sct = 4_000_000, 128, 2048, 1, 0
     lens = rng.integers(20, 101, nb)
     ranks = np.arange(1, R + 1, dtype=np.float64)
