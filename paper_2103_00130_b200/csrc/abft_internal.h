@@ -84,6 +84,10 @@ struct GemmParams {
     // [0, kb_half) of tile t, adds the partial and runs the epilogue. split == 1: one unit per tile.
     int split;
     int kb_half;
+    // checksum-column GEMV by the pairs the tile grid leaves idle (tall narrow shapes): tile epilogues then
+    // contribute no GEMV share, and every row expects row_arrivals = n_tiles + 1 arrivals (n_tiles otherwise)
+    int gemv_helpers;
+    int row_arrivals;
     int32_t* partial;     // [num_tiles][2 CTAs][BN/32][32][128] int32 (split only)
     uint32_t* part_flag;  // [num_tiles * 2], self-resetting
     int32_t* c;

@@ -113,6 +113,105 @@ __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int b, int r
     return s;
 }
 
+// ============================================================ row verdicts
+// One 64-bit atomic per row carries a contribution's GEMV share (high 32 bits), one arrival and its residue
+// (kRowAcc* layout). Atomics on one address are totally ordered, so the thread whose add brings arrival
+// p.row_arrivals holds the complete row: it applies the reference's comparison (P:src/gemm_abft.cpp:113-124),
+// writes the flag and the checksum column (after any injected C'[:, n] fault) and resets the slot.
+__device__ __forceinline__ void row_arrive(const GemmParams& p, int b, int row, unsigned long long add, int& fin,
+                                           int& flag) {
+    unsigned long long* racc = p.row_acc + static_cast<int64_t>(b) * p.m + row;
+    const unsigned long long v = atomicAdd(racc, add) + add;
+    if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.row_arrivals)) {
+        fin = 1;
+        int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
+        for (int f = 0; f < p.nfaults; ++f)
+            if (b == p.fault_b[f] && row == p.fault_row[f] && p.fault_col[f] == p.n)
+                csv ^= static_cast<int32_t>(1u << p.fault_bit[f]);  // fault in C'[:, n]
+        const uint32_t res = static_cast<uint32_t>(v & kRowAccResMask) % 127u;
+        flag = static_cast<int32_t>(res) != mod127(csv);
+        p.flags[b * p.flags_bstride + row] = static_cast<uint8_t>(flag);
+        p.csum[b * p.csum_bstride + static_cast<int64_t>(row) * p.csum_ld] = csv;
+        *racc = 0ull;  // self-resetting workspace
+    }
+}
+// (finished rows) << 32 | (flagged rows) per warp on the problem's word; the call's last finished row publishes
+__device__ __forceinline__ void warp_publish(const GemmParams& p, int b, int fin, int flag) {
+    const uint32_t nfin = __popc(__ballot_sync(0xffffffffu, fin));
+    const uint32_t nflag = __popc(__ballot_sync(0xffffffffu, flag));
+    if ((threadIdx.x & 31) == 0 && nfin) {
+        const unsigned long long prev = atomicAdd(p.err_pack + b, (static_cast<unsigned long long>(nfin) << 32) | nflag);
+        if ((prev >> 32) + nfin == static_cast<unsigned long long>(p.m)) {
+            p.err_count[b] = static_cast<uint32_t>(prev) + nflag;
+            p.err_pack[b] = 0ull;
+        }
+    }
+}
+
+// GEMV helpers (GemmParams::gemv_helpers): when the tile grid leaves pairs idle and few N tiles would split
+// K (tall, narrow shards such as the D5 MLP layers), the idle CTAs compute the whole checksum column
+// C'[:, n] = A * cs and add it as one extra arrival per row. A warp takes 8 consecutive rows of a problem;
+// rows are read coalesced (lane l: bytes [16 l + 512 c, +16) of chunk c), four rows x four 512-byte chunks
+// of loads in flight per lane before any is consumed (the helpers are latency-bound otherwise), each row
+// reduced with one redux.sync and kept by lane (row % 8), which then arrives for its row.
+__device__ __forceinline__ uint4 ld_slot(const uint8_t* p, int valid) {
+    if (valid >= 16) return __ldg(reinterpret_cast<const uint4*>(p));
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int e = 0; e < valid; ++e) w[e >> 2] |= static_cast<uint32_t>(p[e]) << (8 * (e & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ void gemv_helper(const GemmParams& p, int helper_cta, int helper_ctas) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hw = helper_cta * (blockDim.x >> 5) + warp, nhw = helper_ctas * (blockDim.x >> 5);
+    const int tasks_per_problem = (p.m + 7) / 8;
+    const long long tasks = static_cast<long long>(tasks_per_problem) * p.batch;
+    for (long long g = hw; g < tasks; g += nhw) {
+        const int b = static_cast<int>(g / tasks_per_problem);
+        const int r0 = static_cast<int>(g - static_cast<long long>(b) * tasks_per_problem) * 8;
+        const uint8_t* abase = p.a + b * p.a_bstride;
+        const uint8_t* cs = reinterpret_cast<const uint8_t*>(p.cs + b * p.cs_bstride);
+        uint32_t mine = 0u;
+#pragma unroll 1
+        for (int j0 = 0; j0 < 8 && r0 + j0 < p.m; j0 += 4) {
+            uint32_t part[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+            for (int k0 = 0; k0 < p.k; k0 += 2048) {
+                uint4 av[4][4], cv[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int kp = k0 + 512 * c + 16 * lane;
+                    const int valid = min(16, max(0, p.k - kp));
+                    cv[c] = valid > 0 ? ld_slot(cs + kp, valid) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        av[j][c] = (valid > 0 && r0 + j0 + j < p.m)
+                                       ? ld_slot(abase + static_cast<int64_t>(r0 + j0 + j) * p.lda + kp, valid)
+                                       : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        part[j] = __dp4a(av[j][c].x, cv[c].x, part[j]);
+                        part[j] = __dp4a(av[j][c].y, cv[c].y, part[j]);
+                        part[j] = __dp4a(av[j][c].z, cv[c].z, part[j]);
+                        part[j] = __dp4a(av[j][c].w, cv[c].w, part[j]);
+                    }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t tot = __reduce_add_sync(0xffffffffu, part[j]);
+                if (lane == j0 + j) mine = tot;
+            }
+        }
+        int fin = 0, flag = 0;
+        const int row = r0 + lane;
+        if (lane < 8 && row < p.m)
+            row_arrive(p, b, row, (static_cast<unsigned long long>(mine) << 32) | (1ull << kRowAccCountShift), fin, flag);
+        warp_publish(p, b, fin, flag);
+    }
+}
+
 // ============================================================ GEMM (CTA pairs)
 template <int BN>
 struct PairCfg {
@@ -260,7 +359,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     // read and written (PDL: blocks until the previous grid on the stream has completed).
     griddep_wait();
 
-    if (warp == 0 || warp >= 6) {
+    if (CHECKED && p.gemv_helpers && pair >= num_units) {
+        // ---------------- idle pair: checksum-column GEMV for every row (see gemv_helper)
+        gemv_helper(p, (pair - num_units) * 2 + static_cast<int>(rank), (npairs - num_units) * 2);
+    } else if (warp == 0 || warp >= 6) {
         // ---------------- TMA producers (both CTAs; completion counted on the leader's barrier). An SM
         // serves the TMA requests of ONE issuing warp one after another (~275-300 ns each under load,
         // scripts/pipe_bench9.cu), so the stage is split over three warps issuing in parallel:
@@ -355,7 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             // This tile's share of the checksum column C'[row][n] = sum_p A[row][p]*cs[p]: K blocks
             // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
             uint32_t cs_part = 0;
-            if (CHECKED && x.kh == 0) {
+            if (CHECKED && x.kh == 0 && !p.gemv_helpers) {
                 const int kb0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
                 const int kb1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
                 if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, x.b, row, kb0 * kBK, min(kb1 * kBK, p.k));
@@ -556,37 +658,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 // brings arrival n_tiles holds the complete row and finalizes it -- no fences, no
                 // counters, no second pass.
                 int fin = 0, flag = 0;
-                if (row < p.m) {
-                    const unsigned long long add = (static_cast<unsigned long long>(cs_part) << 32) |
-                                                   (1ull << kRowAccCountShift) |
-                                                   static_cast<unsigned long long>(mod127(rsum));
-                    unsigned long long* racc = p.row_acc + static_cast<int64_t>(x.b) * p.m + row;
-                    const unsigned long long v = atomicAdd(racc, add) + add;
-                    if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.n_tiles)) {
-                        fin = 1;
-                        int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
-                        for (int f = 0; f < p.nfaults; ++f)
-                            if (x.b == p.fault_b[f] && row == p.fault_row[f] && p.fault_col[f] == p.n)
-                                csv ^= static_cast<int32_t>(1u << p.fault_bit[f]);  // fault in C'[:, n]
-                        const uint32_t res = static_cast<uint32_t>(v & kRowAccResMask) % 127u;
-                        flag = static_cast<int32_t>(res) != mod127(csv);
-                        p.flags[x.b * p.flags_bstride + row] = static_cast<uint8_t>(flag);
-                        p.csum[x.b * p.csum_bstride + static_cast<int64_t>(row) * p.csum_ld] = csv;
-                        *racc = 0ull;  // self-resetting workspace
-                    }
-                }
+                if (row < p.m)
+                    row_arrive(p, x.b, row,
+                               (static_cast<unsigned long long>(p.gemv_helpers ? 0u : cs_part) << 32) |
+                                   (1ull << kRowAccCountShift) | static_cast<unsigned long long>(mod127(rsum)),
+                               fin, flag);
                 if (trace && local == 0 && threadIdx.x == 64) trace[8] = globaltimer();
-                const uint32_t nfin = __popc(__ballot_sync(0xffffffffu, fin));
-                const uint32_t nflag = __popc(__ballot_sync(0xffffffffu, flag));
-                if (lane == 0 && nfin) {
-                    // (finished rows) << 32 | (flagged rows); the call's last finished row publishes
-                    const unsigned long long prev =
-                        atomicAdd(p.err_pack + x.b, (static_cast<unsigned long long>(nfin) << 32) | nflag);
-                    if ((prev >> 32) + nfin == static_cast<unsigned long long>(p.m)) {
-                        p.err_count[x.b] = static_cast<uint32_t>(prev) + nflag;
-                        p.err_pack[x.b] = 0ull;
-                    }
-                }
+                warp_publish(p, x.b, fin, flag);
             }
         }
         if constexpr (EPI == kEpiTmaStore) {

@@ -476,8 +476,14 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (t.epi == kEpiTmaStore)
         map_c = make_map_c(d_c, static_cast<uint64_t>(w.n), static_cast<uint64_t>(m), static_cast<uint64_t>(ldc),
                            static_cast<uint64_t>(nb), static_cast<uint64_t>(bt.c_bstride));
-    const int pairs = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.num_tiles) * p.split,
-                                                         std::max(1, device_sm_count() / 2)));
+    const int all_pairs = std::max(1, device_sm_count() / 2);
+    int pairs = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(p.num_tiles) * p.split, all_pairs));
+    // Tall narrow shapes leave pairs idle while one or a few N tiles would each carry a large share of the
+    // checksum GEMV: the idle pairs compute it instead (gemv_helper). ABFTLP_GEMV_HELPERS=0 disables.
+    const bool helpers_ok = !std::getenv("ABFTLP_GEMV_HELPERS") || std::atoi(std::getenv("ABFTLP_GEMV_HELPERS")) != 0;
+    p.gemv_helpers = (checked && helpers_ok && n_tiles <= 4 && all_pairs - pairs >= pairs) ? 1 : 0;
+    p.row_arrivals = static_cast<int>(n_tiles) + p.gemv_helpers;
+    if (p.gemv_helpers) pairs = all_pairs;
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
 }

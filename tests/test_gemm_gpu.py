@@ -235,3 +235,21 @@ def test_empty_m(G):
     pb = G.PackedEncodedWeight(np.ones((4, 3), np.int8))
     res = G.abft_gemm(np.zeros((0, 4), np.uint8), pb)
     assert res.errCount == 0 and res.cTemp.data.shape == (0, 4)
+
+
+@pytest.mark.parametrize("m,n,k", [(8192, 64, 2048), (4096, 200, 1000), (3000, 64, 777), (2050, 129, 640)])
+def test_gemv_helpers_tall_narrow_bit_exact(G, m, n, k, monkeypatch):
+    """Tall narrow shapes (the D5 MLP shards): the checksum column is computed by the pairs the tile grid
+    leaves idle (gemv_helper) and added as one extra arrival per row. C', checksum column, verdicts and
+    both fault sides are identical to the oracle, and identical with the helpers switched off."""
+    a, b = rnd(m + 3 * n + k, m, n, k)
+    pb = G.PackedEncodedWeight(b)
+    ct, fl, err = O.abft_gemm(a, b)
+    for helpers in ("1", "0"):
+        monkeypatch.setenv("ABFTLP_GEMV_HELPERS", helpers)
+        for _ in range(2):  # self-resetting row workspace
+            res = G.abft_gemm(a, pb)
+            assert np.array_equal(res.cTemp.data.cpu().numpy(), ct) and res.errCount == err == 0
+        for col in (n // 2, n):
+            bad = G.abft_gemm(a, pb, fault=(m - 1, col, 17))
+            assert bad.errCount == 1 and int(bad.rowFlags[m - 1].item()) == 1
