@@ -500,7 +500,6 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
     int nb_done = 0;
     int64_t bag = static_cast<int64_t>(blockIdx.x) * GROUPS + grp;
     while (bag < p.num_bags) {
-        const unsigned long long next_req = fetch();  // in flight while this bag is processed
         if (tr && lane == 0 && nb_done < 4) tr[1 + 3 * nb_done] = globaltimer();
 
         float acc[CPL];
@@ -564,6 +563,10 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
             for (int c = 0; c < NST - 1; ++c) issue(c, ixs[c]);
         }
         int64_t ix_ahead = NST - 1 < nchunks ? index_of(NST - 1) : -1;
+        // the next bag id is requested once this bag's first gathers are in flight (at launch every group
+        // requests at once: on one address those atomics serialise for ~1 us, which must not delay the
+        // first loads) and is only consumed when this bag is done
+        const unsigned long long next_req = fetch();
         for (int ch = 0; ch < nchunks; ++ch) {
             const int sl = ch % NST;
             issue(ch + NST - 1, ix_ahead);
