@@ -428,19 +428,21 @@ __device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsig
 // Columns c, c+1 of a lane word as spliced floats (before the magic subtraction).
 template <int ELEM, typename W>
 __device__ __forceinline__ unsigned long long decode_pair_bits(W w, int c) {
-    uint32_t lo, hi;
     if constexpr (ELEM == kEbU4) {
-        lo = static_cast<uint32_t>(w >> (4 * c)) & 0xFu;
-        hi = static_cast<uint32_t>(w >> (4 * c + 4)) & 0xFu;
+        const uint32_t lo = static_cast<uint32_t>(w >> (4 * c)) & 0xFu;
+        const uint32_t hi = static_cast<uint32_t>(w >> (4 * c + 4)) & 0xFu;
+        return static_cast<unsigned long long>(0x4B000000u | lo) |
+               (static_cast<unsigned long long>(0x4B000000u | hi) << 32);
     } else {
-        lo = static_cast<uint32_t>(w >> (8 * c)) & 0xFFu;
-        hi = static_cast<uint32_t>(w >> (8 * c + 8)) & 0xFFu;
-        if constexpr (ELEM == kEbS8) {
-            lo ^= 0x80u;
-            hi ^= 0x80u;
-        }
+        // one PRMT per element: byte c of the lane word under the 0x4B0000 mantissa splice (s8: the sign flip
+        // is one XOR per 32-bit half, shared by its four elements)
+        uint32_t half = (sizeof(W) == 8 && c >= 4) ? static_cast<uint32_t>(static_cast<uint64_t>(w) >> 32)
+                                                   : static_cast<uint32_t>(w);
+        if constexpr (ELEM == kEbS8) half ^= 0x80808080u;
+        const uint32_t bsel = static_cast<uint32_t>(c & 3);  // selector nibbles [byte, 4, 5, 7] -> 0x4B0000bb
+        return static_cast<unsigned long long>(__byte_perm(half, 0x4B000000u, 0x7540u | bsel)) |
+               (static_cast<unsigned long long>(__byte_perm(half, 0x4B000000u, 0x7540u | (bsel + 1))) << 32);
     }
-    return static_cast<unsigned long long>(0x4B000000u | lo) | (static_cast<unsigned long long>(0x4B000000u | hi) << 32);
 }
 
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
