@@ -133,6 +133,47 @@ def cpu_gemm_sample(threads: int, reps: int = 1):
     return threads * reps * OPS / dt / 1e12, kind, dt
 
 
+def cpu_eb_sample():
+    """E3 / E4 batches through the oracle's C restatement of abft_embedding_bag (single thread; the reference
+    implements s8 rows only, so the u8 / u4 configs run on its restatement). Host tables of the
+    configs' shapes and distributions, the bags of eb_secondary. Returns {cfg: {ms, alg_gbs}}."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+    out = {}
+    rng = np.random.default_rng(3)
+    for name in ("E3", "E4"):
+        if name == "E3":
+            R, d, nb, elem = 4_000_000, 128, 2048, "u8"
+            lens = rng.integers(20, 101, nb)
+            ranks = np.arange(1, R + 1, dtype=np.float64)
+            cdf = np.cumsum(ranks ** -1.05)
+            cdf /= cdf[-1]
+            idx = rng.permutation(R)[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+            w, rb, meta_b = None, d, 12
+            sc = rng.uniform(1e-3, 1e-2, R).astype(np.float32)
+            bi = rng.uniform(-1, 1, R).astype(np.float32)
+        else:
+            R, d, nb, elem = 8_000_000, 64, 4096, "u4"
+            lens = rng.integers(1, 151, nb)
+            idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
+            w = rng.uniform(0, 1, int(lens.sum())).astype(np.float32)
+            rb, meta_b = d // 2, 8
+            sc = rng.uniform(1e-3, 1e-2, R).astype(np.float16)
+            bi = rng.uniform(-1, 1, R).astype(np.float16)
+        rows = rng.integers(0, 256, (R, rb), dtype=np.uint8)
+        sums = O.row_sums(rows, elem, d)
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        t0 = time.perf_counter()
+        O.eb(rows, sc, bi, off, idx, w, elem=elem, dim=d, row_sums_=sums)
+        dt = time.perf_counter() - t0
+        L_ = int(lens.sum())
+        alg = L_ * (rb + meta_b + 4 + 8 + (4 if w is not None else 0)) + 8 * (nb + 1) + 4 * nb * d + nb
+        out[name] = {"ms": dt * 1e3, "alg_gbs": alg / dt / 1e9, "cores": 1, "kind": "port",
+                     "sample": f"one {name} batch ({nb} bags, {L_} lookups), oracle restatement ({elem} rows)"}
+        del rows, sums
+    return out
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -468,6 +509,11 @@ def run_gpu_arm(args, rank, world, dist):
         tops, kind, dt = cpu_gemm_sample(threads)
         line["cpu_baseline"] = {"value": tops, "unit": "TOPS", "cores": threads, "kind": kind,
                                 "sample": f"{threads} concurrent G2 abft_gemm calls ({dt:.1f} s wall)"}
+        if secondary is not None:
+            try:
+                line["cpu_baseline"]["eb"] = cpu_eb_sample()
+            except MemoryError:
+                pass
     print(json.dumps(line), flush=True)
 
 
@@ -652,15 +698,18 @@ def eb_secondary(L, dev, st, vp, pk):
     import torch
     out = {}
     rng = np.random.default_rng(3)
-    for name in ("E3", "E4"):
-        if name == "E3":
+    for name in ("E3", "E4", "E3_uniform"):
+        if name.startswith("E3"):
             R, d, nb, elem, st_t, meta_b = 4_000_000, 128, 2048, 1, 0, 12
             lens = rng.integers(20, 101, nb)
-            ranks = np.arange(1, R + 1, dtype=np.float64)
-            cdf = np.cumsum(ranks ** -1.05)
-            cdf /= cdf[-1]
-            perm = rng.permutation(R)
-            idx = perm[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+            if name == "E3":
+                ranks = np.arange(1, R + 1, dtype=np.float64)
+                cdf = np.cumsum(ranks ** -1.05)
+                cdf /= cdf[-1]
+                perm = rng.permutation(R)
+                idx = perm[np.searchsorted(cdf, rng.random(int(lens.sum())))].astype(np.int64)
+            else:  # uniform-index control (no Zipf-hot rows served from L2)
+                idx = rng.integers(0, R, int(lens.sum())).astype(np.int64)
             wts = None
             row_b = d
         else:
