@@ -133,6 +133,29 @@ def cpu_gemm_sample(threads: int, reps: int = 1):
     return threads * reps * OPS / dt / 1e12, kind, dt
 
 
+def plan_segments(plan: dict, runs: int, group_max: int, max_faults: int = 8) -> list:
+    """Split a job of `runs` GEMMs into launches: maximal ranges of runs without a B' fault become grouped
+    launches ("group", first, count, [(problem, fault)...]) carrying their C' faults (at most `max_faults`
+    per launch, the kernel's fault list); each B'-fault run is its own launch ("B", run, p, j, bit) between a
+    flip and an unflip of B'. `plan` maps run -> ("B", p, j, bit) | ("C", row, col, bit)."""
+    segments = []
+    start = 0
+    for run in sorted(r for r, f in plan.items() if f[0] == "B") + [runs]:
+        i = start
+        while i < run:
+            cnt = min(run - i, group_max)
+            c_in = [r for r in range(i, i + cnt) if r in plan and plan[r][0] == "C"]
+            if len(c_in) > max_faults:  # cut the group before its (max_faults+1)-th C' fault
+                cnt = c_in[max_faults] - i
+            fl = [(r - i, plan[r]) for r in range(i, i + cnt) if r in plan and plan[r][0] == "C"]
+            segments.append(("group", i, cnt, fl))
+            i += cnt
+        if run < runs:
+            segments.append(("B", run) + tuple(plan[run][1:]))
+        start = run + 1
+    return segments
+
+
 def cpu_eb_sample():
     """E3 / E4 batches through the oracle's C restatement of abft_embedding_bag (single thread; the reference
     implements s8 rows only, so the u8 / u4 configs run on its restatement). Host tables of the
@@ -244,19 +267,7 @@ def run_gpu_arm(args, rank, world, dist):
     # launches (abftlp_gemm_checked_batched_faults: problem b = run b, its own A, C', csum, flags and count;
     # the C' faults of the group ride in the launch's fault list). A run with a B' fault must see the
     # corrupted weight alone, so it is its own launch between a flip and an unflip of B'.
-    segments = []  # ("group", first, count, [faults]) | ("B", run, p, j, bit)
-    start = 0
-    for run in sorted(r for r, f in plan.items() if f[0] == "B") + [JOB]:
-        i = start
-        while i < run:
-            cnt = min(run - i, GROUP_MAX)
-            fl = [(r - i, plan[r]) for r in range(i, i + cnt) if r in plan and plan[r][0] == "C"]
-            segments.append(("group", i, cnt, fl))
-            i += cnt
-        if run < JOB:
-            segments.append(("B", run) + plan[run][1:])
-        start = run + 1
-    assert all(len(sg[3]) <= 8 for sg in segments if sg[0] == "group")
+    segments = plan_segments(plan, JOB, GROUP_MAX)
 
     def launch_group(i0, cnt, fl, checked):
         if checked:
