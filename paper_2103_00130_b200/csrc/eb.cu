@@ -326,7 +326,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // L1-allocating variant for row data: Zipf-hot rows are then served by the SM's L1 instead of
 // hammering one L2 slice.
 __device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem) {
+#ifdef ABFT_EB_ROWS_CG  // (experiment switch: rows through L2 only)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+#elif defined(ABFT_EB_ROWS_256B)  // (experiment switch: L2 prefetch hint for row pieces)
+    asm volatile("cp.async.ca.shared.global.L2::256B [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+#else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
