@@ -530,8 +530,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 const int col0 = n0 + c * 32;
                 if (col0 >= p.n) break;  // warp-uniform
                 uint32_t v[32];
+#ifdef ABFT_TRACE_CHUNKS
+                if (trace && local == 0 && threadIdx.x == 64 && c < 2) trace[12 + c] = globaltimer();
+#endif
                 tmem_ld_32x32b_x32(t_row + c * 32, v);
                 tmem_wait_ld();
+#ifdef ABFT_TRACE_CHUNKS
+                if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[14] = globaltimer();
+#endif
                 if (spart != nullptr) {
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4) {

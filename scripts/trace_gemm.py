@@ -57,7 +57,7 @@ for rep in range(3):
     t0 = t[:, 0].min()
     rel = np.where(t > 0, (t - t0) / 1000.0, np.nan)
     names = {0: "start", 1: "setup", 2: "first_kb(L)", 9: "kb1", 10: "kb2", 11: "kb3", 3: "last_issue(L)",
-             4: "epi_start", 14: "split: published", 12: "split: flag seen", 13: "split: partial in", 7: "chunks_done",
+             4: "epi_start", 14: "split: published / c0 loaded", 12: "split: flag seen / c0 start", 13: "split: partial in / c1 start", 7: "chunks_done",
              8: "cnt_done", 5: "epi_end", 6: "end"}
     print(f"rep {rep}: event {e0.elapsed_time(e1)*1e3:.2f} us, ctas {len(t)}, span {np.nanmax(rel[:, 6]):.2f} us")
     for i, nm in names.items():
