@@ -270,7 +270,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     constexpr int STAGES = Cfg::kStages;
     constexpr int KS = Cfg::KS;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by pointer arithmetic on the __shared__ array (not through an integer round trip),
+    // so the compiler keeps the shared state space: staging-buffer accesses compile to STS/LDS, not to
+    // generic ST/LD
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* staging = smem + STAGES * Cfg::kStageBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(staging + Cfg::kStaging);
     uint64_t* empty = full + STAGES;
@@ -679,8 +682,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         }
         if (trace && threadIdx.x == 64) trace[5] = globaltimer();
     }
+#ifdef ABFT_TRACE_ROLES  // (debug: when each non-epilogue warp reaches the final cluster barrier)
+    if (trace && lane == 0 && (warp == 0 || warp == 1 || warp >= 6))
+        trace[warp == 0 ? 9 : warp == 1 ? 10 : warp == 6 ? 11 : 12] = globaltimer();
+#endif
     tc_fence_before();
+#ifdef ABFT_END_RELAXED
+    cluster_sync_relaxed();
+#else
     cluster_sync();
+#endif
     if (trace && threadIdx.x == 0) trace[6] = globaltimer();
     if (warp == 1) {
         tc_fence_after();
