@@ -195,3 +195,39 @@ def test_table_file_round_trip(E):  # P:tests/test_embedding_abft.cpp:171-195
             E.load_table(p)
     with pytest.raises(_lib.IoError):
         E.load_table("/nonexistent/abft.tbl")
+
+
+@pytest.mark.parametrize("elem,scale,d,weighted,wpb", [("s8", "f32", 128, False, "1"), ("u4", "f16", 64, True, "1"),
+                                                       ("u8", "f32", 128, True, "2"), ("s8", "f16", 256, False, "4"),
+                                                       ("u8", "f32", 64, False, "2")])
+def test_many_bags_per_group_bit_exact(E, elem, scale, d, weighted, wpb, monkeypatch):
+    """Far more bags than resident bag groups (every group works through many bags, including empty ones and
+    runs of them), on each warps-per-bag split: bit-exact against the oracle, including the flag count."""
+    monkeypatch.setenv("ABFTLP_EB_WPB", wpb)
+    rng = np.random.default_rng(d * 7 + int(wpb))
+    R, nb = 3000, 30000
+    rb = d // 2 if elem == "u4" else d
+    rows = rng.integers(0 if elem != "s8" else -128, 256 if elem != "s8" else 128, (R, rb)).astype(
+        np.int8 if elem == "s8" else np.uint8)
+    sdt = np.float16 if scale == "f16" else np.float32
+    sc = rng.uniform(1e-3, 1e-2, R).astype(sdt)
+    bi = rng.uniform(-1, 1, R).astype(sdt)
+    lens = rng.integers(0, 41, nb)
+    lens[rng.random(nb) < 0.1] = 0  # 10 % empty bags, some consecutive
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    idx = rng.integers(0, R, off[-1]).astype(np.int64)
+    w = rng.uniform(0, 1, off[-1]).astype(np.float32) if weighted else None
+    t = E.QuantEmbeddingTable(rows, sc, bi, elem=elem, dim=d)
+    # corrupt a few rows after the row sums (the stored sums stay those of the clean rows), so bags are flagged
+    rows_now = rows.copy().view(np.uint8)
+    for r in rng.choice(R, 20, replace=False):
+        col, bit = int(rng.integers(0, d)), int(rng.integers(0, 4))
+        t.flip_bit(int(r), col, bit)
+        if elem == "u4":
+            rows_now[r, col // 2] ^= np.uint8(1 << (bit + 4 * (col & 1)))
+        else:
+            rows_now[r, col] ^= np.uint8(1 << bit)
+    ref = O.eb(rows_now.view(rows.dtype), sc, bi, off, idx, w, elem=elem, dim=d, row_sums_=O.row_sums(rows, elem, d))
+    out, flags, rsum, csum, cnt = E.eb_csr(t, off, idx, w)
+    assert_same(out, flags, rsum, csum, ref)
+    assert int(cnt.item()) == int(ref[3].sum()) > 0
