@@ -767,12 +767,30 @@ def eb_secondary(L, dev, st, vp, pk):
                 if s >= 2:
                     ts.append(e0.elapsed_time(e1) * 1e3)
             res[checked] = statistics.median(ts)
+        # random-gather floor of the same lookups (abftlp_gather_probe): every looked-up record read once with
+        # maximal memory-level parallelism and no arithmetic, L2 flushed -- the practical roof for these batches
+        rec = 128 if row_b > 64 else 64  # E3: the 128-B rows; E4: the table's packed 64-B row+meta records
+        gtab = rows if rec == row_b else torch.empty((R, rec), dtype=torch.uint8, device=dev)
+        sink = torch.zeros(1, dtype=torch.int32, device=dev)
+        fts = []
+        for s_ in range(5):
+            L.call("abftlp_l2_flush", vp(fb), fb.numel(), 50 + s_, st)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            L.call("abftlp_gather_probe", vp(gtab), rec, vp(ix), L_, vp(sink), st)
+            e1.record()
+            torch.cuda.synchronize()
+            fts.append(e0.elapsed_time(e1) * 1e3)
+        floor_us = statistics.median(fts[1:])
+        del gtab
         flagged = int(fl.to(torch.int64).sum().item())
         L.lib.abftlp_eb_table_free(tab)
         gbs = alg / (res[True] * 1e-6) / 1e9
         out[name] = {"checked_us": res[True], "unchecked_us": res[False], "alg_bytes": alg, "alg_gbs": gbs,
                      "hbm_frac": gbs / pk["hbm_gbs"], "overhead_pct": 100 * (res[True] - res[False]) / res[False],
-                     "lookups": L_, "bags": nb, "injected_row_faults": n_faults, "flagged_bags": flagged}
+                     "lookups": L_, "bags": nb, "injected_row_faults": n_faults, "flagged_bags": flagged,
+                     "gather_floor_us": floor_us, "frac_of_gather_floor": floor_us / res[True],
+                     "gather_floor_how": f"abftlp_gather_probe: the {L_} looked-up {rec}-B records, L2 flushed"}
         del rows, sc, bi, off, ix, o, fl, fb
         torch.cuda.empty_cache()
     return out

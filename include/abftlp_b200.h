@@ -249,8 +249,13 @@ abftlp_status abftlp_eb_table_flip_bits(abftlp_eb_table* t, const int64_t* d_row
 abftlp_status abftlp_generate(void* d_out, uint64_t count, uint64_t seed, uint64_t rng_stream,
                               uint64_t off, int32_t kind, double lo, double hi, uint64_t bound,
                               abftlp_stream stream);
-/* Writes a buffer larger than L2 (benchmark cache flush). */
+/* Reads a buffer larger than L2 (benchmark cache flush). */
 abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream);
+/* Benchmark roof for the EmbeddingBag lines: reads record d_idx[i] (rec_bytes each, a multiple of 16 up to 512,
+ * from d_table) for every i < n with maximal memory-level parallelism and no arithmetic -- the random-gather
+ * floor of the same lookups. d_sink: one device uint32 (written practically never). */
+abftlp_status abftlp_gather_probe(const void* d_table, uint64_t rec_bytes, const int64_t* d_idx, uint64_t n,
+                                  uint32_t* d_sink, abftlp_stream stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

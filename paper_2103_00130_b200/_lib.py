@@ -131,6 +131,7 @@ _SIGS = {
     "abftlp_eb_table_flip_bits": (i32, [vp, vp, vp, vp, u64, vp, vp]),
     "abftlp_generate": (i32, [vp, u64, u64, u64, u64, i32, f64, f64, u64, vp]),
     "abftlp_l2_flush": (i32, [vp, u64, i32, vp]),
+    "abftlp_gather_probe": (i32, [vp, u64, vp, u64, vp, vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -795,6 +795,18 @@ __attribute__((visibility("default"))) void abftlp_debug_eb_trace(unsigned long 
     abftk::set_eb_trace(d_trace);
 }
 
+abftlp_status abftlp_gather_probe(const void* d_table, uint64_t rec_bytes, const int64_t* d_idx, uint64_t n,
+                                  uint32_t* d_sink, abftlp_stream stream) {
+    if (!d_table || !d_sink || (n && !d_idx)) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    if (rec_bytes == 0 || rec_bytes % 16 != 0 || rec_bytes > 512)
+        return fail(ABFTLP_ERR_INVALID_ARGUMENT, "gather_probe: rec_bytes must be a multiple of 16 up to 512");
+    return guarded([&] {
+        ABFT_CUDA(abftk::launch_gather_probe(d_table, static_cast<int64_t>(rec_bytes), d_idx, static_cast<int64_t>(n),
+                                             d_sink, as_stream(stream)));
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_l2_flush(void* d_buf, uint64_t bytes, int32_t salt, abftlp_stream stream) {
     if (!d_buf) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
     return guarded([&] {

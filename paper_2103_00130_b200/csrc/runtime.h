@@ -133,6 +133,8 @@ cudaError_t launch_set_random(void* cell, int width, uint64_t state, cudaStream_
 cudaError_t launch_nonzero(const uint32_t* value, uint8_t* out, int64_t slot, cudaStream_t st);
 cudaError_t launch_any_flag(const uint8_t* flags, int64_t n, uint8_t* out, int64_t slot, cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, int salt, cudaStream_t st);
+cudaError_t launch_gather_probe(const void* table, int64_t rec_bytes, const int64_t* idx, int64_t n, uint32_t* sink,
+                                cudaStream_t st);
 
 // Host SplitMix64, identical to P:src/rng.hpp:10-43 (drives fault placement on the host).
 struct SplitMix64 {
