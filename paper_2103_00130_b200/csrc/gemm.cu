@@ -640,11 +640,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     }
                     __syncwarp();
                 } else if constexpr (EPI == kEpiDirect) {
+                    // straight from the registers (no shared-memory staging, whose traffic competes with the
+                    // mainloop's operand reads): 16-byte stores when the row segment is aligned
                     if (row < p.m) {
-                        int32_t* crow = cb + static_cast<int64_t>(row) * p.ldc;
+                        int32_t* crow = cb + static_cast<int64_t>(row) * p.ldc + col0;
+                        if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.n) crow[col0 + j] = static_cast<int32_t>(v[j]);
+                            for (int q4 = 0; q4 < 8; ++q4)
+                                reinterpret_cast<uint4*>(crow)[q4] =
+                                    make_uint4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < p.n) crow[j] = static_cast<int32_t>(v[j]);
+                        }
                     }
                 }
             }

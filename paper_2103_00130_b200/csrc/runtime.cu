@@ -267,7 +267,7 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
         const int got = std::sscanf(env, "%d,%d,%d", &bn, &e, &sp);
         if (got >= 1 && (bn == 64 || bn == 128 || bn == 256)) {
             GemmTiling t{bn, epi, 1};
-            if (got >= 2 && e == kEpiNone) t.epi = kEpiNone;
+            if (got >= 2 && (e == kEpiNone || e == kEpiDirect)) t.epi = e;
             if (got >= 2 && (e == kEpiTmaStore || e == kEpiStg) && c_tma_ok) t.epi = e;
             const int64_t tiles = m_tiles * ((n + bn - 1) / bn);
             if (got == 3 && sp == 2 && split_ok(bn, tiles)) t.split = 2;

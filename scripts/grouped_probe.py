@@ -57,7 +57,7 @@ def timeit(fn, reps=3):
 
 
 ref = None
-for tiling in ("256", "128"):
+for tiling in (os.environ.get("TILINGS", "256 128").split()):
     os.environ["ABFTLP_GEMM_TILING"] = tiling
     for chunk in CHUNKS:
         for ck in (True, False):
