@@ -222,6 +222,22 @@ abftlp_status abftlp_eb_checked_scatter(const abftlp_eb_table* t, const int64_t*
                                         uint64_t bags_per_dest, uint32_t* d_flag_count,
                                         int32_t* d_status, abftlp_stream stream);
 
+/* Grouped checked lookups over several tables (one element type, scale type and dim; e.g. one GPU's tables of
+ * the D5 DLRM step) in ONE persistent launch: table i has its own CSR bags (d_offsets[i], d_indices[i],
+ * optional d_weights[i]), the same bag count per table, and scatter destinations d_out_dest[i] / d_flag_dest[i]
+ * (device arrays of pointers, as in abftlp_eb_checked_scatter). The host arrays passed to _create are read
+ * once; the group keeps a device copy. Results are identical to one abftlp_eb_checked_scatter per table. */
+typedef struct abftlp_eb_group_s abftlp_eb_group;
+abftlp_status abftlp_eb_group_create(const abftlp_eb_table* const* tables, uint32_t ntables,
+                                     const int64_t* const* d_offsets, const int64_t* const* d_indices,
+                                     const float* const* d_weights /* nullable */,
+                                     float* const* const* d_out_dest, uint8_t* const* const* d_flag_dest,
+                                     abftlp_eb_group** out);
+void abftlp_eb_group_free(abftlp_eb_group* g);
+abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
+                                              uint64_t flag_ld, uint64_t bags_per_dest, uint32_t* d_flag_count,
+                                              int32_t* d_status, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ fault injection */
 /* XOR bit `bit` of element `index` of an array of `elem_bytes`-wide integers
  * (flip_bit, P:src/fault_lab.hpp:87-93). */

@@ -111,6 +111,7 @@ _SIGS = {
     "abftlp_gemm_checked_host": (i32, [vp, u64, u64, vp, vp, u64, vp, vp, vp, vp]),
     "abftlp_eb_table_create": (i32, [i32, vp, u64, u64, u64, i32, vp, vp, vp, vp, P(vp)]),
     "abftlp_eb_table_free": (None, [vp]),
+    "abftlp_eb_group_free": (None, [vp]),
     "abftlp_eb_table_validate": (i32, [vp, vp, vp, P(u64)]),
     "abftlp_eb_table_row_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_checked": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, vp, vp, vp, vp, vp]),
@@ -124,6 +125,8 @@ _SIGS = {
     "abftlp_requantize": (i32, [vp, u64, u64, u64, vp, vp, vp, vp, u64, vp]),
     "abftlp_row_sums_u8": (i32, [vp, u64, u64, u64, vp, vp]),
     "abftlp_gemm_weight_col_sums": (i32, [vp, vp, vp]),
+    "abftlp_eb_group_create": (i32, [vp, u32, vp, vp, vp, vp, vp, vp]),
+    "abftlp_eb_group_checked_scatter": (i32, [vp, u64, u64, u64, u64, vp, vp, vp]),
     "abftlp_eb_checked_scatter": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, u64, u64, vp, vp, vp]),
     "abftlp_flip_bit": (i32, [vp, u32, u64, u32, vp]),
     "abftlp_gemm_weight_flip_bit": (i32, [vp, u64, u64, u32, vp]),

@@ -153,6 +153,18 @@ struct EbTable {
     int64_t rec_stride = 0, meta_off = 0, packed_cap = 0;
 };
 
+// One table of a grouped EmbeddingBag launch (EbParams::tables): the per-table fields of EbParams.
+struct EbTableDesc {
+    const uint8_t* data;
+    const void* meta;
+    int64_t meta_stride, rows, row_stride;
+    const int64_t* offsets;  // [bags_per_table + 1]
+    const int64_t* indices;
+    const float* weights;    // nullable
+    float* const* out_dest;  // scatter destinations of this table (see EbParams)
+    uint8_t* const* flag_dest;
+};
+
 struct EbParams {
     const uint8_t* data;
     const void* meta;
@@ -181,6 +193,11 @@ struct EbParams {
     uint8_t* const* flag_dest;
     int64_t bags_per_dest;
     int64_t flag_ld;
+    // grouped tables (one launch over several tables of one element type, scale type and dim): when set,
+    // num_bags counts the bags of ALL tables, bag g is bag g % bags_per_table of table g / bags_per_table, and
+    // the per-table fields (data, meta, offsets, indices, weights, scatter destinations) come from tables[t]
+    const EbTableDesc* tables;
+    int64_t bags_per_table;
 };
 
 }  // namespace abftk

@@ -40,6 +40,9 @@ struct abftlp_gemm_weight_s {
 struct abftlp_eb_table_s {
     abftk::EbTable* t;
 };
+struct abftlp_eb_group_s {
+    abftk::EbGroup* g;
+};
 
 namespace {
 
@@ -724,6 +727,41 @@ abftlp_status abftlp_eb_checked_scatter(const abftlp_eb_table* t, const int64_t*
         abftk::eb_run(*t->t, d_offsets, d_indices, static_cast<int64_t>(num_bags), d_weights, nullptr,
                       static_cast<int64_t>(ld_out), true, nullptr, nullptr, nullptr, d_flag_count, d_status,
                       as_stream(stream), &sc);
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_group_create(const abftlp_eb_table* const* tables, uint32_t ntables,
+                                     const int64_t* const* d_offsets, const int64_t* const* d_indices,
+                                     const float* const* d_weights, float* const* const* d_out_dest,
+                                     uint8_t* const* const* d_flag_dest, abftlp_eb_group** out) {
+    if (!out || !tables || ntables == 0) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        std::vector<const abftk::EbTable*> ts(ntables);
+        for (uint32_t i = 0; i < ntables; ++i) {
+            if (!tables[i]) throw std::invalid_argument("null argument");
+            ts[i] = tables[i]->t;
+        }
+        *out = new abftlp_eb_group_s{abftk::eb_group_create(ts.data(), ntables, d_offsets, d_indices, d_weights,
+                                                            d_out_dest, d_flag_dest)};
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_eb_group_free(abftlp_eb_group* g) {
+    if (!g) return;
+    abftk::eb_group_free(g->g);
+    delete g;
+}
+
+abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
+                                              uint64_t flag_ld, uint64_t bags_per_dest, uint32_t* d_flag_count,
+                                              int32_t* d_status, abftlp_stream stream) {
+    if (!g) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_group_run(*g->g, static_cast<int64_t>(bags_per_table), static_cast<int64_t>(ld_out),
+                            static_cast<int64_t>(flag_ld), static_cast<int64_t>(bags_per_dest), true, d_flag_count,
+                            d_status, as_stream(stream));
         return ABFTLP_OK;
     });
 }

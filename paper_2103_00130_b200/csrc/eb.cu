@@ -509,6 +509,24 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
     int64_t bag = static_cast<int64_t>(blockIdx.x) * GROUPS + grp;
     while (bag < p.num_bags) {
         if (tr && lane == 0 && nb_done < 4) tr[1 + 3 * nb_done] = globaltimer();
+        // the bag's table view: the launch's own fields, or (grouped tables) its table's descriptor
+        EbParams tv = p;
+        int64_t lb = bag;  // bag index within its table
+        if (p.tables) {
+            const int64_t t = bag / p.bags_per_table;
+            lb = bag - t * p.bags_per_table;
+            const EbTableDesc& dsc = p.tables[t];
+            tv.data = dsc.data;
+            tv.meta = dsc.meta;
+            tv.meta_stride = dsc.meta_stride;
+            tv.rows = dsc.rows;
+            tv.row_stride = dsc.row_stride;
+            tv.offsets = dsc.offsets;
+            tv.indices = dsc.indices;
+            tv.weights = dsc.weights;
+            tv.out_dest = dsc.out_dest;
+            tv.flag_dest = dsc.flag_dest;
+        }
 
         float acc[CPL];
 #pragma unroll
@@ -521,7 +539,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                                                   -8388608.0f - (ELEM == kEbS8 ? 128.0f : 0.0f));
         double csum = 0.0;
         bool oob = false;
-        const int64_t beg = p.offsets[bag], end = p.offsets[bag + 1];
+        const int64_t beg = tv.offsets[lb], end = tv.offsets[lb + 1];
         const int nchunks = static_cast<int>((end - beg + kChunk - 1) / kChunk);
         // Issue the gathers of chunk `ch` (indices `ix`, one per lane) into ring slot ch % NST. Slots past
         // the bag or out of range get a neutral record (scale = bias = 0, weight 1): they add +0.0, an
@@ -533,15 +551,15 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                 const int sl = ch % NST;
                 const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
                 const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
-                const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(p.rows);
+                const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(tv.rows);
                 if (lane < cnt && !valid) oob = true;
-                S.off[lane] = valid ? ix * p.row_stride + slice_byte : -1;
+                S.off[lane] = valid ? ix * tv.row_stride + slice_byte : -1;
                 if (valid) {
                     if constexpr (SCALE == kEbF32)
-                        cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(p.meta) + ix * p.meta_stride);
+                        cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
                     else
-                        cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(p.meta) + ix * p.meta_stride);
-                    if constexpr (WEIGHTED) cp_async4(&S.w[sl][lane], p.weights + base + lane);
+                        cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
+                    if constexpr (WEIGHTED) cp_async4(&S.w[sl][lane], tv.weights + base + lane);
                 } else {
                     S.meta[sl][lane] = make_uint4(0u, 0u, 0u, 0u);
                     if constexpr (WEIGHTED) S.w[sl][lane] = 1.0f;
@@ -552,7 +570,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                     const int piece = lane + 32 * i;
                     const int r = piece / PIECES, q = piece % PIECES;
                     const int64_t o = S.off[r];
-                    if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], p.data + o + q * 16);
+                    if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
                 }
                 __syncwarp();  // S.off is reused by the next issue
             }
@@ -560,7 +578,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
         };
         auto index_of = [&](int ch) -> int64_t {
             const int64_t e = beg + static_cast<int64_t>(ch) * kChunk + lane;
-            return e < end ? p.indices[e] : -1;
+            return e < end ? tv.indices[e] : -1;
         };
         // prologue: NST-1 chunks in flight, the index of the next one loaded ahead
         {
@@ -670,7 +688,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
         }
         csum = __shfl_sync(0xffffffffu, csum, 0);
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
-        float* dst = out_row(p, bag) + slice * 32 * CPL + lane * CPL;
+        float* dst = out_row(tv, lb) + slice * 32 * CPL + lane * CPL;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
         if constexpr (CHECKED) {
@@ -709,7 +727,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                     rsum = exact;  // every partial sum is exact, so any order gives the reference's value
                 } else {
                     rsum = 0.0;  // the reference's sequential order over the stored outputs
-                    const float* row = out_row(p, bag);
+                    const float* row = out_row(tv, lb);
                     for (int j0 = 0; j0 < p.dim; j0 += 32) {
                         const float v = (j0 + lane < p.dim) ? row[j0 + lane] : 0.0f;
                         for (int l = 0; l < 32 && j0 + l < p.dim; ++l)
@@ -720,7 +738,7 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                 const double mx = fmax(fmax(fabs(rsum), fabs(csum)), 1.0);
                 const int flag = diff > __dmul_rn(1e-5, mx);
                 if (lane == 0) {
-                    if (uint8_t* fs = flag_slot(p, bag)) *fs = static_cast<uint8_t>(flag);
+                    if (uint8_t* fs = flag_slot(tv, lb)) *fs = static_cast<uint8_t>(flag);
                     if (p.rsum) p.rsum[bag] = rsum;
                     if (p.csum) p.csum[bag] = csum;
                     if (flag) atomicAdd(&blk_flags, 1u);
@@ -1021,6 +1039,7 @@ static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, c
         const int64_t cpl = d32 / wpb;
         const bool async_ok = (p.row_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 16) == 0 &&
                               (reinterpret_cast<uintptr_t>(p.meta) % 16) == 0 && !std::getenv("ABFTLP_EB_SYNC");
+        if (p.tables && !async_ok) return cudaErrorNotSupported;  // grouped tables: async kernel only
         if (async_ok) {
 #define ABFT_ASYNC(CPL_, WPB_) \
     if (cpl == CPL_ && wpb == WPB_) return launch_bag_async<ELEM, SCALE, CPL_, WPB_>(p, checked, log2d, st)
@@ -1056,6 +1075,7 @@ static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, c
         ABFT_FAST(8, 2);
 #undef ABFT_FAST
     }
+    if (p.tables) return cudaErrorNotSupported;  // grouped tables: async kernel only
     if (d > 32 * kGenericSlots) return cudaErrorInvalidValue;
     return launch_bag_generic<ELEM, SCALE>(p, checked, log2d, st);
 }

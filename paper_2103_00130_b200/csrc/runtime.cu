@@ -688,6 +688,100 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     cuda_check(e, "eb_bag_kernel");
 }
 
+static EbTableDesc eb_desc(const EbTable& t) {
+    EbTableDesc d{};
+    d.data = t.packed ? t.packed : t.data;
+    d.meta = t.packed ? static_cast<const void*>(t.packed + t.meta_off) : t.meta;
+    d.meta_stride = t.packed ? t.rec_stride
+                             : static_cast<int64_t>(t.scale_type == kEbF32 ? sizeof(EbMetaF32) : sizeof(EbMetaF16));
+    d.rows = t.rows;
+    d.row_stride = t.packed ? t.rec_stride : t.row_stride;
+    return d;
+}
+
+EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const int64_t* const* d_offsets,
+                         const int64_t* const* d_indices, const float* const* d_weights, float* const* const* d_out_dest,
+                         uint8_t* const* const* d_flag_dest) {
+    if (ntables < 1 || !tables || !d_offsets || !d_indices || !d_out_dest || !d_flag_dest)
+        throw std::invalid_argument("null argument");
+    std::vector<EbTableDesc> h(static_cast<size_t>(ntables));
+    const bool weighted = d_weights != nullptr && d_weights[0] != nullptr;
+    for (int64_t i = 0; i < ntables; ++i) {
+        const EbTable* t = tables[i];
+        if (!t || !d_offsets[i] || !d_indices[i] || !d_out_dest[i] || !d_flag_dest[i])
+            throw std::invalid_argument("null argument");
+        if (t->elem != tables[0]->elem || t->scale_type != tables[0]->scale_type || t->dim != tables[0]->dim ||
+            (t->packed != nullptr) != (tables[0]->packed != nullptr))
+            throw std::invalid_argument("eb_group: tables must share element type, scale type, dim and layout");
+        if (weighted != (d_weights != nullptr && d_weights[i] != nullptr))
+            throw std::invalid_argument("eb_group: either every table or none has weights");
+        h[i] = eb_desc(*t);
+        h[i].offsets = d_offsets[i];
+        h[i].indices = d_indices[i];
+        h[i].weights = weighted ? d_weights[i] : nullptr;
+        h[i].out_dest = d_out_dest[i];
+        h[i].flag_dest = d_flag_dest[i];
+    }
+    auto* g = new EbGroup();
+    g->tables.assign(tables, tables + ntables);
+    g->weighted = weighted;
+    cudaError_t e = cudaMalloc(&g->d_desc, sizeof(EbTableDesc) * h.size());
+    if (e == cudaSuccess) e = cudaMemcpy(g->d_desc, h.data(), sizeof(EbTableDesc) * h.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(g->d_desc);
+        delete g;
+        cuda_check(e, "eb_group_create");
+    }
+    return g;
+}
+
+void eb_group_free(EbGroup* g) {
+    if (!g) return;
+    cudaFree(g->d_desc);
+    delete g;
+}
+
+void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int64_t flag_ld, int64_t bags_per_dest,
+                  bool checked, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st) {
+    if (bags_per_table < 0) throw std::invalid_argument("embedding_bag: negative bag count");
+    const EbTable& t0 = *g.tables[0];
+    if (ld_out < t0.dim || bags_per_dest <= 0) throw std::invalid_argument("embedding_bag: invalid scatter destinations");
+    const int64_t total = bags_per_table * static_cast<int64_t>(g.tables.size());
+    if (total == 0) {
+        if (checked && d_flag_count) cuda_check(cudaMemsetAsync(d_flag_count, 0, 4, st), "cudaMemsetAsync");
+        return;
+    }
+    Workspace& ws = ws_for(st);
+    std::lock_guard<std::mutex> lk(ws.mu);
+    const EbTableDesc d0 = eb_desc(t0);
+    EbParams p{};
+    p.data = d0.data;  // table 0's layout (shared by the group) drives the kernel choice
+    p.meta = d0.meta;
+    p.meta_stride = d0.meta_stride;
+    p.rows = d0.rows;
+    p.dim = t0.dim;
+    p.row_stride = d0.row_stride;
+    // the weighted template variant is chosen from this pointer's presence; the kernel reads each table's own
+    p.weights = g.weighted ? reinterpret_cast<const float*>(g.d_desc) : nullptr;
+    p.num_bags = total;
+    p.ld_out = ld_out;
+    p.flag_count = checked ? d_flag_count : nullptr;
+    p.status = d_status;
+    p.ws_flag_acc = ws.small + 4;
+    p.ws_block_cnt = ws.small + 5;
+    p.ws_bag_ctr = reinterpret_cast<unsigned long long*>(ws.small + 6);
+    p.trace = g_eb_trace;
+    p.neg_zero = -0.0f;
+    p.bags_per_dest = bags_per_dest;
+    p.flag_ld = flag_ld;
+    p.tables = g.d_desc;
+    p.bags_per_table = bags_per_table;
+    const cudaError_t e = launch_eb_bags(t0.elem, t0.scale_type, p, checked, st);
+    if (e == cudaErrorNotSupported)
+        throw std::invalid_argument("eb_group: needs 16-byte aligned rows / metadata and dim % 32 == 0");
+    cuda_check(e, "eb_bag_async_kernel (grouped tables)");
+}
+
 void eb_flip_bit(EbTable& t, int64_t row, int64_t col, uint32_t bit, cudaStream_t st) {
     if (row < 0 || row >= t.rows || col < 0 || col >= t.dim)
         throw std::out_of_range("inject_eb_table: coordinates out of range");

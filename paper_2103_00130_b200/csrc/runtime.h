@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include <vector>
+
 #include "abft_internal.h"
 
 namespace abftk {
@@ -96,6 +98,19 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
             double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st,
             const EbScatter* scatter = nullptr);
 int64_t eb_elem_row_bytes(int elem, int64_t dim);
+// Grouped lookups: several tables of one element type, scale type and dim, each with its own bags (the same
+// count per table), scatter destinations and optional weights, in ONE persistent launch (D5: a GPU's tables).
+struct EbGroup {
+    std::vector<const EbTable*> tables;
+    EbTableDesc* d_desc = nullptr;  // device copy of the per-table descriptors
+    bool weighted = false;
+};
+EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const int64_t* const* d_offsets,
+                         const int64_t* const* d_indices, const float* const* d_weights, float* const* const* d_out_dest,
+                         uint8_t* const* const* d_flag_dest);
+void eb_group_free(EbGroup* g);
+void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int64_t flag_ld, int64_t bags_per_dest,
+                  bool checked, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st);
 
 // ---- fault lab
 void flip_bit(void* d_base, uint64_t byte_offset, uint32_t bit, cudaStream_t st);

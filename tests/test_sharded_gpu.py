@@ -73,3 +73,71 @@ def test_sharded_classes_world1():
     for t in range(T):
         assert np.array_equal(out[:, t].cpu().numpy().view(np.uint32), refs[t][0].view(np.uint32))
         assert np.array_equal(flags[:, t].cpu().numpy(), refs[t][3])
+
+
+@pytest.mark.parametrize("elem,scale,d,weighted", [("s8", "f32", 128, False), ("u4", "f16", 64, True)])
+def test_grouped_tables_equal_per_table_scatter(elem, scale, d, weighted):
+    """abftlp_eb_group_checked_scatter (all of a GPU's tables in ONE launch, D5) writes exactly what one
+    abftlp_eb_checked_scatter per table writes: pooled vectors, flags and the total flag count."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200 import embedding as E
+    dev = torch.device("cuda")
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    rng = np.random.default_rng(d)
+    T, R, B, G = 5, 4000, 1200, 4
+    Bg = B // G
+    tabs, keep, bags = [], [], []
+    for t in range(T):
+        rb = d // 2 if elem == "u4" else d
+        rows = rng.integers(0 if elem != "s8" else -128, 256 if elem != "s8" else 128, (R, rb)).astype(
+            np.int8 if elem == "s8" else np.uint8)
+        sdt = np.float16 if scale == "f16" else np.float32
+        tab = E.QuantEmbeddingTable(rows, rng.uniform(1e-3, 1e-2, R).astype(sdt), rng.uniform(-1, 1, R).astype(sdt),
+                                    elem=elem, dim=d)
+        for r in rng.choice(R, 10, replace=False):  # some corrupted rows -> some flagged bags
+            tab.flip_bit(int(r), int(rng.integers(0, d)), 1)
+        lens = rng.integers(0, 60, B)
+        off = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)).to(dev)
+        ix = torch.from_numpy(rng.integers(0, R, int(lens.sum())).astype(np.int64)).to(dev)
+        w = torch.from_numpy(rng.uniform(0, 1, int(lens.sum())).astype(np.float32)).to(dev) if weighted else None
+        tabs.append(tab)
+        bags.append((off, ix, w))
+    outs = [torch.full((G, Bg, T, d), float("nan"), dtype=torch.float32, device=dev) for _ in range(2)]
+    flgs = [torch.full((G, Bg, T), 7, dtype=torch.uint8, device=dev) for _ in range(2)]
+    cnt = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(3)]
+    dests = []
+    for k in range(2):
+        per = []
+        for t in range(T):
+            o = torch.tensor([outs[k][g, 0, t].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
+            f = torch.tensor([flgs[k][g, 0, t:].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
+            per.append((o, f))
+        dests.append(per)
+    total = 0
+    for t in range(T):  # reference: one scatter launch per table
+        off, ix, w = bags[t]
+        o, f = dests[0][t]
+        L.call("abftlp_eb_checked_scatter", tabs[t].handle, vp(off), vp(ix), B, vp(w) if w is not None else None,
+               vp(o), T * d, vp(f), T, Bg, vp(cnt[0]), None, None)
+        total += int(cnt[0].item())
+    P = C.c_void_p
+    th = (P * T)(*[tabs[t].handle for t in range(T)])
+    offs = (P * T)(*[P(bags[t][0].data_ptr()) for t in range(T)])
+    ixs = (P * T)(*[P(bags[t][1].data_ptr()) for t in range(T)])
+    ws = (P * T)(*[P(bags[t][2].data_ptr()) for t in range(T)]) if weighted else None
+    ods = (P * T)(*[P(dests[1][t][0].data_ptr()) for t in range(T)])
+    fds = (P * T)(*[P(dests[1][t][1].data_ptr()) for t in range(T)])
+    grp = C.c_void_p()
+    L.call("abftlp_eb_group_create", th, T, offs, ixs, ws, ods, fds, C.byref(grp))
+    for _ in range(2):  # self-resetting workspace
+        L.call("abftlp_eb_group_checked_scatter", grp, B, T * d, T, Bg, vp(cnt[1]), None, None)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[1].view(torch.int32), outs[0].view(torch.int32))
+        assert torch.equal(flgs[1], flgs[0])
+        assert int(cnt[1].item()) == total > 0
+    L.lib.abftlp_eb_group_free(grp)
