@@ -209,6 +209,39 @@ def eb_csr_scatter(table: QuantEmbeddingTable, offsets, indices, weights, out_de
     return cnt
 
 
+def eb_group_scatter(tables: list, bags: list, out_dests: list, flag_dests: list, ld_out: int, flag_ld: int,
+                     bags_per_dest: int, stream=None) -> torch.Tensor:
+    """eb_csr_scatter for several tables (one element type, scale type and dim; the same bag count each) in ONE
+    launch (abftlp_eb_group_checked_scatter). ``bags[i] = (offsets, indices, weights-or-None)`` of table i;
+    ``out_dests[i]`` / ``flag_dests[i]`` are table i's destination lists. Returns the total flag count."""
+    T = len(tables)
+    dev = device()
+    csr = [(to_device(o, torch.int64), to_device(i, torch.int64), None if w is None else to_device(w, torch.float32))
+           for o, i, w in bags]
+    nb = int(csr[0][0].numel()) - 1
+    if any(int(o.numel()) - 1 != nb for o, _, _ in csr):
+        raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "eb_group: every table needs the same bag count")
+    optrs = [torch.tensor([t.data_ptr() for t in od], dtype=torch.int64, device=dev) for od in out_dests]
+    fptrs = [torch.tensor([t.data_ptr() for t in fd], dtype=torch.int64, device=dev) for fd in flag_dests]
+    P = C.c_void_p
+    arr = lambda xs: (P * T)(*xs)  # noqa: E731
+    weights = None if csr[0][2] is None else arr([P(w.data_ptr()) for _, _, w in csr])
+    grp = C.c_void_p()
+    _lib.call("abftlp_eb_group_create", arr([t.handle for t in tables]), T, arr([P(o.data_ptr()) for o, _, _ in csr]),
+              arr([P(i.data_ptr()) if i.numel() else P(8) for _, i, _ in csr]), weights,
+              arr([P(o.data_ptr()) for o in optrs]), arr([P(f.data_ptr()) for f in fptrs]), C.byref(grp))
+    try:
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("abftlp_eb_group_checked_scatter", grp, nb, ld_out, flag_ld, bags_per_dest, ptr(cnt), ptr(status),
+                  stream_handle(stream))
+        if int(status.item()) & 1:
+            raise IndexError("embedding_bag: index out of range")
+    finally:
+        _lib.lib.abftlp_eb_group_free(grp)
+    return cnt
+
+
 def embedding_bag(table: QuantEmbeddingTable, bag: IndexBag) -> torch.Tensor:
     """Plain pooled lookup, fp32 accumulation (P:src/embedding_abft.cpp:47-60)."""
     off, idx, w = _csr([bag])

@@ -102,6 +102,20 @@ class GpuEbBackend:
         flags = [send_flags[g, 0, slot:] for g in range(G)]
         eb_csr_scatter(table, offsets, indices, weights, outs, flags, ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
 
+    def run_all_into(self, tables: list, bags: list, send, send_flags) -> None:
+        """All local tables (slot order) in ONE launch when they share type and dim (abftlp_eb_group_*)."""
+        from .embedding import eb_group_scatter
+        G, Bg, Tg, d = (int(s) for s in send.shape)
+        same = len({(t.elem, t.scale_dtype, t.dim()) for t in tables}) == 1 and \
+            len({w is None for _, _, w in bags}) == 1
+        if len(tables) < 2 or not same:
+            for slot, (table, (off, idx, w)) in enumerate(zip(tables, bags)):
+                self.run_into(table, off, idx, w, send, send_flags, slot)
+            return
+        outs = [[send[g, 0, slot] for g in range(G)] for slot in range(len(tables))]
+        flags = [[send_flags[g, 0, slot:] for g in range(G)] for slot in range(len(tables))]
+        eb_group_scatter(tables, bags, outs, flags, ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
+
 
 class ShardedEmbeddingBags:
     """Table-wise sharded checked EmbeddingBag for a batch of `batch` samples over `num_tables` tables.
@@ -128,11 +142,16 @@ class ShardedEmbeddingBags:
         G, Bg, Tg, d = self.world, self.B // self.world, self.Tg, self.d
         send = torch.zeros((G, Bg, Tg, d), dtype=torch.float32, device=self.device)
         send_f = torch.zeros((G, Bg, Tg), dtype=torch.uint8, device=self.device)
-        for slot, t in enumerate(sorted(self.tables)):
-            off, idx, w = bags[t]
-            if len(off) != self.B + 1:
+        order = sorted(self.tables)
+        for t in order:
+            if len(bags[t][0]) != self.B + 1:
                 raise ValueError("ShardedEmbeddingBags: every table needs one bag per sample")
-            self.backend.run_into(self.tables[t], off, idx, w, send, send_f, slot)
+        if hasattr(self.backend, "run_all_into"):  # all local tables in one launch
+            self.backend.run_all_into([self.tables[t] for t in order], [bags[t] for t in order], send, send_f)
+        else:
+            for slot, t in enumerate(order):
+                off, idx, w = bags[t]
+                self.backend.run_into(self.tables[t], off, idx, w, send, send_f, slot)
         if G > 1:
             recv = torch.empty_like(send)
             recv_f = torch.empty_like(send_f)
