@@ -31,15 +31,23 @@ with torch.cuda.stream(s):
         L.call("abftlp_gemm_checked_batched", vp(a), nb, m, k, m * k, wb, vp(c), n + 1, m * (n + 1),
                C.c_void_p(c.data_ptr() + 4 * n), n + 1, m * (n + 1), vp(fl), m, vp(err), None, st)
 
+    c2 = torch.empty((nb, m, n), dtype=torch.int32, device=dev)  # aligned C (TMA epilogue), csum separate
+    cs2 = torch.empty((nb, m), dtype=torch.int32, device=dev)
+
+    def batched_aligned():
+        L.call("abftlp_gemm_checked_batched", vp(a), nb, m, k, m * k, wb, vp(c2), n, m * n, vp(cs2), 1, m, vp(fl), m,
+               vp(err), None, st)
+
     def separate():
         for t in range(nb):
             L.call("abftlp_gemm_checked", vp(a[t]), m, k, ws[t], vp(c[t]), n + 1, C.c_void_p(c[t].data_ptr() + 4 * n),
                    n + 1, vp(fl[t]), vp(err[t:t + 1]), None, st)
 
     batched()
+    batched_aligned()
     separate()
 graphs = {}
-for name, fn in (("batched", batched), ("separate", separate)):
+for name, fn in (("batched", batched), ("batched_aligned_C", batched_aligned), ("separate", separate)):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         fn()
