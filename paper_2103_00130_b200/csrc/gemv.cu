@@ -146,10 +146,15 @@ __global__ void __launch_bounds__(32 * kGemvWarps) gemv_checked_kernel(const Gem
                     p.flags[i] = static_cast<uint8_t>(flag);
                     p.csum[static_cast<int64_t>(i) * p.csum_ld] = csv;
                     p.row_acc[i] = 0ull;
-                    const unsigned long long prev = atomicAdd(p.err_pack, (1ull << 32) | static_cast<unsigned>(flag));
-                    if ((prev >> 32) + 1 == static_cast<unsigned long long>(p.m)) {
-                        *p.err_count = static_cast<uint32_t>(prev) + static_cast<uint32_t>(flag);
-                        *p.err_pack = 0ull;
+                    if (p.m == 1) {  // the only row: its finisher publishes the count (no second round trip)
+                        *p.err_count = static_cast<uint32_t>(flag);
+                    } else {
+                        const unsigned long long prev =
+                            atomicAdd(p.err_pack, (1ull << 32) | static_cast<unsigned>(flag));
+                        if ((prev >> 32) + 1 == static_cast<unsigned long long>(p.m)) {
+                            *p.err_count = static_cast<uint32_t>(prev) + static_cast<uint32_t>(flag);
+                            *p.err_pack = 0ull;
+                        }
                     }
                 }
             }
