@@ -416,7 +416,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 const int steps = unit_of(u).steps;
                 const int acc = local & 1;
                 const uint32_t aph = (local >> 1) & 1;
+#ifdef ABFT_TRACE_STEADY  // (debug: steady-state tile 8: how long the MMA waits for its accumulator)
+                if (trace && local == 8) trace[11] = globaltimer();
+#endif
                 mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef ABFT_TRACE_STEADY
+                if (trace && local == 8) trace[12] = globaltimer();
+#endif
                 tc_fence_after();
                 const uint32_t d = tmem + static_cast<uint32_t>(acc * BN);
                 for (int ks = 0; ks < steps; ++ks, ++it) {
@@ -425,7 +431,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     if (trace && local == 0 && ks == 0) trace[2] = globaltimer();
+#ifndef ABFT_TRACE_STEADY
                     if (trace && local == 0 && ks >= 1 && ks <= 3) trace[8 + ks] = globaltimer();  // stage arrivals
+#endif
                     const uint32_t a0 = smem_u32(smem + s * Cfg::kStageBytes);
                     const uint32_t b0 = a0 + KS * Cfg::kABytes;
 #pragma unroll
@@ -468,6 +476,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
+#ifdef ABFT_TRACE_STEADY
+            if (trace && local == 8 && threadIdx.x == 64) trace[9] = globaltimer();
+#endif
             const int n0 = nt * BN;
             const uint32_t t_row = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             // split-K exchange slot of this CTA's half tile (BN*128 int32): [BN/32 chunks][8 column quads]
@@ -644,7 +655,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                     // mainloop's operand reads): 16-byte stores when the row segment is aligned
                     if (row < p.m) {
                         int32_t* crow = cb + static_cast<int64_t>(row) * p.ldc + col0;
-                        if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+                        if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 31) == 0) {
+#pragma unroll
+                            for (int q8 = 0; q8 < 4; ++q8)  // 32-byte stores: full sectors (STG.256)
+                                asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + 8 * q8),
+                                             "r"(v[8 * q8]), "r"(v[8 * q8 + 1]), "r"(v[8 * q8 + 2]), "r"(v[8 * q8 + 3]),
+                                             "r"(v[8 * q8 + 4]), "r"(v[8 * q8 + 5]), "r"(v[8 * q8 + 6]), "r"(v[8 * q8 + 7])
+                                             : "memory");
+                        } else if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
 #pragma unroll
                             for (int q4 = 0; q4 < 8; ++q4)
                                 reinterpret_cast<uint4*>(crow)[q4] =
@@ -658,6 +676,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 }
             }
             if (trace && local == 0 && threadIdx.x == 64) trace[7] = globaltimer();
+#ifdef ABFT_TRACE_STEADY
+            if (trace && local == 8 && threadIdx.x == 64) trace[10] = globaltimer();
+            if (trace && local == 9 && threadIdx.x == 64) trace[13] = globaltimer();
+#endif
             if (pflag != nullptr && threadIdx.x == 64) *pflag = 0u;  // self-resetting for the next call
             // accumulator drained: let the MMA warp reuse it
             tc_fence_before();
