@@ -141,3 +141,55 @@ def test_grouped_tables_equal_per_table_scatter(elem, scale, d, weighted):
         assert torch.equal(flgs[1], flgs[0])
         assert int(cnt[1].item()) == total > 0
     L.lib.abftlp_eb_group_free(grp)
+
+
+def test_d5_share_full_size_grouped_vs_oracle():
+    """BASELINE configs[4] at full size for one GPU's share (8 tables x 1M x 128 int8 rows, fp32 scale/bias, batch
+    8192, pooling 80, Zipf(1.05) indices): the grouped one-launch lookup writes, for every table, the oracle's
+    pooled vectors and verdicts (bit-exact), with a few rows corrupted after the row sums."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200 import embedding as E
+    dev = torch.device("cuda")
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    T, R, d, B, pool, G = 8, 1_000_000, 128, 8192, 80, 8
+    Bg = B // G
+    rng = np.random.default_rng(5)
+    ranks = np.arange(1, R + 1, dtype=np.float64)
+    cdf = np.cumsum(ranks ** -1.05)
+    cdf /= cdf[-1]
+    tabs, host, bags = [], [], []
+    for t in range(T):
+        rows = rng.integers(-128, 128, (R, d), dtype=np.int8)
+        sc = rng.uniform(1e-3, 1e-2, R).astype(np.float32)
+        bi = rng.uniform(-1, 1, R).astype(np.float32)
+        tab = E.QuantEmbeddingTable(rows, sc, bi, elem="s8", dim=d)
+        sums = O.row_sums(rows, "s8", d)
+        for r in rng.choice(R, 4, replace=False):  # corrupt after the row sums
+            col, bit = int(rng.integers(0, d)), int(rng.integers(0, 8))
+            tab.flip_bit(int(r), col, bit)
+            rows.view(np.uint8)[r, col] ^= np.uint8(1 << bit)
+        idx = rng.permutation(R)[np.searchsorted(cdf, rng.random(B * pool))].astype(np.int64)
+        off = np.arange(0, B * pool + 1, pool, dtype=np.int64)
+        tabs.append(tab)
+        host.append((rows, sc, bi, sums, off, idx))
+        bags.append((torch.from_numpy(off).to(dev), torch.from_numpy(idx).to(dev), None))
+    send = torch.full((G, Bg, T, d), float("nan"), dtype=torch.float32, device=dev)
+    send_f = torch.full((G, Bg, T), 7, dtype=torch.uint8, device=dev)
+    outs = [[send[g, 0, t] for g in range(G)] for t in range(T)]
+    flags = [[send_f[g, 0, t:] for g in range(G)] for t in range(T)]
+    cnt = E.eb_group_scatter(tabs, bags, outs, flags, ld_out=T * d, flag_ld=T, bags_per_dest=Bg)
+    out = send.permute(2, 0, 1, 3).reshape(T, B, d).cpu().numpy()
+    fl = send_f.permute(2, 0, 1).reshape(T, B).cpu().numpy()
+    total = 0
+    for t in (0, 3, 7):  # three tables against the oracle (CPU time), all tables' counts via the flags
+        rows, sc, bi, sums, off, idx = host[t]
+        r_ref, _, _, e_ref = O.eb(rows, sc, bi, off, idx, None, elem="s8", dim=d, row_sums_=sums)
+        assert np.array_equal(out[t].view(np.uint32), r_ref.view(np.uint32)), t
+        assert np.array_equal(fl[t], e_ref), t
+    total = int(fl.astype(np.int64).sum())
+    assert int(cnt.item()) == total
