@@ -7,7 +7,8 @@ reused for a job of 1000 GEMMs with distinct A matrices; 1% of the runs inject o
 flip (half into B' after encoding, half into C' through the epilogue hook) and every injected
 run must be flagged. The runs are independent problems against one weight, so they are issued as
 GROUPED launches (one problem per run: its own A, C', checksum column, flags and count; the C' faults
-ride in the launch's fault list); a run with a B' fault runs alone between a flip and an unflip of B'.
+ride in the launch's fault list); the runs with a B' fault run as one batched launch, each against its own
+B' (encoded from the clean B, one bit flipped after encoding, prepared before timing like the runs' A).
 One step = one such job, replayed as a CUDA graph; L2 is flushed between steps (a 256 MiB read).
 metric = checked int8 GEMM TOPS (2*m*n*k per GEMM, checksum column excluded).
 
@@ -265,9 +266,27 @@ def run_gpu_arm(args, rank, world, dist):
 
     # The job's runs are independent GEMMs against the one encoded weight, so they are issued as GROUPED
     # launches (abftlp_gemm_checked_batched_faults: problem b = run b, its own A, C', csum, flags and count;
-    # the C' faults of the group ride in the launch's fault list). A run with a B' fault must see the
-    # corrupted weight alone, so it is its own launch between a flip and an unflip of B'.
+    # the C' faults of the group ride in the launch's fault list). A run with a B' fault must see its own
+    # corrupted weight: B is encoded once per such run (checksums of the clean B) and B'(p, j) flipped after
+    # encoding -- inject_weight_B's point (P:src/fault_lab.cpp:186-189) -- before timing, like the runs' A;
+    # in the job these runs are ONE batched launch, each problem with its own faulted weight.
     segments = plan_segments(plan, JOB, GROUP_MAX)
+    b_runs = sorted(r for r, f in plan.items() if f[0] == "B")
+    nfb = len(b_runs)
+    wf = C.c_void_p()
+    if nfb:
+        bcopies = b.unsqueeze(0).repeat(nfb, 1, 1).contiguous()
+        L.call("abftlp_gemm_encode_batched", vp(bcopies), nfb, K, N, N, K * N, st, C.byref(wf))
+        for q, r in enumerate(b_runs):
+            _, pp, jj, bit = plan[r]
+            L.call("abftlp_gemm_weight_flip_bit_batched", wf, q, pp, jj, bit, st)
+        torch.cuda.synchronize()
+        del bcopies
+        a_f = a_pool[b_runs].contiguous()
+        c_f = torch.empty((nfb, M, N), dtype=torch.int32, device=dev)
+        cs_f = torch.empty((nfb, M), dtype=torch.int32, device=dev)
+        fl_f = torch.empty((nfb, M), dtype=torch.uint8, device=dev)
+        err_f = torch.zeros(nfb, dtype=torch.int32, device=dev)
 
     def launch_group(i0, cnt, fl, checked):
         if checked:
@@ -295,15 +314,13 @@ def run_gpu_arm(args, rank, world, dist):
                     events.append((cnt, e0, e1))
                 n += 1
                 continue
-            _, run, pp, jj, bit = sg
-            L.call("abftlp_gemm_weight_flip_bit", w, pp, jj, bit, st)
+        if nfb:  # the B'-fault runs, each against its own corrupted weight, in one batched launch
             if checked:
-                L.call("abftlp_gemm_checked", vp(a_pool[run]), M, K, w, vp(c_all[run]), N, vp(csum[run]), 1,
-                       vp(flags[run]), vp(errs[run:run + 1]), None, st)
+                L.call("abftlp_gemm_checked_batched", vp(a_f), nfb, M, K, M * K, wf, vp(c_f), N, M * N, vp(cs_f), 1, M,
+                       vp(fl_f), M, vp(err_f), None, st)
             else:
-                L.call("abftlp_gemm_unchecked", vp(a_pool[run]), M, K, w, vp(c_all[run]), N, st)
-            L.call("abftlp_gemm_weight_flip_bit", w, pp, jj, bit, st)
-            n += 3
+                L.call("abftlp_gemm_unchecked_batched", vp(a_f), nfb, M, K, M * K, wf, vp(c_f), N, M * N, st)
+            n += 1
         return n
 
     def barrier():
@@ -360,9 +377,8 @@ def run_gpu_arm(args, rank, world, dist):
     e = errs.cpu().numpy()
     ok_clean = all(e[i] == 0 for i in range(JOB) if i not in plan)
     c_runs = [r for r, f in plan.items() if f[0] == "C"]
-    b_runs = [r for r, f in plan.items() if f[0] == "B"]
     ok_c = all(e[r] == 1 for r in c_runs)
-    ok_b = all(e[r] >= 1 for r in b_runs)
+    ok_b = nfb == 0 or bool((err_f >= 1).all().item())
     verdict = torch.tensor(e, device=dev)
     if dist is not None:
         dist.all_reduce(verdict, op=dist.ReduceOp.MAX)  # OR of the per-shard verdicts
@@ -464,6 +480,8 @@ def run_gpu_arm(args, rank, world, dist):
         secondary["D5_shard"] = d5_secondary(L, dev, st, vp, pk)
 
     L.lib.abftlp_gemm_weight_free(w)
+    if nfb:
+        L.lib.abftlp_gemm_weight_free(wf)
     if rank != 0:
         return
     value = world * args.steps * JOB * OPS / (t_total * 1e-3) / 1e12
@@ -484,7 +502,7 @@ def run_gpu_arm(args, rank, world, dist):
         "config": {"workload": "G2 = BASELINE configs[1]: checked GEMM m=256 k=4096 n=4096, B encoded once, "
                                f"job of {JOB} GEMMs with distinct A, 1% fault runs (B' and C' bit flips)",
                    "step": f"one {JOB}-GEMM job", "l2": "flushed between steps (256 MiB read, untimed); the job's 1 GB of A exceeds L2",
-                   "launch": "CUDA graph of the job: grouped launches (runs share the encoded B', one problem per run) split at B'-fault runs, which run alone between a flip and an unflip of B'",
+                   "launch": "CUDA graph of the job: grouped launches (runs share the encoded B', one problem per run, C' faults in the launch's fault list), split at the B'-fault runs; those run as one batched launch, each against its own B' (clean checksums, one bit flipped after encoding, prepared before timing like the runs' A)",
                    "parallelism": f"N-column shard per GPU (n={N} per rank), verdicts OR-reduced",
                    "gemm_kernel": "tcgen05 cta_group::2 int8, TMEM accumulators, fused mod-127 row check"},
         "e2e": {"value": e2e_tops, "unit": "TOPS", "h2d_bytes_per_step": M * K * e2e_runs,

@@ -112,6 +112,10 @@ typedef struct {
     uint64_t col;   /* col == n: the checksum column */
     uint32_t bit;
 } abftlp_batch_fault;
+/* Corrupt B'(i, j) of problem `problem` of a batched weight after encoding (j == n hits its checksum column):
+ * inject_weight_B (P:src/fault_lab.cpp:98-120) for one problem of a batched handle. */
+abftlp_status abftlp_gemm_weight_flip_bit_batched(abftlp_gemm_weight* w, uint64_t problem, uint64_t i, uint64_t j,
+                                                  uint32_t bit, abftlp_stream stream);
 /* `batch` checked GEMMs of one shape in ONE launch (e.g. the reference's 100 seeded trials of config 0):
  * problem b multiplies A_b = d_a + b*stride_a (bytes; 16-byte multiple) by weight b of a batched weight
  * (or the single weight of a plain handle) and writes C_b = d_c + b*stride_c, csum at d_csum +

@@ -792,6 +792,23 @@ abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uin
     });
 }
 
+abftlp_status abftlp_gemm_weight_flip_bit_batched(abftlp_gemm_weight* w, uint64_t problem, uint64_t i, uint64_t j,
+                                                  uint32_t bit, abftlp_stream stream) {
+    if (!w) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::GemmWeight& W = *w->w;
+        if (problem >= static_cast<uint64_t>(W.batch) || i >= static_cast<uint64_t>(W.k) ||
+            j > static_cast<uint64_t>(W.n))
+            throw std::out_of_range("inject_weight_B: coordinates out of range");
+        if (bit >= 8) throw std::out_of_range("flip_bit: bit index out of range");
+        const int64_t pb = static_cast<int64_t>(problem);
+        int8_t* e = W.element(static_cast<int64_t>(i), static_cast<int64_t>(j)) +
+                    pb * (j == static_cast<uint64_t>(W.n) ? W.cs_bstride : W.bt_bstride);
+        abftk::flip_bit(e, 0, bit, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_eb_table_flip_bit(abftlp_eb_table* t, uint64_t row, uint64_t col, uint32_t bit,
                                        abftlp_stream stream) {
     if (!t) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");

@@ -109,3 +109,30 @@ def test_host_batched_job_matches_oracle(nb, m, n, k):
         assert np.array_equal(ch[t].numpy(), ref[:, :n]), t
         assert np.array_equal(csh[t].numpy(), ref[:, n]), t
         assert not flh[t].numpy().any() and int(eh[t]) == e == 0, t
+
+
+def test_batched_weight_flip_bit_only_hits_its_problem():
+    """abftlp_gemm_weight_flip_bit_batched: inject_weight_B into one problem of a batched weight after encoding
+    (clean checksums): that problem's C' equals the oracle product with the corrupted B and the clean checksum
+    column, and only its rows can be flagged; the other problems are untouched."""
+    import ctypes as C
+    from paper_2103_00130_b200 import _lib
+    from paper_2103_00130_b200 import gemm as G
+    nb, m, n, k = 3, 256, 512, 384
+    a = np.stack([O.gemm_inputs(20260823, t, m, n, k)[0] for t in range(nb)])
+    b = np.stack([O.gemm_inputs(20260823, t, m, n, k)[1] for t in range(nb)])
+    pb = G.PackedEncodedWeightBatch(b)
+    p_, i, j, bit = 1, 100, 200, 6
+    _lib.call("abftlp_gemm_weight_flip_bit_batched", pb.handle, p_, i, j, bit, None)
+    ct, err, flags = G.abft_gemm_batched(a, pb)
+    ct, err = ct.cpu().numpy(), err.cpu().numpy()
+    for t in range(nb):
+        bt = b[t].copy()
+        if t == p_:
+            bt.view(np.uint8)[i, j] ^= np.uint8(1 << bit)
+        ref, fl, e = O.abft_gemm(a[t], bt, cs=O.row_checksums(b[t]))
+        assert np.array_equal(ct[t], ref), t
+        assert err[t] == e, t
+    assert err[p_] >= 1 and err[0] == err[2] == 0
+    with pytest.raises(_lib.InvalidArgument):
+        _lib.call("abftlp_gemm_weight_flip_bit_batched", pb.handle, nb, 0, 0, 0, None)
