@@ -593,6 +593,18 @@ abftlp_status abftlp_gemm_checked_host_batched(const uint8_t* a, uint64_t batch,
         ABFT_CUDA(cudaEventRecord(s.c_done[0], st));
         ABFT_CUDA(cudaStreamWaitEvent(s.h2d, s.c_done[0], 0));
         const uint64_t chunks = (batch + q - 1) / q;
+        // if anything below throws, copies already queued still reference the caller's host buffers: drain the
+        // three streams before the error reaches the caller
+        struct Drain {
+            cudaStream_t a, b, c;
+            bool armed = true;
+            ~Drain() {
+                if (!armed) return;
+                cudaStreamSynchronize(a);
+                cudaStreamSynchronize(b);
+                cudaStreamSynchronize(c);
+            }
+        } drain{s.h2d, st, s.d2h};
         for (uint64_t i = 0; i < chunks; ++i) {
             const int sl = static_cast<int>(i % 3);
             const uint64_t b0 = i * q, nb = std::min<uint64_t>(q, batch - b0);
@@ -642,6 +654,7 @@ abftlp_status abftlp_gemm_checked_host_batched(const uint8_t* a, uint64_t batch,
             ABFT_CUDA(cudaMemcpyAsync(err_count + b0, derr, nb * 4, cudaMemcpyDeviceToHost, s.d2h));
             ABFT_CUDA(cudaEventRecord(s.out_done[sl], s.d2h));
         }
+        drain.armed = false;
         ABFT_CUDA(cudaStreamSynchronize(s.d2h));
         ABFT_CUDA(cudaStreamSynchronize(st));
         return ABFTLP_OK;
