@@ -247,12 +247,21 @@ struct PairCfg {
     static constexpr int NA = BN == 64 ? ABFT_NA64 : ABFT_NA;  // TMA warps loading A (K split)
     static constexpr int NB = BN == 64 ? ABFT_NB64 : ABFT_NB;  // TMA warps loading B' (K split)
     static constexpr int kProducers = NA + NB;
-    static constexpr int kThreads = 32 * (5 + kProducers);   // producer 0, MMA, 4 epilogue, producers 1..
+#ifndef ABFT_EPI_WARPS
+#define ABFT_EPI_WARPS 4
+#endif
+    // epilogue warps: one group of 4 (one per TMEM lane quarter) or two groups splitting the tile's columns
+    static constexpr int kEpiWarps = ABFT_EPI_WARPS;
+    static constexpr int kEpiGroups = kEpiWarps / 4;
+    static_assert(kEpiWarps == 4 || kEpiWarps == 8, "4 or 8 epilogue warps");
+    // warps: producer 0, MMA, epilogue group 0 (4), producers 1.., epilogue group 1 (4, optional)
+    static constexpr int kThreads = 32 * (1 + 1 + kEpiWarps + (kProducers - 1));
+    static constexpr int kEpiG1 = 5 + kProducers;  // first warp of epilogue group 1
     static_assert(KS % NA == 0 && KS % NB == 0, "producer warps split the stage's k-blocks evenly");
     static constexpr int kABytes = kBM * kBK;                // per CTA per k-block (its 128 rows of A)
     static constexpr int kBBytes = (BN / 2) * kBK;           // per CTA per k-block (its half of the B' tile)
     static constexpr int kStageBytes = KS * (kABytes + kBBytes);
-    static constexpr int kStaging = 4 * kStagingBufs * 4096; // epilogue: 4 warps x bufs x (32 rows x 32 int32)
+    static constexpr int kStaging = kEpiWarps * kStagingBufs * 4096; // epilogue warps x bufs x (32 x 32 int32)
     static constexpr int kBarBytes = 512;
     static constexpr int kRawStages = (227 * 1024 - 1024 - kStaging - kBarBytes) / kStageBytes;
     static constexpr int kStages = kRawStages > 16 ? 16 : kRawStages;
@@ -314,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(&tempty[a], 2 * Cfg::kEpiWarps);  // epilogue warps x 2 CTAs
         }
         mbar_init(xbar, 1);
         fence_mbar_init();
@@ -331,7 +340,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     if (trace && threadIdx.x == 0) trace[1] = globaltimer();
     // warm L2 with this pair's first stages while the previous grid finishes (before griddep_wait:
     // prefetches only touch L2, the point of coherence); one producer warp per operand part
-    if ((warp == 0 || warp >= 6) && lane == 0 && pair < num_units) {
+    const bool is_producer = warp == 0 || (warp >= 6 && warp < Cfg::kEpiG1);
+    const bool is_epi = (warp >= 2 && warp <= 5) || warp >= Cfg::kEpiG1;
+    if (is_producer && lane == 0 && pair < num_units) {
         const int role = warp == 0 ? 0 : warp - 5;
         const Unit x = unit_of(pair);
         const int pre = x.steps < STAGES ? x.steps : STAGES;
@@ -348,12 +359,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         }
     }
     uint32_t tmem = 0;
-    if (warp >= 1 && warp <= 5) {
+    if (warp == 1 || is_epi) {
         if (warp == 1) {
             tmem_alloc_pair<Cfg::kTmemCols>(tmem_holder);
             tc_fence_before();
         }
-        named_bar_sync(2, 160);  // MMA warp + 4 epilogue warps
+        named_bar_sync(2, 32 * (1 + Cfg::kEpiWarps));  // MMA warp + epilogue warps
         tc_fence_after();
         tmem = *tmem_holder;
     }
@@ -365,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     if (CHECKED && p.gemv_helpers && pair >= num_units) {
         // ---------------- idle pair: checksum-column GEMV for every row (see gemv_helper)
         gemv_helper(p, (pair - num_units) * 2 + static_cast<int>(rank), (npairs - num_units) * 2);
-    } else if (warp == 0 || warp >= 6) {
+    } else if (is_producer) {
         // ---------------- TMA producers (both CTAs; completion counted on the leader's barrier). An SM
         // serves the TMA requests of ONE issuing warp one after another (~275-300 ns each under load,
         // scripts/pipe_bench9.cu), so the stage is split over three warps issuing in parallel:
@@ -456,6 +467,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
     } else {
         // ---------------- epilogue: warps 2..5, thread <-> one row of this CTA's 128-row half
         const int q = warp & 3;                  // TMEM lane quarter this warp may access
+        const int eg = warp >= Cfg::kEpiG1 ? 1 : 0;  // epilogue group: chunks c = eg, eg + kEpiGroups, ...
+        const int eslot = eg * 4 + q;                // this warp's staging buffers
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         int local = 0, chunk_ctr = 0;
         for (int u = pair; u < num_units; u += npairs, ++local) {
@@ -469,8 +482,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
             uint32_t cs_part = 0;
             if (CHECKED && x.kh == 0 && !p.gemv_helpers) {
-                const int kb0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
-                const int kb1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
+                const int t0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
+                const int t1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
+                const int kb0 = t0 + (t1 - t0) * eg / Cfg::kEpiGroups;  // the groups split the tile's share
+                const int kb1 = t0 + (t1 - t0) * (eg + 1) / Cfg::kEpiGroups;
                 if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, x.b, row, kb0 * kBK, min(kb1 * kBK, p.k));
             }
             mbar_wait(&tfull[acc], aph);
@@ -491,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 // upper-K unit: publish the partial tile through L2 and hand the tile to its partner
                 uint4* part = reinterpret_cast<uint4*>(p.partial + part_base);
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = eg; c < BN / 32; c += Cfg::kEpiGroups) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(t_row + c * 32, v);
                     tmem_wait_ld();
@@ -508,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                         mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc * 8));
                 }
                 __threadfence();
-                named_bar_sync(1, 128);
+                named_bar_sync(1, 32 * Cfg::kEpiWarps);
                 if (threadIdx.x == 64) {
                     st_release_gpu(pflag, 1u);
                     if (trace) trace[14] = globaltimer();
@@ -540,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
             int32_t* const cb = p.c + x.b * p.c_bstride;  // this problem's C
             long long rsum = 0;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = eg; c < BN / 32; c += Cfg::kEpiGroups) {
                 const int col0 = n0 + c * 32;
                 if (col0 >= p.n) break;  // warp-uniform
                 uint32_t v[32];
@@ -607,7 +622,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 }
                 if constexpr (EPI == kEpiTmaStore) {
                     constexpr int NB = Cfg::kStagingBufs;
-                    uint8_t* buf = staging + (q * NB + (chunk_ctr % NB)) * 4096;
+                    uint8_t* buf = staging + (eslot * NB + (chunk_ctr % NB)) * 4096;
                     if (chunk_ctr >= NB) {
                         if (lane == 0) bulk_wait_read<NB - 1>();
                         __syncwarp();
@@ -626,7 +641,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
                 } else if constexpr (EPI == kEpiStg) {
                     // transpose the warp's 32x32 chunk through its staging buffer so every store
                     // instruction writes four full 128-byte row segments
-                    uint8_t* buf = staging + q * Cfg::kStagingBufs * 4096;
+                    uint8_t* buf = staging + eslot * Cfg::kStagingBufs * 4096;
 #pragma unroll
                     for (int qq = 0; qq < 8; ++qq)
                         *reinterpret_cast<uint4*>(buf + lane * 128 + ((qq ^ (lane & 7)) << 4)) =
@@ -714,7 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThread
         if (trace && threadIdx.x == 64) trace[5] = globaltimer();
     }
 #ifdef ABFT_TRACE_ROLES  // (debug: when each non-epilogue warp reaches the final cluster barrier)
-    if (trace && lane == 0 && (warp == 0 || warp == 1 || warp >= 6))
+    if (trace && lane == 0 && (warp == 0 || warp == 1 || (warp >= 6 && warp <= 7)))
         trace[warp == 0 ? 9 : warp == 1 ? 10 : warp == 6 ? 11 : 12] = globaltimer();
 #endif
     tc_fence_before();
@@ -818,6 +833,7 @@ cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const C
     return launch_epi<64, false>(epi, pairs, a, b, c, p, st);
 }
 
+int gemm_epi_groups() { return PairCfg<64>::kEpiGroups; }  // row arrivals per tile (one per epilogue group)
 int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }
 int gemm_box_a(int bn) {  // k-blocks per A request
     return bn == 256 ? PairCfg<256>::KS / PairCfg<256>::NA : bn == 128 ? PairCfg<128>::KS / PairCfg<128>::NA

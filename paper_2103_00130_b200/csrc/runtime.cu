@@ -109,6 +109,7 @@ static unsigned long long* g_eb_trace = nullptr;  // debug: per-warp EmbeddingBa
 void set_eb_trace(unsigned long long* d_trace) { g_eb_trace = d_trace; }
 
 int gemm_ks(int bn);
+int gemm_epi_groups();
 int gemm_box_a(int bn);
 int gemm_box_b(int bn);
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
@@ -482,7 +483,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // checksum GEMV: the idle pairs compute it instead (gemv_helper). ABFTLP_GEMV_HELPERS=0 disables.
     const bool helpers_ok = !std::getenv("ABFTLP_GEMV_HELPERS") || std::atoi(std::getenv("ABFTLP_GEMV_HELPERS")) != 0;
     p.gemv_helpers = (checked && helpers_ok && n_tiles <= 4 && all_pairs - pairs >= pairs) ? 1 : 0;
-    p.row_arrivals = static_cast<int>(n_tiles) + p.gemv_helpers;
+    p.row_arrivals = static_cast<int>(n_tiles) * gemm_epi_groups() + p.gemv_helpers;
     if (p.gemv_helpers) pairs = all_pairs;
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
