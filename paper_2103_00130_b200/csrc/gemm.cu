@@ -213,7 +213,10 @@ __device__ void gemv_helper(const GemmParams& p, int helper_cta, int helper_ctas
 }
 
 // ============================================================ GEMM (CTA pairs)
-template <int BN>
+#ifndef ABFT_EPI_WARPS
+#define ABFT_EPI_WARPS 4
+#endif
+template <int BN, int EW = ABFT_EPI_WARPS>
 struct PairCfg {
     // k-blocks per pipeline stage. Measured on B200: an SM's TMA requests pipeline (issue ~50 ns each,
     // completions ~100-200 ns apart under full load), so what sustains ingest is BYTES IN FLIGHT, not
@@ -247,11 +250,8 @@ struct PairCfg {
     static constexpr int NA = BN == 64 ? ABFT_NA64 : ABFT_NA;  // TMA warps loading A (K split)
     static constexpr int NB = BN == 64 ? ABFT_NB64 : ABFT_NB;  // TMA warps loading B' (K split)
     static constexpr int kProducers = NA + NB;
-#ifndef ABFT_EPI_WARPS
-#define ABFT_EPI_WARPS 4
-#endif
     // epilogue warps: one group of 4 (one per TMEM lane quarter) or two groups splitting the tile's columns
-    static constexpr int kEpiWarps = ABFT_EPI_WARPS;
+    static constexpr int kEpiWarps = EW;
     static constexpr int kEpiGroups = kEpiWarps / 4;
     static_assert(kEpiWarps == 4 || kEpiWarps == 8, "4 or 8 epilogue warps");
     // warps: producer 0, MMA, epilogue group 0 (4), producers 1.., epilogue group 1 (4, optional)
@@ -271,11 +271,11 @@ struct PairCfg {
     static_assert(kBBytes % 1024 == 0 && kABytes % 1024 == 0, "SW128 tiles must stay 1024-byte aligned");
 };
 
-template <int BN, bool CHECKED, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN>::kThreads, 1)
+template <int BN, bool CHECKED, int EPI, int EW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
-    using Cfg = PairCfg<BN>;
+    using Cfg = PairCfg<BN, EW>;
     constexpr int STAGES = Cfg::kStages;
     constexpr int KS = Cfg::KS;
     extern __shared__ uint8_t smem_raw[];
@@ -785,11 +785,11 @@ __global__ void __launch_bounds__(256) verify_kernel(const int32_t* __restrict__
 }
 
 // ============================================================ host launchers
-template <int BN, bool CHECKED, int EPI>
+template <int BN, bool CHECKED, int EPI, int EW>
 static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                               const GemmParams& p, cudaStream_t st) {
-    using Cfg = PairCfg<BN>;
-    auto kern = gemm_pair_kernel<BN, CHECKED, EPI>;
+    using Cfg = PairCfg<BN, EW>;
+    auto kern = gemm_pair_kernel<BN, CHECKED, EPI, EW>;
     static bool attr_done = false;  // benign race: idempotent attribute set
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
@@ -811,29 +811,30 @@ static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap
 }
 
 template <int BN, bool CHECKED>
-static cudaError_t launch_epi(int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+static cudaError_t launch_epi(int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                               const GemmParams& p, cudaStream_t st) {
     switch (epi) {
-        case kEpiTmaStore: return launch_one<BN, CHECKED, kEpiTmaStore>(pairs, a, b, c, p, st);
-        case kEpiNone: return launch_one<BN, CHECKED, kEpiNone>(pairs, a, b, c, p, st);
-        case kEpiStg: return launch_one<BN, CHECKED, kEpiStg>(pairs, a, b, c, p, st);
-        default: return launch_one<BN, CHECKED, kEpiDirect>(pairs, a, b, c, p, st);
+        case kEpiTmaStore:  // 8 epilogue warps only with the TMA-store epilogue (short-K batched problems)
+            return ew == 8 ? launch_one<BN, CHECKED, kEpiTmaStore, 8>(pairs, a, b, c, p, st)
+                           : launch_one<BN, CHECKED, kEpiTmaStore, 4>(pairs, a, b, c, p, st);
+        case kEpiNone: return launch_one<BN, CHECKED, kEpiNone, 4>(pairs, a, b, c, p, st);
+        case kEpiStg: return launch_one<BN, CHECKED, kEpiStg, 4>(pairs, a, b, c, p, st);
+        default: return launch_one<BN, CHECKED, kEpiDirect, 4>(pairs, a, b, c, p, st);
     }
 }
 
-cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b,
+cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b,
                                const CUtensorMap& c, const GemmParams& p, cudaStream_t st) {
     if (checked) {
-        if (bn == 256) return launch_epi<256, true>(epi, pairs, a, b, c, p, st);
-        if (bn == 128) return launch_epi<128, true>(epi, pairs, a, b, c, p, st);
-        return launch_epi<64, true>(epi, pairs, a, b, c, p, st);
+        if (bn == 256) return launch_epi<256, true>(epi, ew, pairs, a, b, c, p, st);
+        if (bn == 128) return launch_epi<128, true>(epi, ew, pairs, a, b, c, p, st);
+        return launch_epi<64, true>(epi, ew, pairs, a, b, c, p, st);
     }
-    if (bn == 256) return launch_epi<256, false>(epi, pairs, a, b, c, p, st);
-    if (bn == 128) return launch_epi<128, false>(epi, pairs, a, b, c, p, st);
-    return launch_epi<64, false>(epi, pairs, a, b, c, p, st);
+    if (bn == 256) return launch_epi<256, false>(epi, ew, pairs, a, b, c, p, st);
+    if (bn == 128) return launch_epi<128, false>(epi, ew, pairs, a, b, c, p, st);
+    return launch_epi<64, false>(epi, ew, pairs, a, b, c, p, st);
 }
 
-int gemm_epi_groups() { return PairCfg<64>::kEpiGroups; }  // row arrivals per tile (one per epilogue group)
 int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }
 int gemm_box_a(int bn) {  // k-blocks per A request
     return bn == 256 ? PairCfg<256>::KS / PairCfg<256>::NA : bn == 128 ? PairCfg<128>::KS / PairCfg<128>::NA

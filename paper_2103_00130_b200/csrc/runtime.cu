@@ -109,7 +109,6 @@ static unsigned long long* g_eb_trace = nullptr;  // debug: per-warp EmbeddingBa
 void set_eb_trace(unsigned long long* d_trace) { g_eb_trace = d_trace; }
 
 int gemm_ks(int bn);
-int gemm_epi_groups();
 int gemm_box_a(int bn);
 int gemm_box_b(int bn);
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st);
@@ -483,9 +482,18 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // checksum GEMV: the idle pairs compute it instead (gemv_helper). ABFTLP_GEMV_HELPERS=0 disables.
     const bool helpers_ok = !std::getenv("ABFTLP_GEMV_HELPERS") || std::atoi(std::getenv("ABFTLP_GEMV_HELPERS")) != 0;
     p.gemv_helpers = (checked && helpers_ok && n_tiles <= 4 && all_pairs - pairs >= pairs) ? 1 : 0;
-    p.row_arrivals = static_cast<int>(n_tiles) * gemm_epi_groups() + p.gemv_helpers;
+    // Epilogue warps: 8 (two groups splitting each tile's columns, one row arrival each) when a batched
+    // launch's tiles have a short mainloop (k <= 1024) and the TMA-store epilogue, where the epilogue is
+    // the exposed part (G1: 26 -> 21 us per 100 trials); 4 otherwise (with long mainloops the extra warps
+    // slow the mainloop: grouped G2 2.9 -> 2.4 POPS). ABFTLP_GEMM_EW=4|8 overrides.
+    int ew = (nb > 1 && kb <= 8 && t.epi == kEpiTmaStore) ? 8 : 4;
+    if (const char* e = std::getenv("ABFTLP_GEMM_EW")) {
+        const int f = std::atoi(e);
+        if (f == 4 || (f == 8 && t.epi == kEpiTmaStore)) ew = f;
+    }
+    p.row_arrivals = static_cast<int>(n_tiles) * (ew / 4) + p.gemv_helpers;
     if (p.gemv_helpers) pairs = all_pairs;
-    cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
+    cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, ew, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
 }
 

@@ -120,7 +120,7 @@ void gen(void* d_out, int64_t count, uint64_t seed, uint64_t stream, uint64_t of
 void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
 
 // ---- launchers implemented in the .cu files
-cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int pairs, const CUtensorMap& a, const CUtensorMap& b,
+cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b,
                                const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st);
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st);

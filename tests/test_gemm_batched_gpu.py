@@ -136,3 +136,28 @@ def test_batched_weight_flip_bit_only_hits_its_problem():
     assert err[p_] >= 1 and err[0] == err[2] == 0
     with pytest.raises(_lib.InvalidArgument):
         _lib.call("abftlp_gemm_weight_flip_bit_batched", pb.handle, nb, 0, 0, 0, None)
+
+
+@pytest.mark.parametrize("ew", ["4", "8"])
+@pytest.mark.parametrize("nb,m,n,k", [(6, 64, 512, 512), (3, 256, 1024, 1024), (4, 130, 300, 1000)])
+def test_epilogue_warp_counts_bit_exact(nb, m, n, k, ew, monkeypatch):
+    """The checked epilogue with one group of 4 warps or two groups of 4 splitting each tile's columns (one row
+    arrival per group): identical C', checksum column, flags and counts, with C' faults on both sides."""
+    from paper_2103_00130_b200 import gemm as G
+    monkeypatch.setenv("ABFTLP_GEMM_EW", ew)
+    a = np.stack([O.gemm_inputs(20260823, t, m, n, k)[0] for t in range(nb)])
+    b = np.stack([O.gemm_inputs(20260823, t, m, n, k)[1] for t in range(nb)])
+    pb = G.PackedEncodedWeightBatch(b)
+    faults = [(0, m - 1, n, 3), (nb - 1, 1, n // 2, 30)]
+    for fl_ in (None, faults):
+        ct, err, flags = G.abft_gemm_batched(a, pb, faults=fl_) if fl_ else G.abft_gemm_batched(a, pb)
+        ct, err = ct.cpu().numpy(), err.cpu().numpy()
+        for t in range(nb):
+            ref, _, _ = O.abft_gemm(a[t], b[t])
+            ref = ref.copy()
+            for (p_, i, j, bit) in (fl_ or []):
+                if p_ == t:
+                    ref[i, j] = np.int32(np.uint32(ref[i, j].view(np.uint32) ^ np.uint32(1 << bit)).view(np.int32))
+            e_ref, _ = O.verify(ref)
+            assert np.array_equal(ct[t], ref), t
+            assert err[t] == e_ref, t
