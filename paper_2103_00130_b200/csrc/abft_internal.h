@@ -88,6 +88,9 @@ struct GemmParams {
     // contribute no GEMV share, and every row expects row_arrivals = n_tiles + 1 arrivals (n_tiles otherwise)
     int gemv_helpers;
     int row_arrivals;
+    // checksum column on the tensor cores: B' column n holds cs, the tile covering column n reads C'[:, n]
+    // from its accumulator, no GEMV share (n_tiles counts that tile)
+    int cs_mma;
     int32_t* partial;     // [num_tiles][2 CTAs][BN/32][32][128] int32 (split only)
     uint32_t* part_flag;  // [num_tiles * 2], self-resetting
     int32_t* c;

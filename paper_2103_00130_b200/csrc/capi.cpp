@@ -801,6 +801,10 @@ abftlp_status abftlp_gemm_weight_flip_bit(abftlp_gemm_weight* w, uint64_t i, uin
             throw std::out_of_range("inject_weight_B: coordinates out of range");
         if (bit >= 8) throw std::out_of_range("flip_bit: bit index out of range");
         abftk::flip_bit(W.element(static_cast<int64_t>(i), static_cast<int64_t>(j)), 0, bit, as_stream(stream));
+        if (j == static_cast<uint64_t>(W.n) && W.n < W.n_pad)  // the checksum column also lives in B' column n
+            abftk::flip_bit(W.bt + (static_cast<int64_t>(i) / abftk::kBK) * W.n_pad * abftk::kBK + W.n * abftk::kBK +
+                                static_cast<int64_t>(i) % abftk::kBK,
+                            0, bit, as_stream(stream));
         return ABFTLP_OK;
     });
 }
@@ -818,6 +822,10 @@ abftlp_status abftlp_gemm_weight_flip_bit_batched(abftlp_gemm_weight* w, uint64_
         int8_t* e = W.element(static_cast<int64_t>(i), static_cast<int64_t>(j)) +
                     pb * (j == static_cast<uint64_t>(W.n) ? W.cs_bstride : W.bt_bstride);
         abftk::flip_bit(e, 0, bit, as_stream(stream));
+        if (j == static_cast<uint64_t>(W.n) && W.n < W.n_pad)  // the checksum column also lives in B' column n
+            abftk::flip_bit(W.bt + pb * W.bt_bstride + (static_cast<int64_t>(i) / abftk::kBK) * W.n_pad * abftk::kBK +
+                                W.n * abftk::kBK + static_cast<int64_t>(i) % abftk::kBK,
+                            0, bit, as_stream(stream));
         return ABFTLP_OK;
     });
 }

@@ -66,15 +66,20 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
     if (tid < 64) {
         const long long s = part[0][tid] + part[1][tid] + part[2][tid] + part[3][tid];
         const int64_t p = p0 + tid;
-        cs[p] = p < k ? static_cast<int8_t>(mod127(s)) : static_cast<int8_t>(0);
+        const int8_t v = p < k ? static_cast<int8_t>(mod127(s)) : static_cast<int8_t>(0);
+        cs[p] = v;
+        if (n < n_pad) slab[n * kBK + tid] = v;  // the checksum column as B' column n: C'[:, n] on the tensor cores
     }
 }
 
 // Replace the checksum vector with caller-supplied values.
-__global__ void set_checksums_kernel(int8_t* __restrict__ cs, const int8_t* __restrict__ src, int64_t k) {
+__global__ void set_checksums_kernel(int8_t* __restrict__ cs, const int8_t* __restrict__ src, int64_t k,
+                                     int8_t* __restrict__ bt, int64_t n, int64_t n_pad) {
     for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < k;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         cs[p] = src[p];
+        if (n < n_pad) bt[(p / kBK) * n_pad * kBK + n * kBK + (p % kBK)] = src[p];  // B' column n mirrors cs
+    }
 }
 
 // Logical k x (n+1) view [B | cs] of an encoded weight (PackedEncodedWeight::at contract).
@@ -481,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             // This tile's share of the checksum column C'[row][n] = sum_p A[row][p]*cs[p]: K blocks
             // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
             uint32_t cs_part = 0;
-            if (CHECKED && x.kh == 0 && !p.gemv_helpers) {
+            if (CHECKED && x.kh == 0 && !p.gemv_helpers && !p.cs_mma) {
                 const int t0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
                 const int t1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
                 const int kb0 = t0 + (t1 - t0) * eg / Cfg::kEpiGroups;  // the groups split the tile's share
@@ -634,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (row0 < p.m) tma_store_3d(&tmC, buf, col0, row0, x.b);
+                        if (row0 < p.m && col0 < p.n) tma_store_3d(&tmC, buf, col0, row0, x.b);
                         bulk_commit();
                     }
                     ++chunk_ctr;
@@ -688,6 +693,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                                 if (col0 + j < p.n) crow[j] = static_cast<int32_t>(v[j]);
                         }
                     }
+                }
+            }
+            if constexpr (CHECKED) {
+                // C'[row][n] = A*cs computed by the tensor cores (B' column n) when this tile covers column n
+                if (p.cs_mma && eg == 0 && n0 <= p.n && p.n < n0 + BN) {
+                    cs_part = tmem_ld_32x32b_x1(t_row + static_cast<uint32_t>(p.n - n0));
+                    tmem_wait_ld();
                 }
             }
             if (trace && local == 0 && threadIdx.x == 64) trace[7] = globaltimer();
@@ -853,7 +865,7 @@ cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t s
 }
 
 cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t st) {
-    set_checksums_kernel<<<static_cast<unsigned>((w.k + 255) / 256), 256, 0, st>>>(w.cs, src, w.k);
+    set_checksums_kernel<<<static_cast<unsigned>((w.k + 255) / 256), 256, 0, st>>>(w.cs, src, w.k, w.bt, w.n, w.n_pad);
     return cudaGetLastError();
 }
 

@@ -177,6 +177,8 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
     if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
     if (batch < 1) throw std::invalid_argument("abftlp_gemm_encode: batch < 1");
     if (batch > 1 && b_bstride < ldb * (k - 1) + n) throw std::invalid_argument("abftlp_gemm_encode: batch stride too small");
+    // When n_pad > n, B' column n holds the checksum column (PackedEncodedWeight's [B | cs],
+    // P:src/gemm_abft.hpp:30-59), so a tile that covers it gets C'[:, n] from the tensor cores (GemmParams::cs_mma)
     const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, kRowAlign);
     const size_t per_bt = static_cast<size_t>(n_pad * k_pad);
     const size_t need_bt = per_bt * static_cast<size_t>(batch), need_cs = static_cast<size_t>(k_pad * batch);
@@ -253,7 +255,6 @@ static int64_t gemm_kb_split(int64_t kb, int ks) { return (kb + 1) / 2 + ks - 1 
 
 GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool c_tma_ok, bool fault) {
     (void)fault;
-    (void)checked;  // checked and unchecked run the same MMA tiles (the checksum column is a GEMV)
     const int pairs = std::max(1, device_sm_count() / 2);
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
     const int64_t kb = k_pad / kBK;
@@ -285,11 +286,19 @@ GemmTiling choose_tiling(int64_t m, int64_t n, int64_t k_pad, bool checked, bool
             const int64_t units = tiles * split;
             const int64_t waves = (units + pairs - 1) / pairs;
             const double kb_unit = split == 2 ? double(gemm_kb_split(kb, gemm_ks(bn))) : double(kb);
-            const double cost = waves * kb_unit * per_kb + (split == 2 ? 8000.0 + 8.0 * bn : 0.0) + drain;
+            // checked: a tile's CUDA-core GEMV share (kb / n_tiles k-blocks per row, ~1100 cycles each, run
+            // alongside the mainloop) unless the checksum column rides in the MMA (last tile has room, cs_mma)
+            const int64_t n_tiles = (n + bn - 1) / bn;
+            const double gemv = (checked && (split == 2 || n % bn == 0)) ? 1100.0 * double(kb) / double(n_tiles) : 0.0;
+            // + a fixed ~1.5 us per wave of tiles (first-stage latency and epilogue tail; measured: two half-
+            // empty waves of 64-wide tiles lose to one wave of 128-wide ones on the narrow D5 shards)
+            const double cost = waves * (std::max(kb_unit * per_kb, gemv) + 3000.0) +
+                                (split == 2 ? 8000.0 + 8.0 * bn : 0.0) + drain;
             if (cost < best_cost * 0.97) {
                 best_cost = cost;
                 best = {bn, epi, split};
             }
+
         }
     }
     return best;
@@ -409,8 +418,15 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (!d_c) t.epi = kEpiNone;  // requantized output only
 
     const int64_t m_tiles = (m + kPairM - 1) / kPairM;
-    const int64_t n_tiles = (w.n + t.bn - 1) / t.bn;
     const int64_t kb = w.k_pad / kBK;
+    // The checksum column C'[:, n] comes from the tensor cores (B' column n) when the last tile has room for it
+    // (no extra tile); otherwise the tiles' epilogues compute it as a GEMV share. ABFTLP_CS_MMA=0|1 overrides
+    // (1 adds a tile for column n when there is no room).
+    const int64_t n_tiles_plain = (w.n + t.bn - 1) / t.bn;
+    bool cs_mma = checked && t.split == 1 && w.n % t.bn != 0;  // implies n < n_pad: B' column n exists
+    if (const char* e = std::getenv("ABFTLP_CS_MMA"))
+        cs_mma = checked && t.split == 1 && std::atoi(e) != 0 && w.n < w.n_pad && w.n / t.bn < (w.n_pad + t.bn - 1) / t.bn;
+    const int64_t n_tiles = cs_mma ? (w.n + 1 + t.bn - 1) / t.bn : n_tiles_plain;
     if (nb * m_tiles * n_tiles * t.split > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
 
     if (checked && n_tiles > kMaxCheckedNTiles) throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
@@ -481,7 +497,8 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // Tall narrow shapes leave pairs idle while one or a few N tiles would each carry a large share of the
     // checksum GEMV: the idle pairs compute it instead (gemv_helper). ABFTLP_GEMV_HELPERS=0 disables.
     const bool helpers_ok = !std::getenv("ABFTLP_GEMV_HELPERS") || std::atoi(std::getenv("ABFTLP_GEMV_HELPERS")) != 0;
-    p.gemv_helpers = (checked && helpers_ok && n_tiles <= 4 && all_pairs - pairs >= pairs) ? 1 : 0;
+    p.cs_mma = cs_mma ? 1 : 0;
+    p.gemv_helpers = (checked && !cs_mma && helpers_ok && n_tiles <= 4 && all_pairs - pairs >= pairs) ? 1 : 0;
     // Epilogue warps: 8 (two groups splitting each tile's columns, one row arrival each) when a batched
     // launch's tiles have a short mainloop (k <= 1024) and the TMA-store epilogue, where the epilogue is
     // the exposed part (G1: 26 -> 21 us per 100 trials); 4 otherwise (with long mainloops the extra warps
