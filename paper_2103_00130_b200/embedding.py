@@ -221,8 +221,10 @@ def eb_group_scatter(tables: list, bags: list, out_dests: list, flag_dests: list
     nb = int(csr[0][0].numel()) - 1
     if any(int(o.numel()) - 1 != nb for o, _, _ in csr):
         raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "eb_group: every table needs the same bag count")
-    optrs = [torch.tensor([t.data_ptr() for t in od], dtype=torch.int64, device=dev) for od in out_dests]
-    fptrs = [torch.tensor([t.data_ptr() for t in fd], dtype=torch.int64, device=dev) for fd in flag_dests]
+    # destinations: tensors (their first element) or raw device addresses (e.g. peer GPUs' symmetric buffers)
+    addr = lambda t: t.data_ptr() if torch.is_tensor(t) else int(t)  # noqa: E731
+    optrs = [torch.tensor([addr(t) for t in od], dtype=torch.int64, device=dev) for od in out_dests]
+    fptrs = [torch.tensor([addr(t) for t in fd], dtype=torch.int64, device=dev) for fd in flag_dests]
     P = C.c_void_p
     arr = lambda xs: (P * T)(*xs)  # noqa: E731
     weights = None if csr[0][2] is None else arr([P(w.data_ptr()) for _, _, w in csr])

@@ -117,13 +117,40 @@ class GpuEbBackend:
         eb_group_scatter(tables, bags, outs, flags, ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
 
 
+class PeerExchange:
+    """The table-wise all-to-all fused into the lookups over NVLink peer memory: every rank's receive
+    buffers [G, B/G, Tg, d] (+ flags) live in symmetric memory, and rank r's grouped lookup kernel writes bag b of
+    its table slot s straight into destination rank g = b // (B/G)'s buffer at [r, b % (B/G), s] -- no send buffer,
+    no separate all-to-all; one device-side barrier orders the peers' writes before the consumer reads."""
+
+    def __init__(self, G: int, Bg: int, Tg: int, d: int, group, device):
+        import torch.distributed._symmetric_memory as symm
+        self.G, self.Bg, self.Tg, self.d = G, Bg, Tg, d
+        self.recv = symm.empty(G, Bg, Tg, d, dtype=torch.float32, device=device)
+        self.recv_f = symm.empty(G, Bg, Tg, dtype=torch.uint8, device=device)
+        name = (group or dist.group.WORLD).group_name
+        self.h = symm.rendezvous(self.recv, name)
+        self.hf = symm.rendezvous(self.recv_f, name)
+        self.rank = self.h.rank
+
+    def destinations(self, slot: int):
+        """Per destination rank g: the address of peer g's recv[rank, 0, slot] (pooled rows) and recv_f[...] (flags)."""
+        r, Bg, Tg, d = self.rank, self.Bg, self.Tg, self.d
+        outs = [int(p) + ((r * Bg) * Tg + slot) * d * 4 for p in self.h.buffer_ptrs]
+        flags = [int(p) + (r * Bg) * Tg + slot for p in self.hf.buffer_ptrs]
+        return outs, flags
+
+    def barrier(self):
+        self.h.barrier()
+
+
 class ShardedEmbeddingBags:
     """Table-wise sharded checked EmbeddingBag for a batch of `batch` samples over `num_tables` tables.
     `tables` maps this rank's table ids (t % G == rank) to their tables. Returns, for this rank's slice of
     the batch (samples [rank*B/G, (rank+1)*B/G)), pooled outputs [B/G, T, d] and verdicts [B/G, T]."""
 
     def __init__(self, tables: dict, num_tables: int, batch: int, dim: int, group=None, backend=None,
-                 device: torch.device | str | None = None):
+                 device: torch.device | str | None = None, exchange: str = "nccl"):
         self.group = group
         self.world, self.rank = _world(group)
         if batch % self.world:
@@ -136,16 +163,29 @@ class ShardedEmbeddingBags:
         self.backend = backend or GpuEbBackend()
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+        if exchange not in ("nccl", "peer"):
+            raise ValueError("ShardedEmbeddingBags: exchange must be 'nccl' or 'peer'")
+        # "peer": lookups write straight into the destination ranks' symmetric buffers (GPU backend only)
+        self.peer = PeerExchange(self.world, self.B // self.world, self.Tg, dim, group, self.device) \
+            if exchange == "peer" else None
 
     def __call__(self, bags: dict) -> tuple[torch.Tensor, torch.Tensor]:
         """bags[t] = (offsets[B+1], indices, weights-or-None) for every local table t."""
         G, Bg, Tg, d = self.world, self.B // self.world, self.Tg, self.d
-        send = torch.zeros((G, Bg, Tg, d), dtype=torch.float32, device=self.device)
-        send_f = torch.zeros((G, Bg, Tg), dtype=torch.uint8, device=self.device)
         order = sorted(self.tables)
         for t in order:
             if len(bags[t][0]) != self.B + 1:
                 raise ValueError("ShardedEmbeddingBags: every table needs one bag per sample")
+        if self.peer is not None:  # lookups + exchange in one grouped launch over peer memory
+            from .embedding import eb_group_scatter
+            dst = [self.peer.destinations(slot) for slot in range(len(order))]
+            self.peer.barrier()  # every peer has consumed its previous exchange before it is overwritten
+            eb_group_scatter([self.tables[t] for t in order], [bags[t] for t in order], [o for o, _ in dst],
+                             [f for _, f in dst], ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
+            self.peer.barrier()
+            return self._gather(self.peer.recv, self.peer.recv_f)
+        send = torch.zeros((G, Bg, Tg, d), dtype=torch.float32, device=self.device)
+        send_f = torch.zeros((G, Bg, Tg), dtype=torch.uint8, device=self.device)
         if hasattr(self.backend, "run_all_into"):  # all local tables in one launch
             self.backend.run_all_into([self.tables[t] for t in order], [bags[t] for t in order], send, send_f)
         else:
@@ -159,6 +199,11 @@ class ShardedEmbeddingBags:
             dist.all_to_all_single(recv_f, send_f, group=self.group)
         else:
             recv, recv_f = send, send_f
+        return self._gather(recv, recv_f)
+
+    def _gather(self, recv, recv_f):
+        """[G, B/G, Tg, d] received slots -> this rank's samples [B/G, T, d] in table order."""
+        G, Bg, d = self.world, self.B // self.world, self.d
         out = torch.empty((Bg, self.T, d), dtype=torch.float32, device=self.device)
         flags = torch.empty((Bg, self.T), dtype=torch.uint8, device=self.device)
         for g in range(G):

@@ -193,3 +193,44 @@ def test_d5_share_full_size_grouped_vs_oracle():
         assert np.array_equal(fl[t], e_ref), t
     total = int(fl.astype(np.int64).sum())
     assert int(cnt.item()) == total
+
+
+def test_peer_exchange_world1_matches_oracle():
+    """ShardedEmbeddingBags(exchange="peer"): the grouped lookup kernel writes straight into the ranks' symmetric
+    receive buffers (peer memory over NVLink at world > 1; the rank's own buffer here, world size 1 -- the only
+    GPU count this run has), then a device-side barrier. Identical to the oracle and to the NCCL-exchange path."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2103_00130_b200 import embedding as E
+    from paper_2103_00130_b200 import sharded as S
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        T, B, d = 4, 16, 128
+        tables, bags, refs = {}, {}, {}
+        for t in range(T):
+            rows, sc, bi, tab = _table(E, "s8", 2000, d, 60 + t)
+            rng = np.random.default_rng(70 + t)
+            off = np.concatenate([[0], np.cumsum(rng.integers(0, 40, B))]).astype(np.int64)
+            idx = rng.integers(0, 2000, off[-1]).astype(np.int64)
+            tables[t], bags[t] = tab, (off, idx, None)
+            refs[t] = O.eb(rows, sc, bi, off, idx, None, elem="s8", dim=d)
+        try:
+            peer = S.ShardedEmbeddingBags(tables, T, B, d, exchange="peer")
+        except RuntimeError as e:  # symmetric memory unavailable on this driver / box
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        for _ in range(2):  # the exchange buffers are reused call to call
+            out, flags = peer(bags)
+            for t in range(T):
+                assert np.array_equal(out[:, t].cpu().numpy().view(np.uint32), refs[t][0].view(np.uint32))
+                assert np.array_equal(flags[:, t].cpu().numpy(), refs[t][3])
+        out2, flags2 = S.ShardedEmbeddingBags(tables, T, B, d)(bags)
+        assert torch.equal(out.view(torch.int32), out2.view(torch.int32)) and torch.equal(flags, flags2)
+    finally:
+        dist.destroy_process_group()
