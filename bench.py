@@ -815,6 +815,21 @@ def eb_secondary(L, dev, st, vp, pk):
                 if s >= 2:
                     ts.append(e0.elapsed_time(e1) * 1e3)
             res[checked] = statistics.median(ts)
+        # steady state: 20 batches back to back (programmatic dependent launch overlaps launch and tail)
+        def b2b():
+            for _ in range(20):
+                L.call("abftlp_eb_checked", tab, vp(off), vp(ix), nb, vp(wts) if wts is not None else None, vp(o), d,
+                       vp(fl), None, None, None, None, st)
+        b2b()
+        L.call("abftlp_l2_flush", vp(fb), fb.numel(), 77, st)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b2b()
+        e1.record()
+        torch.cuda.synchronize()
+        b2b_us = e0.elapsed_time(e1) * 1e3 / 20
         # random-gather floor of the same lookups (abftlp_gather_probe): every looked-up record read once with
         # maximal memory-level parallelism and no arithmetic, L2 flushed -- the practical roof for these batches
         rec = 128 if row_b > 64 else 64  # E3: the 128-B rows; E4: the table's packed 64-B row+meta records
@@ -838,6 +853,8 @@ def eb_secondary(L, dev, st, vp, pk):
                      "hbm_frac": gbs / pk["hbm_gbs"], "overhead_pct": 100 * (res[True] - res[False]) / res[False],
                      "lookups": L_, "bags": nb, "injected_row_faults": n_faults, "flagged_bags": flagged,
                      "gather_floor_us": floor_us, "frac_of_gather_floor": floor_us / res[True],
+                     "checked_us_back_to_back": b2b_us,
+                     "b2b_how": "20 batches back to back on one stream (same bags), after one L2 flush",
                      "gather_floor_how": f"abftlp_gather_probe: the {L_} looked-up {rec}-B records, L2 flushed"}
         del rows, sc, bi, off, ix, o, fl, fb
         torch.cuda.empty_cache()

@@ -231,3 +231,17 @@ def test_many_bags_per_group_bit_exact(E, elem, scale, d, weighted, wpb, monkeyp
     out, flags, rsum, csum, cnt = E.eb_csr(t, off, idx, w)
     assert_same(out, flags, rsum, csum, ref)
     assert int(cnt.item()) == int(ref[3].sum()) > 0
+
+
+def test_gather_probe_runs_and_validates(E):
+    """abftlp_gather_probe (the bench's random-gather roof): runs on a table and rejects bad record sizes."""
+    import ctypes as C
+    from paper_2103_00130_b200 import _lib
+    tab = torch.zeros((1000, 64), dtype=torch.uint8, device="cuda")
+    idx = torch.randint(0, 1000, (5000,), dtype=torch.int64, device="cuda")
+    sink = torch.zeros(1, dtype=torch.int32, device="cuda")
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.call("abftlp_gather_probe", vp(tab), 64, vp(idx), 5000, vp(sink), None)
+    torch.cuda.synchronize()
+    with pytest.raises(_lib.InvalidArgument):
+        _lib.call("abftlp_gather_probe", vp(tab), 24, vp(idx), 5000, vp(sink), None)
