@@ -35,6 +35,9 @@ typedef struct abftlp_gemm_weight_s abftlp_gemm_weight;
 abftlp_status abftlp_gemm_encode(const int8_t* d_b, uint64_t k, uint64_t n, uint64_t ldb,
                                  abftlp_stream stream, abftlp_gemm_weight** out);
 void abftlp_gemm_weight_free(abftlp_gemm_weight* w);
+/* Re-encode a single-weight handle in place from a new B of the same k x n (e.g. after a weight update):
+ * no allocation, asynchronous on `stream`; calls in flight on other streams must be ordered by the caller. */
+abftlp_status abftlp_gemm_reencode(abftlp_gemm_weight* w, const int8_t* d_b, uint64_t ldb, abftlp_stream stream);
 /* PackedEncodedWeight::k()/n() (P:src/gemm_abft.hpp:37-38). */
 abftlp_status abftlp_gemm_weight_dims(const abftlp_gemm_weight* w, uint64_t* k, uint64_t* n);
 /* Copies WeightChecksum::values (k int8) to d_cs. */

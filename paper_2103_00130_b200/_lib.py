@@ -120,6 +120,7 @@ _SIGS = {
     "abftlp_gemm_checked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, vp]),
     "abftlp_gemm_checked_host_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, vp, u64, vp, vp]),
     "abftlp_gemm_weight_flip_bit_batched": (i32, [vp, u64, u64, u64, u32, vp]),
+    "abftlp_gemm_reencode": (i32, [vp, vp, u64, vp]),
     "abftlp_gemm_checked_batched_faults": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, u64, vp]),
     "abftlp_gemm_unchecked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp]),
     "abftlp_gemm_checked_requant": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),

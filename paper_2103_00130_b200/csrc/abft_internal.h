@@ -37,6 +37,7 @@ struct GemmWeight {
     int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad >= n
     int8_t* bt = nullptr;          // k_pad/128 x n_pad x 128
     int8_t* cs = nullptr;          // k_pad (WeightChecksum::values, each in [0,126]; zero pad)
+    int32_t* cs_acc = nullptr;     // k_pad x batch encoder scratch: per-row sums of column-block residues (zeroed)
     bool owns = true;
     size_t bt_cap = 0, cs_cap = 0;  // allocation capacities (campaign scratch re-encodes in place)
     int64_t batch = 1;              // independent weights stored back to back (batched GEMM)

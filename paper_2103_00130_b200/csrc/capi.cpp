@@ -278,6 +278,16 @@ abftlp_status abftlp_gemm_encode(const int8_t* d_b, uint64_t k, uint64_t n, uint
     });
 }
 
+abftlp_status abftlp_gemm_reencode(abftlp_gemm_weight* w, const int8_t* d_b, uint64_t ldb, abftlp_stream stream) {
+    if (!w || !d_b) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::GemmWeight& W = *w->w;
+        if (W.batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
+        abftk::encode_weight_into(W, d_b, W.k, W.n, static_cast<int64_t>(ldb), as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_gemm_encode_batched(const int8_t* d_b, uint64_t batch, uint64_t k, uint64_t n, uint64_t ldb,
                                          uint64_t stride_b, abftlp_stream stream, abftlp_gemm_weight** out) {
     if (!out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");

@@ -72,6 +72,58 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
     }
 }
 
+// 2-D encoder (the one above walks every column of a 64-row slab in one block: 64 blocks for k = 4096, ~150 GB/s):
+// one block per 64 x 64 tile of B -- coalesced 16-byte loads, a shared-memory transpose into B'[kb][j][p % 128]
+// (16-byte stores), and each row's partial sum over the tile's 64 columns reduced mod 127 and added to cs_acc[p]
+// (the residue of a sum is the sum of the residues: P:src/gemm_abft.cpp:60-71 reduces the int64 row sum once).
+// encode_finalize_kernel then writes cs (and B' column n) and re-zeroes cs_acc.
+__global__ void __launch_bounds__(256) encode_tiles_kernel(const int8_t* __restrict__ b, int64_t k, int64_t n,
+                                                           int64_t ldb, int8_t* __restrict__ bt, int64_t n_pad,
+                                                           int32_t* __restrict__ cs_acc) {
+    __shared__ __align__(16) int8_t tile[64][64 + 16];
+    const int tid = threadIdx.x;
+    const int64_t p0 = static_cast<int64_t>(blockIdx.y) * 64, j0 = static_cast<int64_t>(blockIdx.x) * 64;
+    {
+        const int r = tid >> 2, q = tid & 3;  // row r, 16-byte segment q
+        const int64_t p = p0 + r, j = j0 + 16 * q;
+        alignas(16) int8_t v[16];
+        const int8_t* src = b + p * ldb + j;
+        if (p < k && j + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = (p < k && j + e < n) ? src[e] : static_cast<int8_t>(0);
+        }
+        *reinterpret_cast<uint4*>(&tile[r][16 * q]) = *reinterpret_cast<const uint4*>(v);
+        int s = 0;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) s += v[e];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (q == 0 && p < k && j0 < n) atomicAdd(&cs_acc[p], mod127(s));
+    }
+    __syncthreads();
+    {
+        const int c = tid >> 2, q = tid & 3;  // column c, rows [16 q, 16 q + 16)
+        alignas(16) int8_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = tile[16 * q + e][c];
+        int8_t* dst = bt + (p0 / kBK) * n_pad * kBK + (j0 + c) * kBK + (p0 % kBK) + 16 * q;
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+    }
+}
+
+__global__ void encode_finalize_kernel(int32_t* __restrict__ cs_acc, int8_t* __restrict__ cs, int8_t* __restrict__ bt,
+                                       int64_t k, int64_t k_pad, int64_t n, int64_t n_pad) {
+    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < k_pad;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int8_t v = p < k ? static_cast<int8_t>(cs_acc[p] % 127) : static_cast<int8_t>(0);
+        cs[p] = v;
+        if (n < n_pad) bt[(p / kBK) * n_pad * kBK + n * kBK + (p % kBK)] = v;  // checksum column as B' column n
+        cs_acc[p] = 0;
+    }
+}
+
 // Replace the checksum vector with caller-supplied values.
 __global__ void set_checksums_kernel(int8_t* __restrict__ cs, const int8_t* __restrict__ src, int64_t k,
                                      int8_t* __restrict__ bt, int64_t n, int64_t n_pad) {
@@ -870,7 +922,16 @@ cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t 
 }
 
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st) {
-    encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs);
+    if (!w.cs_acc) {  // (handles without encoder scratch)
+        encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs);
+        return cudaGetLastError();
+    }
+    const dim3 grid(static_cast<unsigned>(w.n_pad / 64), static_cast<unsigned>(w.k_pad / 64));
+    encode_tiles_kernel<<<grid, 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs_acc);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    encode_finalize_kernel<<<static_cast<unsigned>((w.k_pad + 255) / 256), 256, 0, st>>>(w.cs_acc, w.cs, w.bt, k,
+                                                                                         w.k_pad, n, w.n_pad);
     return cudaGetLastError();
 }
 

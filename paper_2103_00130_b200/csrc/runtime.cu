@@ -187,11 +187,15 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
             cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
             cudaFree(w.bt);
             cudaFree(w.cs);
+            cudaFree(w.cs_acc);
             w.bt = nullptr;
             w.cs = nullptr;
+            w.cs_acc = nullptr;
         }
         cuda_check(cudaMalloc(&w.bt, need_bt), "cudaMalloc(B')");
         cuda_check(cudaMalloc(&w.cs, need_cs), "cudaMalloc(cs)");
+        cuda_check(cudaMalloc(&w.cs_acc, need_cs * sizeof(int32_t)), "cudaMalloc(cs scratch)");
+        cuda_check(cudaMemsetAsync(w.cs_acc, 0, need_cs * sizeof(int32_t), st), "cudaMemsetAsync(cs scratch)");
         w.bt_cap = need_bt;
         w.cs_cap = need_cs;
     }
@@ -206,6 +210,7 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
         GemmWeight one = w;
         one.bt = w.bt + b * w.bt_bstride;
         one.cs = w.cs + b * w.cs_bstride;
+        one.cs_acc = w.cs_acc + b * w.cs_bstride;
         cuda_check(launch_encode_weight(d_b + b * b_bstride, k, n, ldb, one, st), "encode_weight_kernel");
     }
     for (int bn : {64, 128, 256})
@@ -240,6 +245,7 @@ void free_weight(GemmWeight* w) {
     if (w->owns) {
         cudaFree(w->bt);
         cudaFree(w->cs);
+        cudaFree(w->cs_acc);
     }
     delete w;
 }
