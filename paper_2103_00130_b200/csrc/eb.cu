@@ -513,7 +513,11 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
         EbParams tv = p;
         int64_t lb = bag;  // bag index within its table
         if (p.tables) {
-            const int64_t t = bag / p.bags_per_table;
+            // 32-bit division when the launch's bag ids fit (a 64-bit divide is a ~40-instruction sequence
+            // on the per-bag path)
+            const int64_t t = p.num_bags <= 0xFFFFFFFFll
+                                  ? static_cast<int64_t>(static_cast<uint32_t>(bag) / static_cast<uint32_t>(p.bags_per_table))
+                                  : bag / p.bags_per_table;
             lb = bag - t * p.bags_per_table;
             const EbTableDesc& dsc = p.tables[t];
             tv.data = dsc.data;
@@ -704,21 +708,28 @@ __global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, 
                 umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
                 sm = __dadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, o));
             }
-            if (lane == 0) {
-                part_sum[warp] = sm;
-                part_emax[warp] = emax;
-                part_umin[warp] = umin;
+            if constexpr (WPB > 1) {
+                if (lane == 0) {
+                    part_sum[warp] = sm;
+                    part_emax[warp] = emax;
+                    part_umin[warp] = umin;
+                }
             }
             // only the WPB warps of this bag synchronise (their slices and outputs are complete)
             group_sync();
             if (slice == 0) {
-                int E = -100000, U = 100000;
-                double exact = 0.0;
+                int E = emax, U = umin;  // WPB == 1: the warp's own reduction, no shared-memory round trip
+                double exact = sm;
+                if constexpr (WPB > 1) {
+                    E = -100000;
+                    U = 100000;
+                    exact = 0.0;
 #pragma unroll
-                for (int s2 = 0; s2 < WPB; ++s2) {
-                    E = max(E, part_emax[warp + s2]);
-                    U = min(U, part_umin[warp + s2]);
-                    exact = __dadd_rn(exact, part_sum[warp + s2]);
+                    for (int s2 = 0; s2 < WPB; ++s2) {
+                        E = max(E, part_emax[warp + s2]);
+                        U = min(U, part_umin[warp + s2]);
+                        exact = __dadd_rn(exact, part_sum[warp + s2]);
+                    }
                 }
                 double rsum;
                 if (E == -100000) {
