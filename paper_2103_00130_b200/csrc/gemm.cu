@@ -178,7 +178,9 @@ __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int b, int r
 __device__ __forceinline__ void row_arrive(const GemmParams& p, int b, int row, unsigned long long add, int& fin,
                                            int& flag) {
     unsigned long long* racc = p.row_acc + static_cast<int64_t>(b) * p.m + row;
-    const unsigned long long v = atomicAdd(racc, add) + add;
+    // a row with one contribution (one N tile, checksum in the same tile) is complete here: no round trip
+    const bool sole = p.row_arrivals == 1;
+    const unsigned long long v = sole ? add : atomicAdd(racc, add) + add;
     if (((v >> kRowAccCountShift) & kRowAccCountMask) == static_cast<unsigned long long>(p.row_arrivals)) {
         fin = 1;
         int32_t csv = static_cast<int32_t>(static_cast<uint32_t>(v >> 32));
@@ -189,7 +191,7 @@ __device__ __forceinline__ void row_arrive(const GemmParams& p, int b, int row, 
         flag = static_cast<int32_t>(res) != mod127(csv);
         p.flags[b * p.flags_bstride + row] = static_cast<uint8_t>(flag);
         p.csum[b * p.csum_bstride + static_cast<int64_t>(row) * p.csum_ld] = csv;
-        *racc = 0ull;  // self-resetting workspace
+        if (!sole) *racc = 0ull;  // self-resetting workspace (a sole arrival never touched it)
     }
 }
 // (finished rows) << 32 | (flagged rows) per warp on the problem's word; the call's last finished row publishes
