@@ -253,3 +253,24 @@ def test_gemv_helpers_tall_narrow_bit_exact(G, m, n, k, monkeypatch):
         for col in (n // 2, n):
             bad = G.abft_gemm(a, pb, fault=(m - 1, col, 17))
             assert bad.errCount == 1 and int(bad.rowFlags[m - 1].item()) == 1
+
+
+@pytest.mark.parametrize("m,n,k", [(8192, 64, 512), (1000, 100, 640), (300, 127, 1300)])
+def test_single_tile_rows_bit_exact_and_workspace_clean(G, m, n, k, monkeypatch):
+    """One N tile with the checksum column in the same tile (BN=128): each row has one contribution and is
+    finalized without the row atomic. Verdicts with faults on both sides of the checksum column, repeated
+    calls, and a following multi-tile call (which uses the shared per-row workspace) all stay exact."""
+    monkeypatch.setenv("ABFTLP_GEMM_TILING", "128")
+    a, b = rnd(7 * m + n + k, m, n, k)
+    pb = G.PackedEncodedWeight(b)
+    ct, fl, err = O.abft_gemm(a, b)
+    for _ in range(2):
+        res = G.abft_gemm(a, pb)
+        assert np.array_equal(res.cTemp.data.cpu().numpy(), ct) and res.errCount == err == 0
+    for row, col in ((0, n), (m - 1, n // 2), (m // 2, 0)):
+        bad = G.abft_gemm(a, pb, fault=(row, col, 7))
+        flags = bad.rowFlags.cpu().numpy()
+        assert bad.errCount == 1 and flags[row] == 1 and int(flags.sum()) == 1
+    monkeypatch.setenv("ABFTLP_GEMM_TILING", "64")  # n > 64: several tiles per row, row atomics again
+    a2, b2 = rnd(m + 1, m, 2 * n, k)
+    check_against_oracle(G, a2, b2)
