@@ -104,27 +104,77 @@ __global__ void __launch_bounds__(128) cpa_kernel(const unsigned char* __restric
     atomicAdd(out, acc);
 }
 
+
+template <int S>
+__global__ void __launch_bounds__(128) bulk_kernel(const unsigned char* __restrict__ tab, const int* __restrict__ idx,
+                                                   long long n, unsigned long long* out) {
+    extern __shared__ __align__(1024) unsigned char dyn[];
+    __shared__ __align__(8) unsigned long long bar[4][S];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* buf = dyn + w * S * 4096;
+    if (lane < S) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&bar[w][lane])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    unsigned long long acc = 0;
+    const long long gw = (long long)blockIdx.x * 4 + w, nw = (long long)gridDim.x * 4;
+    const long long nch = (n + 31) / 32;
+    auto issue = [&](long long ch, int slot) {
+        const long long c = ch * 32;
+        const int ix = c + lane < n ? idx[c + lane] : 0;
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[w][slot])), "r"(32 * 128)
+                         : "memory");
+        __syncwarp();
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                     ::"r"(smem_u32(buf + slot * 4096 + lane * 128)), "l"(tab + (long long)ix * 128),
+                       "r"(smem_u32(&bar[w][slot]))
+                     : "memory");
+    };
+    int k = 0;
+    for (int s = 0; s < S - 1; ++s)
+        if (gw + s * nw < nch) issue(gw + s * nw, s);
+    unsigned phases = 0;
+    for (long long ch = gw; ch < nch; ch += nw, ++k) {
+        const long long nx = ch + (S - 1) * nw;
+        if (nx < nch) issue(nx, (k + S - 1) % S);
+        const int slot = k % S;
+        asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+                         smem_u32(&bar[w][slot])),
+                     "r"((phases >> slot) & 1u)
+                     : "memory");
+        phases ^= 1u << slot;
+        const unsigned char* row = buf + slot * 4096 + lane * 128;
+        unsigned s = 0;
+        for (int e = 0; e < 128; e += 4) s += *reinterpret_cast<const unsigned*>(row + ((e + 4 * lane) & 127)) & 0xFFu;
+        if (ch * 32 + lane < n) acc += s;
+        __syncwarp();
+    }
+    atomicAdd(out, acc);
+}
+
 template <int S>
 void run(const CUtensorMap& m, unsigned char* tab, int* idx, long long n, unsigned long long* out, int bps,
          unsigned long long ref) {
     const int smem = 4 * S * 4096;
     cudaFuncSetAttribute(g4_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(cpa_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(bulk_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int kind = 0; kind < 2; ++kind) {
+    for (int kind = 0; kind < 3; ++kind) {
         float best = 1e30f; unsigned long long got = 0;
         for (int rep = 0; rep < 4; ++rep) {
             cudaMemset(out, 0, 8);
             cudaEventRecord(e0);
             if (kind == 0) g4_kernel<S><<<148 * bps, 128, smem>>>(m, idx, n, out);
-            else cpa_kernel<S><<<148 * bps, 128, smem>>>(tab, idx, n, out);
+            else if (kind == 1) cpa_kernel<S><<<148 * bps, 128, smem>>>(tab, idx, n, out);
+            else bulk_kernel<S><<<148 * bps, 128, smem>>>(tab, idx, n, out);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             if (rep && ms < best) best = ms;
             cudaMemcpy(&got, out, 8, cudaMemcpyDeviceToHost);
         }
-        printf("S=%d bps=%d %s: %.2f us %.2f TB/s %s (%s)\n", S, bps, kind == 0 ? "gather4" : "cp.async", best * 1e3,
+        printf("S=%d bps=%d %s: %.2f us %.2f TB/s %s (%s)\n", S, bps, kind == 0 ? "gather4" : kind == 1 ? "cp.async" : "bulk1d", best * 1e3,
                n * 128.0 / (best * 1e-3) / 1e12, got == ref ? "OK" : "MISMATCH", cudaGetErrorString(cudaGetLastError()));
     }
 }
