@@ -451,8 +451,12 @@ __device__ __forceinline__ unsigned long long decode_pair_bits(W w, int c) {
     }
 }
 
+#ifndef ABFT_EB_MINB_SMALL
+#define ABFT_EB_MINB_SMALL 2  // resident blocks per SM asked of ptxas for 32-byte slices (E4-class rows)
+#endif
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
-__global__ void __launch_bounds__(256, 2) eb_bag_async_kernel(const EbParams p, int log2d) {
+__global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? ABFT_EB_MINB_SMALL : 2)
+    eb_bag_async_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
     constexpr int SLICE = 32 * BPL;        // bytes of a row this warp needs
     constexpr int PIECES = SLICE / 16;     // 16-B copies per row slice
