@@ -114,3 +114,24 @@ def test_python_layer_refuses_cpu_tensors_without_gpu():
     from paper_2103_00130_b200 import gemm
     with pytest.raises(RuntimeError, match="CUDA"):
         gemm.PackedEncodedWeight([[1, 2], [3, 4]])
+
+
+def test_new_device_entry_points_reject_null_arguments():
+    """The grouped-job, grouped-table and probe entry points validate their arguments before any device
+    work (the reference's guarded() convention: -1 and "null argument" / the reason in last_error)."""
+    vp = C.c_void_p
+    assert L.lib.abftlp_eb_group_create(None, 0, None, None, None, None, None, None) == L.ERR_INVALID_ARGUMENT
+    assert "null argument" in L.last_error()
+    g = vp()
+    tabs = (vp * 1)(None)
+    assert L.lib.abftlp_eb_group_create(tabs, 1, None, None, None, None, None, C.byref(g)) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_eb_group_checked_scatter(None, 1, 1, 1, 1, None, None, None) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_gemm_checked_host_batched(None, 1, 1, 1, 1, None, None, 1, 1, None, 1, None, 1, None,
+                                                  None) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_gemm_checked_batched_faults(None, 1, 1, 1, 1, None, None, 1, 1, None, 1, 1, None, 1, None,
+                                                    None, 0, None) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_gemm_weight_flip_bit_batched(None, 0, 0, 0, 0, None) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_gather_probe(None, 128, None, 0, None, None) == L.ERR_INVALID_ARGUMENT
+    assert L.lib.abftlp_gather_probe(vp(16), 24, None, 0, vp(16), None) == L.ERR_INVALID_ARGUMENT
+    assert "multiple of 16" in L.last_error()
+    assert L.lib.abftlp_flip_bit(None, 4, 0, 0, None) == L.ERR_INVALID_ARGUMENT
