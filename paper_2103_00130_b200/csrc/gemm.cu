@@ -671,8 +671,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 }
                 if constexpr (CHECKED) {
                     if (col0 + 32 <= p.n) {
+                        // pairwise tree: 5 dependent int64 adds instead of a 32-long carry chain (exact in
+                        // any order: |sum| < 32 * 2^31)
+                        long long t[16];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) rsum += static_cast<int32_t>(v[j]);
+                        for (int j = 0; j < 16; ++j)
+                            t[j] = static_cast<long long>(static_cast<int32_t>(v[2 * j])) + static_cast<int32_t>(v[2 * j + 1]);
+#pragma unroll
+                        for (int w2 = 8; w2 > 0; w2 >>= 1)
+#pragma unroll
+                            for (int j = 0; j < w2; ++j) t[j] += t[j + w2];
+                        rsum += t[0];
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -690,8 +699,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     for (int qq = 0; qq < 8; ++qq)
                         *reinterpret_cast<uint4*>(buf + lane * 128 + ((qq ^ (lane & 7)) << 4)) =
                             make_uint4(v[4 * qq], v[4 * qq + 1], v[4 * qq + 2], v[4 * qq + 3]);
+#ifdef ABFT_TRACE_CHUNKS
+                    if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[10] = globaltimer();
+#endif
                     fence_proxy_async_smem();
                     __syncwarp();
+#ifdef ABFT_TRACE_CHUNKS
+                    if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[11] = globaltimer();
+#endif
                     if (lane == 0) {
                         if (row0 < p.m && col0 < p.n) tma_store_3d(&tmC, buf, col0, row0, x.b);
                         bulk_commit();
