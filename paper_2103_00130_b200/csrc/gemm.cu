@@ -669,6 +669,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                             if (col0 + j < p.n) dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
                     }
                 }
+#ifdef ABFT_TRACE_CHUNKS
+                if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[9] = globaltimer();
+#endif
                 if constexpr (CHECKED) {
                     if (col0 + 32 <= p.n) {
                         // pairwise tree: 5 dependent int64 adds instead of a 32-long carry chain (exact in
