@@ -149,7 +149,8 @@ struct ChunkStage {      // per warp
 
 // Fast path: d == 32 * CPL * WPB, rows 8-byte aligned. Block = 8 warps = 8 / WPB bags.
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
-__global__ void __launch_bounds__(256, 4) eb_bag_kernel(const EbParams p, int log2d) {  // <= 64 regs: 32 warps/SM
+// 4 blocks/SM (<= 64 regs, 32 warps/SM) spills 0.5-0.9 KB per thread at 8 columns per lane; 2 blocks/SM does not.
+__global__ void __launch_bounds__(256, CPL >= 8 ? 2 : 4) eb_bag_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;  // bytes per lane per row
     constexpr int BAGS = 8 / WPB;
     using Word = typename LaneWord<BPL>::T;

@@ -245,3 +245,39 @@ def test_gather_probe_runs_and_validates(E):
     torch.cuda.synchronize()
     with pytest.raises(_lib.InvalidArgument):
         _lib.call("abftlp_gather_probe", vp(tab), 24, vp(idx), 5000, vp(sink), None)
+
+
+@pytest.mark.parametrize("elem,scale,d,weighted", [("s8", "f32", 256, False), ("u8", "f16", 256, True),
+                                                   ("u4", "f32", 256, True), ("s8", "f32", 128, True),
+                                                   ("u4", "f16", 64, False), ("u8", "f32", 32, False)])
+def test_sync_fast_path_bit_exact(E, elem, scale, d, weighted, monkeypatch):
+    """The 8-byte-aligned (non-cp.async) warp-per-bag kernel, forced with ABFTLP_EB_SYNC: bit-exact against the
+    oracle on 1, 2, 4 and 8 columns per lane, with faulted rows flagged."""
+    monkeypatch.setenv("ABFTLP_EB_SYNC", "1")
+    rng = np.random.default_rng(d * 13 + len(elem))
+    R, nb = 2000, 700
+    rb = d // 2 if elem == "u4" else d
+    rows = rng.integers(0 if elem != "s8" else -128, 256 if elem != "s8" else 128, (R, rb)).astype(
+        np.int8 if elem == "s8" else np.uint8)
+    sdt = np.float16 if scale == "f16" else np.float32
+    sc = rng.uniform(1e-3, 1e-2, R).astype(sdt)
+    bi = rng.uniform(-1, 1, R).astype(sdt)
+    lens = rng.integers(0, 90, nb)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    idx = rng.integers(0, R, off[-1]).astype(np.int64)
+    w = rng.uniform(0, 1, off[-1]).astype(np.float32) if weighted else None
+    t = E.QuantEmbeddingTable(rows, sc, bi, elem=elem, dim=d)
+    rows_now = rows.copy().view(np.uint8)
+    for r in rng.choice(R, 10, replace=False):
+        col, bit = int(rng.integers(0, d)), int(rng.integers(0, 4))
+        t.flip_bit(int(r), col, bit)
+        if elem == "u4":
+            rows_now[r, col // 2] ^= np.uint8(1 << (bit + 4 * (col & 1)))
+        else:
+            rows_now[r, col] ^= np.uint8(1 << bit)
+    ref = O.eb(rows_now.view(rows.dtype), sc, bi, off, idx, w, elem=elem, dim=d, row_sums_=O.row_sums(rows, elem, d))
+    out, flags, rsum, csum, cnt = E.eb_csr(t, off, idx, w)
+    assert_same(out, flags, rsum, csum, ref)
+    assert int(cnt.item()) == int(ref[3].sum()) > 0
+    out_u, *_ = E.eb_csr(t, off, idx, w, checked=False)
+    assert torch.equal(out_u, out)
