@@ -274,3 +274,27 @@ def test_single_tile_rows_bit_exact_and_workspace_clean(G, m, n, k, monkeypatch)
     monkeypatch.setenv("ABFTLP_GEMM_TILING", "64")  # n > 64: several tiles per row, row atomics again
     a2, b2 = rnd(m + 1, m, 2 * n, k)
     check_against_oracle(G, a2, b2)
+
+
+def test_production_path_agrees_with_dual_encoded_oracle(G):  # P:tests/test_gemm_abft.cpp:211-236
+    """50 ragged shapes (m, n, k in [1, 16]): the B200 C' equals the exact product block of the dual-encoded
+    oracle (P:tests/dual_check.hpp:23-46); one bit flipped in C' is located by the dual check at its cell and
+    flagged by the device verify."""
+    rng = np.random.default_rng(19)
+    for _ in range(50):
+        m, n, k = (int(v) for v in rng.integers(1, 17, 3))
+        a, b = rnd(int(rng.integers(1 << 30)), m, n, k)
+        res = G.abft_gemm(a, G.PackedEncodedWeight(b))
+        assert res.errCount == 0
+        dual = O.dual_product(a, b)
+        assert O.dual_check(dual)[0] == 0
+        ct = res.cTemp.data.cpu().numpy()
+        assert np.array_equal(ct[:, :n].astype(np.int64), dual[:m, :n])
+        i, j, bit = int(rng.integers(m)), int(rng.integers(n)), int(rng.integers(32))
+        before = int(ct[i, j])
+        after = int(np.array([before], np.int32).view(np.uint32)[0] ^ np.uint32(1 << bit))
+        after = int(np.array([after], np.uint32).view(np.int32)[0])
+        res.cTemp.data[i, j] = after
+        dual[i, j] += after - before
+        assert O.dual_check(dual) == (1, i, j)
+        assert G.verify_checksums(res.cTemp) > 0
