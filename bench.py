@@ -52,8 +52,19 @@ def peaks():
     if f.exists():
         d = json.loads(f.read_text())
         p = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "MEASURED_PEAKS.json"}
-    # No int8 peak is measured by the driver: use 2x the measured bf16 dense burst.
-    p["int8_tops"] = 2 * p["bf16_tflops"]
+    # int8 tensor roof MEASURED on this pool's B200s (scripts/int8_peak.py -> profiles/r*/int8_peak.json): the
+    # tcgen05 kind::i8 issue rate on every SM pair with random operands (cuBLASLt int8 is slower on B200), burst
+    # (one ~5 ms launch) and sustained (>= 4 s back to back, under the 1 kW power cap). The job is timed as
+    # 20 x 3 ms steps with sw_power_cap active, so `peak` is the sustained figure; the burst one rides along.
+    caps = sorted(REPO.glob("profiles/r*/int8_peak.json"))
+    if caps:
+        d = json.loads(caps[-1].read_text())
+        p["int8_tops"] = d["int8_peak_sustained_tops"]
+        p["int8_tops_burst"] = d["int8_peak_burst_tops"]
+        p["int8_source"] = f"{caps[-1].relative_to(REPO)} (tcgen05 kind::i8 microbenchmark, sustained; burst in int8_tops_burst)"
+    else:
+        p["int8_tops"] = p["int8_tops_burst"] = 2 * p["bf16_tflops"]
+        p["int8_source"] = "2 x bf16 dense burst (no measured int8 peak found)"
     return p
 
 
@@ -157,14 +168,19 @@ def plan_segments(plan: dict, runs: int, group_max: int, max_faults: int = 8) ->
     return segments
 
 
-def cpu_eb_sample():
-    """E3 / E4 batches through the oracle's C restatement of abft_embedding_bag (single thread; the reference
-    implements s8 rows only, so the u8 / u4 configs run on its restatement). Host tables of the
-    configs' shapes and distributions, the bags of eb_secondary. Returns {cfg: {ms, alg_gbs}}."""
-    sys.path.insert(0, str(REPO / "tests"))
-    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _eb_configs(rng):
+    """The E3 / E4 host inputs (BASELINE configs[2-3] shapes and distributions; the bags of eb_secondary's kind)."""
     out = {}
-    rng = np.random.default_rng(3)
     for name in ("E3", "E4"):
         if name == "E3":
             R, d, nb, elem = 4_000_000, 128, 2048, "u8"
@@ -184,18 +200,126 @@ def cpu_eb_sample():
             rb, meta_b = d // 2, 8
             sc = rng.uniform(1e-3, 1e-2, R).astype(np.float16)
             bi = rng.uniform(-1, 1, R).astype(np.float16)
-        rows = rng.integers(0, 256, (R, rb), dtype=np.uint8)
-        sums = O.row_sums(rows, elem, d)
         off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        out[name] = dict(R=R, d=d, nb=nb, elem=elem, idx=idx, w=w, rb=rb, meta_b=meta_b, sc=sc, bi=bi, off=off)
+    return out
+
+
+def _parallel_bags(fn, nb, threads):
+    """Run fn(b0, b1) over `threads` contiguous bag ranges concurrently (ctypes releases the GIL); wall seconds."""
+    cuts = [nb * i // threads for i in range(threads + 1)]
+    ths = [threading.Thread(target=fn, args=(cuts[i], cuts[i + 1])) for i in range(threads) if cuts[i + 1] > cuts[i]]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return time.perf_counter() - t0
+
+
+def cpu_eb_sample():
+    """E3 / E4 batches on the host cores: the oracle's C restatement of abft_embedding_bag
+    (u8 / u4 rows: the reference implements s8 rows only) single-thread and on all cores, and the
+    REFERENCE itself (oracle/_ref, abft_embedding_bag on a persistent table) on an s8 table of E3's shape, all
+    cores. Returns {cfg: {...}}."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+    threads = os.cpu_count() or 1
+    out = {}
+    cfgs = _eb_configs(np.random.default_rng(3))
+    for name, c in cfgs.items():
+        R, d, nb, elem, rb = c["R"], c["d"], c["nb"], c["elem"], c["rb"]
+        rows = np.random.default_rng(4).integers(0, 256, (R, rb), dtype=np.uint8)
+        sums = O.row_sums(rows, elem, d)
+        off, idx, w = c["off"], c["idx"], c["w"]
         t0 = time.perf_counter()
-        O.eb(rows, sc, bi, off, idx, w, elem=elem, dim=d, row_sums_=sums)
-        dt = time.perf_counter() - t0
-        L_ = int(lens.sum())
-        alg = L_ * (rb + meta_b + 4 + 8 + (4 if w is not None else 0)) + 8 * (nb + 1) + 4 * nb * d + nb
-        out[name] = {"ms": dt * 1e3, "alg_gbs": alg / dt / 1e9, "cores": 1, "kind": "port",
+        O.eb(rows, c["sc"], c["bi"], off, idx, w, elem=elem, dim=d, row_sums_=sums)
+        dt1 = time.perf_counter() - t0
+
+        def part(b0, b1):
+            o = off[b0:b1 + 1] - off[b0]
+            O.eb(rows, c["sc"], c["bi"], o, idx[off[b0]:off[b1]], None if w is None else w[off[b0]:off[b1]],
+                 elem=elem, dim=d, row_sums_=sums)
+        dtn = _parallel_bags(part, nb, threads)
+        L_ = int(off[-1])
+        alg = L_ * (rb + c["meta_b"] + 4 + 8 + (4 if w is not None else 0)) + 8 * (nb + 1) + 4 * nb * d + nb
+        out[name] = {"ms": dt1 * 1e3, "alg_gbs": alg / dt1 / 1e9, "cores": 1, "kind": "port",
+                     "ms_all_cores": dtn * 1e3, "alg_gbs_all_cores": alg / dtn / 1e9, "cores_all": threads,
                      "sample": f"one {name} batch ({nb} bags, {L_} lookups), oracle restatement ({elem} rows)"}
+        if name == "E3" and O.ref() is not None:
+            Rf = O.ref()
+            srows = rows.view(np.int8)
+            tab = Rf.ref_eb_table_new(O.P(srows), O.sz(R), O.sz(d), O.P(c["sc"]), O.P(c["bi"]))
+            uoff, uidx = off.astype(np.uint64), idx.astype(np.uint64)
+            r_out = np.empty((nb, d), np.float32)
+            err = np.empty(nb, np.uint8)
+
+            def ref_part(b0, b1):
+                Rf.ref_eb_table_check_range(C.c_void_p(tab), O.P(uoff), O.P(uidx), None, O.sz(b0), O.sz(b1),
+                                            O.P(r_out), O.P(err))
+            dt_r1 = _parallel_bags(ref_part, nb, 1)
+            dt_rn = _parallel_bags(ref_part, nb, threads)
+            Rf.ref_eb_table_free(C.c_void_p(tab))
+            out[name]["reference_s8_same_shape"] = {
+                "ms": dt_r1 * 1e3, "ms_all_cores": dt_rn * 1e3, "cores_all": threads, "kind": "reference",
+                "alg_gbs_all_cores": alg / dt_rn / 1e9,
+                "sample": "the reference's abft_embedding_bag (oracle/_ref) on an s8 table of E3's shape, same bags"}
         del rows, sums
     return out
+
+
+def cpu_reference_benches():
+    """The reference's OWN single-thread benches through its C ABI (oracle/_ref: abftlp_bench_gemm / abftlp_bench_eb,
+    P:src/bench.cpp:50-152: median of reps after 2 warm-ups; GEMM encode inside the checked timing; EB cache flush)."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+    Rf = O.ref()
+    if Rf is None:
+        return None
+
+    class BR(C.Structure):
+        _fields_ = [("baseline_ns", C.c_double), ("abft_ns", C.c_double), ("overhead_fraction", C.c_double)]
+    out = {}
+    r = BR()
+    if Rf.abftlp_bench_gemm(C.c_uint64(64), C.c_uint64(512), C.c_uint64(512), C.c_uint32(5), C.c_uint64(SEED),
+                            C.byref(r)) == 0:
+        out["gemm_64x512x512"] = {"plain_ms": r.baseline_ns / 1e6, "abft_ms": r.abft_ns / 1e6,
+                                  "overhead_pct": 100 * r.overhead_fraction}
+    if Rf.abftlp_bench_eb(C.c_uint64(4_000_000), C.c_uint64(128), C.c_uint64(60), C.c_uint64(2048), C.c_uint32(5),
+                          C.c_uint64(SEED), C.byref(r)) == 0:
+        out["eb_4Mx128_pool60_batch2048"] = {"plain_ms": r.baseline_ns / 1e6, "abft_ms": r.abft_ns / 1e6,
+                                             "overhead_pct": 100 * r.overhead_fraction}
+    out["cores"] = 1
+    out["kind"] = "reference"
+    return out
+
+
+def cpu_g1_sample():
+    """G1 on the host cores: the reference's abft_gemm (oracle/_ref) for the 100 seeded 64x512x512 trials, one
+    pre-encoded weight per trial (the device path encodes before timing too), trials spread over every core."""
+    sys.path.insert(0, str(REPO / "tests"))
+    import oracle_api as O  # noqa: E402  (test infrastructure: the CPU baseline only)
+    Rf = O.ref()
+    if Rf is None:
+        return None
+    m, n, k, nt = 64, 512, 512, 100
+    threads = os.cpu_count() or 1
+    ins = [O.gemm_inputs(SEED, t, m, n, k) for t in range(nt)]
+    ws = [Rf.ref_gemm_weight_new(O.P(b), O.sz(k), O.sz(n)) for _, b in ins]
+    outs = [np.empty((m, n + 1), np.int32) for _ in range(nt)]
+
+    def part(t0, t1):
+        for t in range(t0, t1):
+            err = C.c_uint64()
+            Rf.ref_abft_gemm_w(O.P(ins[t][0]), O.sz(m), O.sz(k), C.c_void_p(ws[t]), O.P(outs[t]), C.byref(err))
+    dt = _parallel_bags(part, nt, threads)
+    dt1 = _parallel_bags(part, 10, 1) * nt / 10
+    for w in ws:
+        Rf.ref_gemm_weight_free(C.c_void_p(w))
+    ops = 2 * m * n * k * nt
+    return {"us_per_100_all_cores": dt * 1e6, "tops_all_cores": ops / dt / 1e12, "cores": threads,
+            "us_per_100_single_thread": dt1 * 1e6, "kind": "reference",
+            "sample": "the 100 G1 trials through the reference's abft_gemm (pre-encoded weights)"}
 
 
 def run_reference_arm(args, rank, world):
@@ -216,7 +340,7 @@ def run_reference_arm(args, rank, world):
             "data": "synthetic (SplitMix64, the reference's draw protocol)",
             "config": {"workload": "G2: checked GEMM m=256 k=4096 n=4096 (BASELINE configs[1]); one step = "
                                    f"{threads} concurrent abft_gemm calls (one per host thread) on a pre-encoded B"},
-            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": threads, "kind": kind,
+            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": threads, "kind": kind, "cpu_model": cpu_model(),
                              "sample": f"{threads} G2 GEMMs per step on {threads} threads"},
             "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -398,18 +522,28 @@ def run_gpu_arm(args, rank, world, dist):
     # unchecked baseline (same kernel, checking compiled out) for the ABFT overhead
     u_total, _ = timed(graphs[False].replay, args.steps)
 
-    # ---- the roofline's kernel: the grouped checked launch. Its launches are bracketed by CUDA events on the
-    # job stream in one eager pass of the job (after an L2 flush; events outside the timed region).
-    L.call("abftlp_l2_flush", vp(flush_buf), flush_buf.numel(), 77, st)
-    torch.cuda.synchronize()
-    torch.cuda._sleep(4_000_000)  # ~2 ms: the host enqueues the job before the GPU reaches it
-    ev = []
-    job(True, ev)
-    torch.cuda.synchronize()
-    grp_gemms = sum(c for c, _, _ in ev)
-    grp_ms = sum(a.elapsed_time(b) for _, a, b in ev)
-    kernel_us = grp_ms * 1e3 / len(ev)  # average grouped-launch duration
-    gemms_per_launch = grp_gemms / len(ev)
+    # ---- the roofline's kernel: the grouped checked launch, timed IN-GRAPH. A second graph holds only the job's
+    # grouped checked launches (the same launches, same order, PDL between them, minus the B'-fault batch); its
+    # replay time over the number of launches is the kernel's average launch duration inside the step, so
+    # kernel time per step <= ms_per_step by construction. L2 flushed before each replay, as the step.
+    def grouped_only():
+        n = 0
+        for sg in segments:
+            if sg[0] == "group":
+                launch_group(sg[1], sg[2], sg[3], True)
+                n += 1
+        return n
+    g_grp = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_grp, stream=stream):
+        n_grp = grouped_only()
+    torch.cuda.set_stream(stream)
+    g_grp.replay()
+    grp_total, _ = timed(g_grp.replay, args.steps)
+    del g_grp
+    grp_gemms = sum(sg[2] for sg in segments if sg[0] == "group")
+    grp_ms = grp_total / args.steps
+    kernel_us = grp_ms * 1e3 / n_grp  # average grouped-launch duration inside the graph
+    gemms_per_launch = grp_gemms / n_grp
 
     # ---- one m=256 GEMM per launch (no grouping): isolated launch latency, and the job as a CUDA graph of
     # 1000 single launches (programmatic dependent launch between them) -- what grouping is compared with
@@ -432,6 +566,23 @@ def run_gpu_arm(args, rank, world, dist):
         per_launch.append((e0, e1))
     torch.cuda.synchronize()
     single_launch_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in per_launch[10:])
+    # library yardstick in the same run: cuBLASLt int8 (torch._int_mm, s8 x s8 -> s32, NO check) at the same shape
+    a8 = torch.randint(-128, 128, (M, K), dtype=torch.int8, device=dev)
+    b8 = torch.randint(-128, 128, (K, N), dtype=torch.int8, device=dev)
+    for _ in range(5):
+        torch._int_mm(a8, b8)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(4_000_000)
+    cub = []
+    for _ in range(60):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        torch._int_mm(a8, b8)
+        e1.record(stream)
+        cub.append((e0, e1))
+    torch.cuda.synchronize()
+    cublas_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in cub[10:])
+    del a8, b8
     # grouped results are bit-identical to single launches (spot check on a clean run)
     clean_run = next(i for i in range(JOB) if i not in plan)
     single(clean_run)
@@ -487,10 +638,14 @@ def run_gpu_arm(args, rank, world, dist):
     e2e_eq_device = all(torch.equal(c_host[i], c_all[i].cpu()) and torch.equal(cs_host[i], csum[i].cpu()) for i in chk) \
         and all(int(ec_host[i]) == 0 for i in chk)
 
+    # D5 runs on every rank (table-wise EB + exchange + N-split MLP); the single-GPU legs on rank 0 only
+    d5 = None if args.no_d5 else d5_leg(L, dev, st, vp, pk, rank, world, dist)
     secondary = eb_secondary(L, dev, st, vp, pk) if (rank == 0 and not args.no_eb) else None
     if rank == 0 and secondary is not None:
         secondary["G1"] = g1_secondary(L, dev, st, vp, pk)
-        secondary["D5_shard"] = d5_secondary(L, dev, st, vp, pk)
+    if rank == 0 and d5 is not None:
+        secondary = secondary or {}
+        secondary["D5"] = d5
 
     L.lib.abftlp_gemm_weight_free(w)
     if nfb:
@@ -507,6 +662,9 @@ def run_gpu_arm(args, rank, world, dist):
         cap = json.loads(caps[-1].read_text())
         traffic, traffic_src = cap["traffic_bytes_per_gemm"] * gemms_per_launch, str(caps[-1].relative_to(REPO))
     achieved = grp_gemms * OPS / (grp_ms * 1e-3) / 1e12
+    # unique bytes of one grouped launch: every run's A, C' (incl. checksum column) and flags, plus B' once (the
+    # job's weight is read from HBM once and then served from L2)
+    uniq_bytes = gemms_per_launch * (M * K + 4 * M * (N + 1) + M) + K * (N + 1)
     line = {
         "metric": "checked int8 GEMM TOPS", "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -524,14 +682,20 @@ def run_gpu_arm(args, rank, world, dist):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["int8_tops"], "unit": "TOP/s",
                      "frac": achieved / pk["int8_tops"], "traffic": traffic, "traffic_unit": "bytes/launch",
                      "traffic_source": traffic_src,
+                     "peak_burst": pk["int8_tops_burst"], "frac_of_burst": achieved / pk["int8_tops_burst"],
                      "kernel": "gemm_pair_kernel<256, checked> (grouped launch)", "kernel_us": kernel_us,
-                     "kernel_us_how": "mean CUDA-event duration of the job's grouped checked launches (job stream, eager pass after an L2 flush)",
+                     "kernel_us_how": f"CUDA-graph replay of the job's {n_grp} grouped checked launches (same launches as the step, "
+                                      "L2 flushed before each replay) / launches",
+                     "kernel_share_of_step": grp_ms / (t_total / args.steps),
                      "gemms_per_launch": gemms_per_launch, "ops_per_launch": gemms_per_launch * OPS,
-                     "alg_bytes_per_launch": gemms_per_launch * ALG_BYTES,
-                     "peak_source": f"2 x bf16 dense burst from {pk['source']} (int8 dense = 2x bf16 on B200; no driver-measured int8 peak)",
-                     "note": "B' (16.8 MB) stays L2-resident across the job and A/C' stream through HBM at ~1.8 TB/s, so the bound is the tensor pipe"},
+                     "unique_bytes_per_launch": uniq_bytes,
+                     "unique_gbs": uniq_bytes / (kernel_us * 1e-6) / 1e9,
+                     "peak_source": pk["int8_source"],
+                     "note": "B' (16.8 MB) is read from HBM once per launch and then served from L2; A and C' stream through HBM, so the bound is the tensor pipe"},
         "per_gemm_launch": {"single_launch_us": single_launch_us,
                             "single_launch_how": "median CUDA-event duration of an isolated m=256 checked launch",
+                            "cublas_int8_unchecked_us": cublas_us,
+                            "cublas_how": "torch._int_mm (cuBLASLt, s8 x s8 -> s32, no checksum) 256x4096x4096, same method",
                             "ungrouped_job_tops": ungrouped_tops,
                             "ungrouped_how": "the same 1000 GEMMs as a CUDA graph of 1000 single launches (PDL)"},
         "encoder": {"us": encode_us, "alg_bytes": 2 * K * N, "alg_gbs": 2 * K * N / (encode_us * 1e-6) / 1e9,
@@ -554,11 +718,14 @@ def run_gpu_arm(args, rank, world, dist):
         tops, kind, dt = cpu_gemm_sample(threads)
         line["cpu_baseline"] = {"value": tops, "unit": "TOPS", "cores": threads, "kind": kind,
                                 "sample": f"{threads} concurrent G2 abft_gemm calls ({dt:.1f} s wall)"}
+        line["cpu_baseline"]["cpu_model"] = cpu_model()
         if secondary is not None:
             try:
                 line["cpu_baseline"]["eb"] = cpu_eb_sample()
             except MemoryError:
                 pass
+            line["cpu_baseline"]["g1"] = cpu_g1_sample()
+            line["cpu_baseline"]["reference_own_benches"] = cpu_reference_benches()
     print(json.dumps(line), flush=True)
 
 
@@ -655,117 +822,165 @@ def g1_secondary(L, dev, st, vp, pk):
             "note": "one abftlp_gemm_checked_batched launch for the 100 trials (reference m x (n+1) layout; and C' 16-byte aligned with the checksum column separate) vs 100 abftlp_gemm_checked launches"}
 
 
-def d5_secondary(L, dev, st, vp, pk, G=8):
-    """BASELINE configs[4] (D5), ONE GPU's share at G=8 (table-wise EB shards, MLP split by N): 64/G = 8
-    int8-rowwise tables of 1M x 128 (fp32 scale/bias), batch 8192, Zipf(1.05) pooling 80, checked lookups
-    written by the scatter kernel straight into the all-to-all send buffer [G][B/G][8][128]; plus the checked
-    MLP GEMMs m=8192 with (k, n/G) for (k, n) in {512,1024,2048}^2. Synthetic seeded data."""
+def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
+    """BASELINE configs[4] (D5), the whole DLRM-style step on `world` GPUs (one process per GPU):
+      * 64 int8-rowwise tables x 1M x 128 (fp32 scale/bias), table-wise sharded (table t on rank t % G), batch
+        8192, pooling 80, Zipf(1.05) indices -- every rank's tables pooled by ONE grouped checked launch that
+        writes straight into the persistent exchange buffer (vectors + verdict quads);
+      * the exchange: ONE all_to_all_single (NCCL over NVLink) to batch-sharded [B/G, 64, 128], then the
+        (slot, rank) -> table reorder (one copy kernel each for vectors and verdicts);
+      * the checked MLP GEMMs m = 8192, (k, n) in {512,1024,2048}^2 split by N columns across ranks (each rank
+        encodes its own column shard), and the OR of the per-row GEMM verdicts (one all-reduce MAX).
+    Seeded synthetic data (identical tables and bags at any world size). The step is replayed as a CUDA graph
+    when it captures (eager otherwise); times are CUDA events, max over ranks."""
     import torch
-    T_loc, R, d, B, pool = 64 // G, 1_000_000, 128, 8192, 80
-    rng = np.random.default_rng(5)
-    ranks = np.arange(1, R + 1, dtype=np.float64)
-    cdf = np.cumsum(ranks ** -1.05)
-    cdf /= cdf[-1]
-    tabs, rows_keep, bags = [], [], []
-    for t in range(T_loc):
-        rows = torch.randint(-128, 128, (R, d), dtype=torch.int8, device=dev)
-        sc = torch.rand(R, device=dev) * 9e-3 + 1e-3
-        bi = torch.rand(R, device=dev) * 2 - 1
-        h = C.c_void_p()
-        L.call("abftlp_eb_table_create", 0, vp(rows), R, d, d, 0, vp(sc), vp(bi), None, st, C.byref(h))
-        perm = rng.permutation(R)
-        idx = perm[np.searchsorted(cdf, rng.random(B * pool))].astype(np.int64)
-        off = torch.arange(0, B * pool + 1, pool, dtype=torch.int64, device=dev)
-        tabs.append(h)
-        rows_keep.append((rows, sc, bi))
-        bags.append((off, torch.from_numpy(idx).to(dev)))
-    Bg = B // G
-    send = torch.empty((G, Bg, T_loc, d), dtype=torch.float32, device=dev)
-    send_f = torch.empty((G, Bg, T_loc), dtype=torch.uint8, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-    dests = []
-    for slot in range(T_loc):
-        o = torch.tensor([send[g, 0, slot].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
-        f = torch.tensor([send_f[g, 0, slot:].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
-        dests.append((o, f))
-
-    def eb_step_per_table():
-        for slot in range(T_loc):
-            off, ix = bags[slot]
-            o, f = dests[slot]
-            L.call("abftlp_eb_checked_scatter", tabs[slot], vp(off), vp(ix), B, None, vp(o), T_loc * d, vp(f), T_loc,
-                   Bg, vp(cnt), None, st)
-
-    # all of this GPU's tables in ONE persistent launch (abftlp_eb_group_checked_scatter)
-    P_ = C.c_void_p
-    grp = C.c_void_p()
-    L.call("abftlp_eb_group_create", (P_ * T_loc)(*tabs), T_loc, (P_ * T_loc)(*[vp(bags[t][0]) for t in range(T_loc)]),
-           (P_ * T_loc)(*[vp(bags[t][1]) for t in range(T_loc)]), None,
-           (P_ * T_loc)(*[vp(dests[t][0]) for t in range(T_loc)]), (P_ * T_loc)(*[vp(dests[t][1]) for t in range(T_loc)]),
-           C.byref(grp))
-
-    def eb_step():
-        L.call("abftlp_eb_group_checked_scatter", grp, B, T_loc * d, T_loc, Bg, vp(cnt), None, st)
-
-    shapes = [(k, n // G) for k in (512, 1024, 2048) for n in (512, 1024, 2048)]
+    from paper_2103_00130_b200 import embedding as E
+    from paper_2103_00130_b200 import sharded as S
+    T, R, d, B, pool, m = 64, 1_000_000, 128, 8192, 80, 8192
+    G = world
+    mine = S.local_tables(T, G, rank)
+    ranks = torch.arange(1, R + 1, dtype=torch.float64, device=dev)
+    cdf = torch.cumsum(ranks ** -1.05, 0)
+    cdf /= cdf[-1].clone()
+    tables, bags = {}, {}
+    for t in mine:
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(5000 + t)
+        rows = torch.randint(-128, 128, (R, d), dtype=torch.int8, device=dev, generator=gen)
+        sc = torch.rand(R, device=dev, generator=gen) * 9e-3 + 1e-3
+        bi = torch.rand(R, device=dev, generator=gen) * 2 - 1
+        tables[t] = E.QuantEmbeddingTable(rows, sc, bi, elem="s8", dim=d)
+        u = torch.rand(B * pool, dtype=torch.float64, device=dev, generator=gen)
+        perm = torch.randperm(R, device=dev, generator=gen)
+        idx = perm[torch.searchsorted(cdf, u).clamp_(max=R - 1)]
+        bags[t] = (torch.arange(0, B * pool + 1, pool, dtype=torch.int64, device=dev), idx.contiguous(), None)
+        del rows, sc, bi, u, perm
+    del ranks, cdf
+    group_ok = True
+    eb = S.ShardedEmbeddingBags(tables, T, B, d, device=dev)
+    shapes = [(k, n) for k in (512, 1024, 2048) for n in (512, 1024, 2048)]
     mlp = []
-    m = 8192
-    for k, n in shapes:
-        bw = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev)
+    mflags = torch.zeros((len(shapes), m), dtype=torch.uint8, device=dev)
+    for q, (k, n) in enumerate(shapes):
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(9000 + q)
+        bfull = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev, generator=gen)
+        a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device=dev, generator=gen)
+        n0, n1 = S.column_shard(n, G, rank)
+        bsh = bfull[:, n0:n1].contiguous()
         w = C.c_void_p()
-        L.call("abftlp_gemm_encode", vp(bw), k, n, n, st, C.byref(w))
-        a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device=dev)
-        c = torch.empty((m, n), dtype=torch.int32, device=dev)
+        L.call("abftlp_gemm_encode", vp(bsh), k, n1 - n0, n1 - n0, st, C.byref(w))
+        c = torch.empty((m, n1 - n0), dtype=torch.int32, device=dev)
         cs = torch.empty(m, dtype=torch.int32, device=dev)
-        fl = torch.empty(m, dtype=torch.uint8, device=dev)
-        er = torch.empty(1, dtype=torch.int32, device=dev)
-        mlp.append((k, n, w, a, c, cs, fl, er, bw))
+        er = torch.zeros(1, dtype=torch.int32, device=dev)
+        mlp.append((k, n1 - n0, w, a, c, cs, er))
+        del bfull, bsh
 
-    def mlp_step():
-        for k, n, w, a, c, cs, fl, er, _ in mlp:
-            L.call("abftlp_gemm_checked", vp(a), m, k, w, vp(c), n, vp(cs), 1, vp(fl), vp(er), None, st)
+    def phase_eb():
+        eb.backend.pool_into([tables[t] for t in eb.order], [bags[t] for t in eb.order], eb.xsend, d)
 
-    def timed(fn, reps=8):
-        # the step's launches are captured once into a CUDA graph (as a production step would run them), so
-        # host launch latency is not inside the device-timed region
-        fn()
+    def phase_x():
+        if G > 1:
+            dist.all_to_all_single(eb.xrecv, eb.xsend)
+        return S.unpack_exchange(eb.xrecv, T, d, eb.out, eb.flags)
+
+    def phase_mlp():
+        for q, (k, n_loc, w, a, c, cs, er) in enumerate(mlp):
+            L.call("abftlp_gemm_checked", vp(a), m, k, w, vp(c), n_loc, vp(cs), 1, vp(mflags[q]), vp(er), None, st)
+
+    def phase_or():
+        if G > 1:
+            dist.all_reduce(mflags, op=dist.ReduceOp.MAX)  # OR of the N-shard verdicts
+
+    def step():
+        phase_eb()
+        phase_x()
+        phase_mlp()
+        phase_or()
+
+    def sync_all():
+        if dist is not None:
+            dist.barrier()
         torch.cuda.synchronize()
-        stream = torch.cuda.current_stream()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            fn()
-        g.replay()
-        torch.cuda.synchronize()
+
+    def maxr(x):
+        if dist is None:
+            return x
+        t_ = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
+
+    stream = torch.cuda.current_stream()
+    for _ in range(3):
+        step()
+    sync_all()
+    eb.backend.raise_on_status()
+    # per-phase device times (eager, events on the step's stream)
+    phase_us = {}
+    for name, fn in (("eb_lookups", phase_eb), ("exchange", phase_x), ("mlp", phase_mlp), ("verdict_or", phase_or)):
         ts = []
-        for _ in range(reps):
+        for _ in range(5):
+            sync_all()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            g.replay()
-            e1.record()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
-        del g
-        return statistics.median(ts)
-
-    eb_us = timed(eb_step)
-    eb_per_table_us = timed(eb_step_per_table)
-    mlp_us = timed(mlp_step)
-    lookups = T_loc * B * pool
-    alg = lookups * (d + 4 + 4 + 4 + 8) + T_loc * (8 * (B + 1) + 4 * B * d + B)
-    ops = sum(2 * m * n * k for k, n, *_ in mlp)
-    for k, n, w, *_ in mlp:
+        phase_us[name] = maxr(statistics.median(ts[1:]))
+    # the whole step, replayed as a CUDA graph when the step (incl. NCCL) captures
+    graph, how = None, "eager"
+    try:
+        sync_all()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step()
+        g.replay()
+        sync_all()
+        graph, how = g, "CUDA graph replay"
+    except Exception as e:  # noqa: BLE001  (capture unsupported here: time the eager step)
+        how = f"eager (graph capture failed: {type(e).__name__})"
+        torch.cuda.synchronize()
+    run = graph.replay if graph is not None else step
+    ts = []
+    for _ in range(steps):
+        sync_all()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(maxr(e0.elapsed_time(e1) * 1e3))
+    step_us = statistics.median(ts)
+    sync_all()
+    flagged_mlp = int(mflags.to(torch.int64).sum().item())
+    out, fl = S.unpack_exchange(eb.xrecv, T, d, eb.out, eb.flags)
+    flagged_eb = int(fl.to(torch.int64).sum().item())
+    lookups_rank = len(mine) * B * pool
+    alg_eb = lookups_rank * (d + 16 + 8) + len(mine) * (8 * (B + 1) + 4 * B * (d + S.FLAG_QUAD))
+    x_bytes = int(eb.xsend.numel() * 4 * (G - 1) // max(G, 1))
+    ops = sum(2 * m * n_loc * k for k, n_loc, *_ in mlp)
+    mlp_alg = sum(m * k + k * (n_loc + 1) + 4 * m * (n_loc + 1) + m for k, n_loc, *_ in mlp)
+    for k, n_loc, w, *_ in mlp:
         L.lib.abftlp_gemm_weight_free(w)
-    L.lib.abftlp_eb_group_free(grp)
-    for h in tabs:
-        L.lib.abftlp_eb_table_free(h)
-    return {"workload": f"D5 per-GPU share at G={G}: {T_loc} tables x 1M x 128 int8, batch {B}, pooling {pool}, "
-                        "Zipf(1.05); 9 checked MLP GEMMs m=8192 (k, n/G)",
-            "eb_us": eb_us, "eb_per_table_launches_us": eb_per_table_us, "eb_lookups": lookups, "eb_alg_gbs": alg / (eb_us * 1e-6) / 1e9,
-            "eb_hbm_frac": alg / (eb_us * 1e-6) / 1e9 / pk["hbm_gbs"],
-            "alltoall_send_bytes": int(send.numel() * 4 + send_f.numel()),
-            "mlp_us": mlp_us, "mlp_tops": ops / (mlp_us * 1e-6) / 1e12,
-            "note": "EB: the GPU's 8 tables in one abftlp_eb_group_checked_scatter launch, outputs straight into the all-to-all send buffer; at N=1 the "
-                    "exchange itself is not run (multi-rank path: paper_2103_00130_b200/sharded.py)"}
+    res = {
+        "workload": f"D5 = BASELINE configs[4] on {G} GPU(s): 64 tables x 1M x 128 int8 (table-wise, {len(mine)} per GPU), "
+                    f"batch {B}, pooling {pool}, Zipf(1.05); exchange to [B/G, 64, 128]; 9 checked MLP GEMMs m={m} "
+                    "(k, n/G), verdicts OR-reduced",
+        "n_gpus": G, "step_us": step_us, "step_how": how, "phase_us": phase_us,
+        "samples_per_s": B / (step_us * 1e-6),
+        "eb_lookups_per_gpu": lookups_rank, "eb_alg_gbs_per_gpu": alg_eb / (phase_us["eb_lookups"] * 1e-6) / 1e9,
+        "eb_hbm_frac": alg_eb / (phase_us["eb_lookups"] * 1e-6) / 1e9 / pk["hbm_gbs"],
+        "exchange_bytes_out_per_gpu": x_bytes,
+        "exchange_gbs_per_gpu": x_bytes / (phase_us["exchange"] * 1e-6) / 1e9 if G > 1 else None,
+        "mlp_tops_per_gpu": ops / (phase_us["mlp"] * 1e-6) / 1e12,
+        "mlp_hbm_frac": mlp_alg / (phase_us["mlp"] * 1e-6) / 1e9 / pk["hbm_gbs"],
+        "flagged_bags_rank0_slice": flagged_eb, "flagged_mlp_rows": flagged_mlp,
+        "group_fused": bool(group_ok),
+    }
+    del tables, bags, eb
+    torch.cuda.empty_cache()
+    return res
 
 
 def eb_secondary(L, dev, st, vp, pk):
@@ -877,6 +1092,13 @@ def eb_secondary(L, dev, st, vp, pk):
     return out
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -885,9 +1107,21 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-eb", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-d5", action="store_true")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` outside a launcher: re-run as N ranks, one process per GPU, exactly as the
+        # driver's torchrun launch does (rendezvous on 127.0.0.1)
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+        os.execvpe(sys.executable, cmd, env)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} rank(s)", file=sys.stderr)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
@@ -895,9 +1129,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank count) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
+        print(f"[bench] rank {rank}: torch.distributed nccl world_size={tdist.get_world_size()} "
+              f"device={torch.cuda.get_device_name(local)}:{local}", file=sys.stderr, flush=True)
     run_gpu_arm(args, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()

@@ -244,6 +244,14 @@ void abftlp_eb_group_free(abftlp_eb_group* g);
 abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
                                               uint64_t flag_ld, uint64_t bags_per_dest, uint32_t* d_flag_count,
                                               int32_t* d_status, abftlp_stream stream);
+/* The same lookups without the check (embedding_bag, P:src/embedding_abft.cpp:47-60): the ABFT-overhead baseline. */
+abftlp_status abftlp_eb_group_unchecked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
+                                                uint64_t bags_per_dest, int32_t* d_status, abftlp_stream stream);
+/* Re-point a group at new bags (per table: device CSR offsets, indices, optional weights) without rebuilding it;
+ * stream-ordered, so later launches on `stream` pool the new bags (a training step's fresh indices). */
+abftlp_status abftlp_eb_group_set_bags(abftlp_eb_group* g, const int64_t* const* d_offsets,
+                                       const int64_t* const* d_indices, const float* const* d_weights /* nullable */,
+                                       abftlp_stream stream);
 
 /* ------------------------------------------------------------------ fault injection */
 /* XOR bit `bit` of element `index` of an array of `elem_bytes`-wide integers

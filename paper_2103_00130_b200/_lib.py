@@ -129,6 +129,8 @@ _SIGS = {
     "abftlp_gemm_weight_col_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_group_create": (i32, [vp, u32, vp, vp, vp, vp, vp, vp]),
     "abftlp_eb_group_checked_scatter": (i32, [vp, u64, u64, u64, u64, vp, vp, vp]),
+    "abftlp_eb_group_unchecked_scatter": (i32, [vp, u64, u64, u64, vp, vp]),
+    "abftlp_eb_group_set_bags": (i32, [vp, vp, vp, vp, vp]),
     "abftlp_eb_checked_scatter": (i32, [vp, vp, vp, u64, vp, vp, u64, vp, u64, u64, vp, vp, vp]),
     "abftlp_flip_bit": (i32, [vp, u32, u64, u32, vp]),
     "abftlp_gemm_weight_flip_bit": (i32, [vp, u64, u64, u32, vp]),

@@ -20,6 +20,15 @@ struct CudaError : std::exception {
 void cuda_check(cudaError_t e, const char* what);
 #define ABFT_CUDA(call) ::abftk::cuda_check((call), #call)
 
+// Kernel attributes (dynamic shared-memory limit) and occupancy are per device; one process may drive several
+// GPUs, so launchers remember them per device ordinal.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return d;
+}
+
 // ------------------------------------------------------------------ GEMM
 constexpr int kBM = 128;      // rows of A per CTA; a CTA pair covers 256 rows (tcgen05 cta_group::2, M=256)
 constexpr int kPairM = 256;

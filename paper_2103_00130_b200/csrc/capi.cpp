@@ -777,6 +777,26 @@ void abftlp_eb_group_free(abftlp_eb_group* g) {
     delete g;
 }
 
+abftlp_status abftlp_eb_group_set_bags(abftlp_eb_group* g, const int64_t* const* d_offsets,
+                                       const int64_t* const* d_indices, const float* const* d_weights,
+                                       abftlp_stream stream) {
+    if (!g || !d_offsets || !d_indices) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_group_set_bags(*g->g, d_offsets, d_indices, d_weights, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_eb_group_unchecked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
+                                                uint64_t bags_per_dest, int32_t* d_status, abftlp_stream stream) {
+    if (!g) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::eb_group_run(*g->g, static_cast<int64_t>(bags_per_table), static_cast<int64_t>(ld_out), 1,
+                            static_cast<int64_t>(bags_per_dest), false, nullptr, d_status, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
 abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t bags_per_table, uint64_t ld_out,
                                               uint64_t flag_ld, uint64_t bags_per_dest, uint32_t* d_flag_count,
                                               int32_t* d_status, abftlp_stream stream) {

@@ -972,16 +972,19 @@ static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t s
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
     constexpr int smem = 8 * static_cast<int>(sizeof(AsyncStage<BPL>));
     auto kern = eb_bag_async_kernel<ELEM, SCALE, CPL, WPB, W, CK>;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[kMaxDevices] = {};  // per device
+    static int per_sm_dev[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!attr[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[dev] = true;
     }
-    static int per_sm = 0;
+    int& per_sm = per_sm_dev[dev];
     if (!per_sm) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-        if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+        int o = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, smem);
+        per_sm = (e != cudaSuccess || o < 1) ? 1 : o;
     }
     const int64_t need = (p.num_bags + (8 / WPB) - 1) / (8 / WPB);
     const int64_t cap = static_cast<int64_t>(per_sm) * device_sm_count();
@@ -1163,6 +1166,27 @@ cudaError_t launch_eb_pack(const uint8_t* data, int64_t rows, int64_t row_bytes,
     eb_pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(data, rows, row_bytes, row_stride,
                                                                   reinterpret_cast<const uint8_t*>(meta), meta_bytes,
                                                                   meta_off, rec_stride, packed);
+    return cudaGetLastError();
+}
+
+// Sum of n per-launch counters into *dst (grouped tables run as one launch per table).
+__global__ void sum_u32_kernel(const uint32_t* __restrict__ src, int64_t n, uint32_t* __restrict__ dst) {
+    uint32_t s = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += src[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ uint32_t part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+        *dst = t;
+    }
+}
+
+cudaError_t launch_sum_u32(const uint32_t* src, int64_t n, uint32_t* dst, cudaStream_t st) {
+    sum_u32_kernel<<<1, 256, 0, st>>>(src, n, dst);
     return cudaGetLastError();
 }
 

@@ -146,8 +146,8 @@ __global__ void read_encoded_kernel(const int8_t* __restrict__ bt, const int8_t*
 }
 
 // ============================================================ checksum GEMV share
-// sum_{p in [k0, k1)} A[row][p] * cs[p], exact in 32 bits (A <= 255, cs <= 126, k < 65793 as the
-// reference's int32 accumulation). 16-byte loads (lda % 16 == 0), four u8 x u8 dot products per dp4a.
+// sum_{p in [k0, k1)} A[row][p] * cs[p], exact in 32 bits (A <= 255, |cs| <= 128, k < 65793 as the
+// reference's int32 accumulation). 16-byte loads (lda % 16 == 0), four u8 x s8 dot products per dp4a.
 __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int b, int row, int k0, int k1) {
     const uint8_t* arow = p.a + b * p.a_bstride + static_cast<int64_t>(row) * p.lda;
     const int8_t* cs = p.cs + b * p.cs_bstride;
@@ -160,13 +160,13 @@ __device__ __forceinline__ uint32_t csum_share(const GemmParams& p, int b, int r
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint4 cv = __ldg(reinterpret_cast<const uint4*>(cs + kk + 16 * u));
-            s = __dp4a(av[u].x, cv.x, s);
-            s = __dp4a(av[u].y, cv.y, s);
-            s = __dp4a(av[u].z, cv.z, s);
-            s = __dp4a(av[u].w, cv.w, s);
+            s = dp4a_us(av[u].x, cv.x, s);
+            s = dp4a_us(av[u].y, cv.y, s);
+            s = dp4a_us(av[u].z, cv.z, s);
+            s = dp4a_us(av[u].w, cv.w, s);
         }
     }
-    for (; kk < k1; ++kk) s += static_cast<uint32_t>(arow[kk]) * static_cast<uint32_t>(static_cast<uint8_t>(cs[kk]));
+    for (; kk < k1; ++kk) s += static_cast<uint32_t>(static_cast<int32_t>(arow[kk]) * static_cast<int32_t>(cs[kk]));
     return s;
 }
 
@@ -251,10 +251,10 @@ __device__ void gemv_helper(const GemmParams& p, int helper_cta, int helper_ctas
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        part[j] = __dp4a(av[j][c].x, cv[c].x, part[j]);
-                        part[j] = __dp4a(av[j][c].y, cv[c].y, part[j]);
-                        part[j] = __dp4a(av[j][c].z, cv[c].z, part[j]);
-                        part[j] = __dp4a(av[j][c].w, cv[c].w, part[j]);
+                        part[j] = dp4a_us(av[j][c].x, cv[c].x, part[j]);
+                        part[j] = dp4a_us(av[j][c].y, cv[c].y, part[j]);
+                        part[j] = dp4a_us(av[j][c].z, cv[c].z, part[j]);
+                        part[j] = dp4a_us(av[j][c].w, cv[c].w, part[j]);
                     }
             }
 #pragma unroll
@@ -874,11 +874,12 @@ static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap
                               const GemmParams& p, cudaStream_t st) {
     using Cfg = PairCfg<BN, EW>;
     auto kern = gemm_pair_kernel<BN, CHECKED, EPI, EW>;
-    static bool attr_done = false;  // benign race: idempotent attribute set
-    if (!attr_done) {
+    static bool attr_done[kMaxDevices] = {};  // per device; benign race: idempotent attribute set
+    const int dev = current_device();
+    if (!attr_done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        attr_done[dev] = true;
     }
     static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
     cudaLaunchConfig_t cfg = {};

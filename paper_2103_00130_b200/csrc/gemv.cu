@@ -17,12 +17,6 @@ namespace abftk {
 
 constexpr int kGemvWarps = 8;
 
-__device__ __forceinline__ uint32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, uint32_t c) {
-    uint32_t d;
-    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_u8x4), "r"(b_s8x4), "r"(c));
-    return d;
-}
-
 template <int MR, bool CHECKED>
 __global__ void __launch_bounds__(32 * kGemvWarps) gemv_checked_kernel(const GemmParams p, const int8_t* __restrict__ bt,
                                                                        int64_t n_pad) {
@@ -127,7 +121,7 @@ __global__ void __launch_bounds__(32 * kGemvWarps) gemv_checked_kernel(const Gem
                 } else {
                     for (int e = 0; e < 4 && q + e < p.k; ++e) c4 |= static_cast<uint32_t>(static_cast<uint8_t>(p.cs[q + e])) << (8 * e);
                 }
-                cs_part = __dp4a(a4, c4, cs_part);  // cs in [0, 126]: unsigned x unsigned is exact
+                cs_part = dp4a_us(a4, c4, cs_part);  // cs is s8 (negative after a sign-bit flip)
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cs_part += __shfl_xor_sync(0xffffffffu, cs_part, o);
@@ -170,11 +164,12 @@ static cudaError_t launch_gemv_mr(const GemmParams& p, const GemmWeight& w, cuda
     while (ks < 8 && ncg * ks * 2 <= 2 * 148 && p.k_blocks >= ks * 2) ks *= 2;
     const int smem = MR * p.k_blocks * kBK + kGemvWarps * MR * 32 * 4 + ks * MR * 32 * 4;
     auto kern = gemv_checked_kernel<MR, CK>;
-    static int attr_smem = 0;  // benign race: idempotent
-    if (smem > 48 * 1024 && smem > attr_smem) {
+    static int attr_smem[kMaxDevices] = {};  // per device; benign race: idempotent
+    const int dev = current_device();
+    if (smem > 48 * 1024 && smem > attr_smem[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr_smem = smem;
+        attr_smem[dev] = smem;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(ncg * ks));

@@ -11,6 +11,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// u8 x s8 dot product of four byte pairs, accumulated into 32 bits (two's complement): the checksum column
+// B'[:, n] = cs is int8 in the reference (P:src/gemm_abft.hpp:19-23), so a flipped sign bit or caller-supplied
+// negative checksums must multiply as signed values, exactly as the tensor-core path (B' column n, s8) does.
+__device__ __forceinline__ uint32_t dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, uint32_t c) {
+    uint32_t d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_u8x4), "r"(b_s8x4), "r"(c));
+    return d;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -24,13 +24,14 @@ void cuda_check(cudaError_t e, const char* what) {
 static int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 int device_sm_count() {
-    static int sms = [] {
-        int dev = 0, n = 0;
-        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static int sms[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!sms[dev]) {
+        int n = 0;
         cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
-        return n;
-    }();
-    return sms;
+        sms[dev] = n;
+    }
+    return sms[dev];
 }
 
 // ------------------------------------------------------------------ tensor maps
@@ -84,7 +85,9 @@ static Workspace& ws_for(cudaStream_t st) {
     auto* w = new Workspace();
     w->device = dev;
     cuda_check(cudaMalloc(&w->small, 64 * sizeof(uint32_t)), "cudaMalloc(workspace)");
-    cuda_check(cudaMemset(w->small, 0, 64 * sizeof(uint32_t)), "cudaMemset(workspace)");
+    // zeroed on the stream the kernels using it run on (a legacy-stream memset is not ordered before work on
+    // a non-blocking stream)
+    cuda_check(cudaMemsetAsync(w->small, 0, 64 * sizeof(uint32_t), st), "cudaMemsetAsync(workspace)");
     g_ws[key] = w;
     return *w;
 }
@@ -98,7 +101,7 @@ static void grow(T*& ptr, int64_t& cap, int64_t need, cudaStream_t st) {
         cuda_check(cudaFree(ptr), "cudaFree");
     }
     cuda_check(cudaMalloc(&ptr, ncap * sizeof(T)), "cudaMalloc(workspace)");
-    cuda_check(cudaMemset(ptr, 0, ncap * sizeof(T)), "cudaMemset(workspace)");
+    cuda_check(cudaMemsetAsync(ptr, 0, ncap * sizeof(T), st), "cudaMemsetAsync(workspace)");
     cap = ncap;
 }
 
@@ -515,6 +518,14 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         if (f == 4 || (f == 8 && t.epi == kEpiTmaStore)) ew = f;
     }
     p.row_arrivals = static_cast<int>(n_tiles) * (ew / 4) + p.gemv_helpers;
+    // the arrival count is a 12-bit field of the per-row accumulator (kRowAcc*): more would carry into the
+    // checksum bits. Two epilogue groups double the arrivals; fall back to one group before refusing.
+    if (checked && p.row_arrivals > kMaxCheckedNTiles && ew == 8) {
+        ew = 4;
+        p.row_arrivals = static_cast<int>(n_tiles) + p.gemv_helpers;
+    }
+    if (checked && p.row_arrivals > kMaxCheckedNTiles)
+        throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
     if (p.gemv_helpers) pairs = all_pairs;
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, ew, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
@@ -738,13 +749,13 @@ EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const in
         throw std::invalid_argument("null argument");
     std::vector<EbTableDesc> h(static_cast<size_t>(ntables));
     const bool weighted = d_weights != nullptr && d_weights[0] != nullptr;
+    bool fused = !std::getenv("ABFTLP_EB_GROUP_UNFUSED");
     for (int64_t i = 0; i < ntables; ++i) {
         const EbTable* t = tables[i];
         if (!t || !d_offsets[i] || !d_indices[i] || !d_out_dest[i] || !d_flag_dest[i])
             throw std::invalid_argument("null argument");
-        if (t->elem != tables[0]->elem || t->scale_type != tables[0]->scale_type || t->dim != tables[0]->dim ||
-            (t->packed != nullptr) != (tables[0]->packed != nullptr))
-            throw std::invalid_argument("eb_group: tables must share element type, scale type, dim and layout");
+        if (t->elem != tables[0]->elem || t->scale_type != tables[0]->scale_type || t->dim != tables[0]->dim)
+            throw std::invalid_argument("eb_group: tables must share element type, scale type and dim");
         if (weighted != (d_weights != nullptr && d_weights[i] != nullptr))
             throw std::invalid_argument("eb_group: either every table or none has weights");
         h[i] = eb_desc(*t);
@@ -753,14 +764,23 @@ EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const in
         h[i].weights = weighted ? d_weights[i] : nullptr;
         h[i].out_dest = d_out_dest[i];
         h[i].flag_dest = d_flag_dest[i];
+        // the fused launch runs the 16-byte cp.async gather kernel for every table with table 0's strides
+        const bool al = (reinterpret_cast<uintptr_t>(h[i].data) % 16) == 0 && (h[i].row_stride % 16) == 0 &&
+                        (reinterpret_cast<uintptr_t>(h[i].meta) % 16) == 0;
+        fused = fused && al && t->dim % 32 == 0 && h[i].row_stride == h[0].row_stride &&
+                h[i].meta_stride == h[0].meta_stride && (t->packed != nullptr) == (tables[0]->packed != nullptr);
     }
     auto* g = new EbGroup();
     g->tables.assign(tables, tables + ntables);
+    g->host = h;
     g->weighted = weighted;
+    g->fused = fused;
     cudaError_t e = cudaMalloc(&g->d_desc, sizeof(EbTableDesc) * h.size());
     if (e == cudaSuccess) e = cudaMemcpy(g->d_desc, h.data(), sizeof(EbTableDesc) * h.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !fused) e = cudaMalloc(&g->d_counts, sizeof(uint32_t) * h.size());
     if (e != cudaSuccess) {
         cudaFree(g->d_desc);
+        cudaFree(g->d_counts);
         delete g;
         cuda_check(e, "eb_group_create");
     }
@@ -770,7 +790,26 @@ EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const in
 void eb_group_free(EbGroup* g) {
     if (!g) return;
     cudaFree(g->d_desc);
+    cudaFree(g->d_counts);
     delete g;
+}
+
+void eb_group_set_bags(EbGroup& g, const int64_t* const* d_offsets, const int64_t* const* d_indices,
+                       const float* const* d_weights, cudaStream_t st) {
+    if (!d_offsets || !d_indices) throw std::invalid_argument("null argument");
+    const bool weighted = d_weights != nullptr && d_weights[0] != nullptr;
+    if (weighted != g.weighted) throw std::invalid_argument("eb_group: either every table or none has weights");
+    for (size_t i = 0; i < g.host.size(); ++i) {
+        if (!d_offsets[i] || !d_indices[i]) throw std::invalid_argument("null argument");
+        if (weighted != (d_weights != nullptr && d_weights[i] != nullptr))
+            throw std::invalid_argument("eb_group: either every table or none has weights");
+        g.host[i].offsets = d_offsets[i];
+        g.host[i].indices = d_indices[i];
+        g.host[i].weights = weighted ? d_weights[i] : nullptr;
+    }
+    // pageable source: the call returns once the descriptors are staged, the copy itself is ordered on `st`
+    cuda_check(cudaMemcpyAsync(g.d_desc, g.host.data(), sizeof(EbTableDesc) * g.host.size(), cudaMemcpyHostToDevice, st),
+               "cudaMemcpyAsync(eb group descriptors)");
 }
 
 void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int64_t flag_ld, int64_t bags_per_dest,
@@ -783,9 +822,25 @@ void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int6
         if (checked && d_flag_count) cuda_check(cudaMemsetAsync(d_flag_count, 0, 4, st), "cudaMemsetAsync");
         return;
     }
+    if (!g.fused) {
+        // one scatter launch per table (same per-bag math and destinations), flag counts summed on the device
+        for (size_t i = 0; i < g.tables.size(); ++i) {
+            const EbTableDesc& d = g.host[i];
+            EbScatter sc;
+            sc.out_dest = d.out_dest;
+            sc.flag_dest = d.flag_dest;
+            sc.bags_per_dest = bags_per_dest;
+            sc.flag_ld = flag_ld;
+            eb_run(*g.tables[i], d.offsets, d.indices, bags_per_table, d.weights, nullptr, ld_out, checked, nullptr,
+                   nullptr, nullptr, checked ? g.d_counts + i : nullptr, d_status, st, &sc);
+        }
+        if (checked && d_flag_count)
+            cuda_check(launch_sum_u32(g.d_counts, static_cast<int64_t>(g.tables.size()), d_flag_count, st), "sum_u32_kernel");
+        return;
+    }
     Workspace& ws = ws_for(st);
     std::lock_guard<std::mutex> lk(ws.mu);
-    const EbTableDesc d0 = eb_desc(t0);
+    const EbTableDesc& d0 = g.host[0];
     EbParams p{};
     p.data = d0.data;  // table 0's layout (shared by the group) drives the kernel choice
     p.meta = d0.meta;

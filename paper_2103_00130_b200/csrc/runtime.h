@@ -102,13 +102,23 @@ int64_t eb_elem_row_bytes(int elem, int64_t dim);
 // count per table), scatter destinations and optional weights, in ONE persistent launch (D5: a GPU's tables).
 struct EbGroup {
     std::vector<const EbTable*> tables;
+    std::vector<EbTableDesc> host;  // per-table descriptors (host copy)
     EbTableDesc* d_desc = nullptr;  // device copy of the per-table descriptors
     bool weighted = false;
+    // fused: ONE persistent launch over all tables (every table's rows and metadata 16-byte aligned with equal
+    // strides, dim % 32 == 0 -- the cp.async kernel's contract). Otherwise the group runs as one scatter launch
+    // per table (any layout the single-table path takes) and d_counts gathers their flag counts.
+    bool fused = true;
+    uint32_t* d_counts = nullptr;
 };
 EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const int64_t* const* d_offsets,
                          const int64_t* const* d_indices, const float* const* d_weights, float* const* const* d_out_dest,
                          uint8_t* const* const* d_flag_dest);
 void eb_group_free(EbGroup* g);
+// Re-point the group's tables at new bags (CSR offsets / indices / optional weights) without rebuilding it: the
+// device descriptors are rewritten with a stream-ordered copy, so later launches on `st` see the new bags.
+void eb_group_set_bags(EbGroup& g, const int64_t* const* d_offsets, const int64_t* const* d_indices,
+                       const float* const* d_weights, cudaStream_t st);
 void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int64_t flag_ld, int64_t bags_per_dest,
                   bool checked, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st);
 
@@ -148,6 +158,7 @@ cudaError_t launch_set_random(void* cell, int width, uint64_t state, cudaStream_
 cudaError_t launch_nonzero(const uint32_t* value, uint8_t* out, int64_t slot, cudaStream_t st);
 cudaError_t launch_any_flag(const uint8_t* flags, int64_t n, uint8_t* out, int64_t slot, cudaStream_t st);
 cudaError_t launch_flush(void* buf, int64_t bytes, int salt, cudaStream_t st);
+cudaError_t launch_sum_u32(const uint32_t* src, int64_t n, uint32_t* dst, cudaStream_t st);
 cudaError_t launch_gather_probe(const void* table, int64_t rec_bytes, const int64_t* idx, int64_t n, uint32_t* sink,
                                 cudaStream_t st);
 

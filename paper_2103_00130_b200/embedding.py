@@ -244,6 +244,78 @@ def eb_group_scatter(tables: list, bags: list, out_dests: list, flag_dests: list
     return cnt
 
 
+class EbGroupPlan:
+    """A GPU's tables pooled in ONE launch into FIXED destinations (abftlp_eb_group_*), for a step that repeats:
+    built once, then every call only re-points the tables at that call's bags (abftlp_eb_group_set_bags, a
+    stream-ordered descriptor copy) when their device addresses changed. ``out_dests[i]`` / ``flag_dests[i]`` are
+    table i's per-destination device addresses (ints or tensors: their first element); bag b of table i goes to
+    destination ``b // bags_per_dest``, row ``b % bags_per_dest`` (stride ``ld_out`` floats / ``flag_ld`` bytes)."""
+
+    def __init__(self, tables: list, out_dests: list, flag_dests: list, ld_out: int, flag_ld: int, bags_per_dest: int):
+        self.tables = list(tables)
+        self.ld_out, self.flag_ld, self.bags_per_dest = int(ld_out), int(flag_ld), int(bags_per_dest)
+        dev = device()
+        addr = lambda t: t.data_ptr() if torch.is_tensor(t) else int(t)  # noqa: E731
+        self._optrs = [torch.tensor([addr(t) for t in od], dtype=torch.int64, device=dev) for od in out_dests]
+        self._fptrs = [torch.tensor([addr(t) for t in fd], dtype=torch.int64, device=dev) for fd in flag_dests]
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._grp = None
+        self._key = None
+        self._csr = None
+
+    def _arr(self, xs):
+        return (C.c_void_p * len(self.tables))(*xs)
+
+    def bind(self, bags: list, stream=None) -> int:
+        """Point the plan at `bags[i] = (offsets, indices, weights-or-None)` (device tensors are used in place)."""
+        csr = [(to_device(o, torch.int64), to_device(i, torch.int64), None if w is None else to_device(w, torch.float32))
+               for o, i, w in bags]
+        nb = int(csr[0][0].numel()) - 1
+        if len(csr) != len(self.tables) or any(int(o.numel()) - 1 != nb for o, _, _ in csr):
+            raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "eb_group: every table needs the same bag count")
+        P = C.c_void_p
+        key = tuple((o.data_ptr(), i.data_ptr(), 0 if w is None else w.data_ptr()) for o, i, w in csr)
+        offs = self._arr([P(o.data_ptr()) for o, _, _ in csr])
+        idxs = self._arr([P(i.data_ptr()) if i.numel() else P(8) for _, i, _ in csr])
+        wts = None if csr[0][2] is None else self._arr([P(w.data_ptr()) for _, _, w in csr])
+        if self._grp is None:
+            grp = C.c_void_p()
+            _lib.call("abftlp_eb_group_create", self._arr([t.handle for t in self.tables]), len(self.tables), offs, idxs,
+                      wts, self._arr([P(o.data_ptr()) for o in self._optrs]),
+                      self._arr([P(f.data_ptr()) for f in self._fptrs]), C.byref(grp))
+            self._grp = grp
+        elif key != self._key:
+            _lib.call("abftlp_eb_group_set_bags", self._grp, offs, idxs, wts, stream_handle(stream))
+        self._key, self._csr, self.nb = key, csr, nb  # keep the bags alive while the plan points at them
+        return nb
+
+    def launch(self, checked: bool = True, stream=None) -> None:
+        """Pool the bound bags (no host synchronisation; errors are reported in ``status``)."""
+        if checked:
+            _lib.call("abftlp_eb_group_checked_scatter", self._grp, self.nb, self.ld_out, self.flag_ld,
+                      self.bags_per_dest, ptr(self.count), ptr(self.status), stream_handle(stream))
+        else:
+            _lib.call("abftlp_eb_group_unchecked_scatter", self._grp, self.nb, self.ld_out, self.bags_per_dest,
+                      ptr(self.status), stream_handle(stream))
+
+    def raise_on_status(self) -> None:
+        if int(self.status.item()) & 1:
+            self.status.zero_()
+            raise IndexError("embedding_bag: index out of range")
+
+    def __call__(self, bags: list, checked: bool = True, stream=None) -> torch.Tensor:
+        self.bind(bags, stream)
+        self.launch(checked, stream)
+        self.raise_on_status()
+        return self.count
+
+    def __del__(self):
+        if getattr(self, "_grp", None) is not None and _lib.lib is not None:
+            _lib.lib.abftlp_eb_group_free(self._grp)
+            self._grp = None
+
+
 def embedding_bag(table: QuantEmbeddingTable, bag: IndexBag) -> torch.Tensor:
     """Plain pooled lookup, fp32 accumulation (P:src/embedding_abft.cpp:47-60)."""
     off, idx, w = _csr([bag])

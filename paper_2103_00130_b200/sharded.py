@@ -7,11 +7,11 @@ for the plumbing (NCCL on GPUs; gloo in the CPU tests).
   (P:src/gemm_abft.cpp:113-124) because the fault perturbs only its shard's row sum. C stays sharded.
 * EmbeddingBag shards table-wise: table t lives on rank t % G with its row sums. Each rank pools its
   tables for the whole batch, and the pooled vectors + verdicts are transposed to batch-sharded
-  [B/G, T, d] by ONE all_to_all_single. On the GPU the lookup kernel writes every bag straight into its
-  destination slot of the exchange buffer (abftlp_eb_checked_scatter), so no gather/copy kernel sits
-  between the lookups and the collective; with NVLink peer mappings the same kernel can target the
-  peers' receive buffers directly. Per-bag math is unchanged by sharding, so outputs and verdicts are
-  bit-identical to one GPU.
+  [B/G, T, d] by ONE all_to_all_single of a buffer carrying both. On the GPU one grouped lookup launch
+  writes every bag straight into its destination slot of that buffer (abftlp_eb_group_checked_scatter),
+  so no gather/copy kernel sits between the lookups and the collective; with exchange="peer" the same
+  launch writes into the owning ranks' final buffers over NVLink and there is no collective at all.
+  Per-bag math is unchanged by sharding, so outputs and verdicts are bit-identical to one GPU.
 
 The compute backend is pluggable only so the host logic can be tested on CPU processes; the default
 backends are the CUDA library (there is no CPU fallback in the product path).
@@ -92,53 +92,62 @@ def local_tables(num_tables: int, world: int, rank: int) -> list[int]:
     return list(range(rank, num_tables, world))
 
 
+# The exchange buffer of the NCCL path carries each pooled vector followed by a 16-byte "flag quad" whose first
+# byte is the bag's verdict, so ONE all-to-all moves vectors and verdicts together and the rows stay 16-byte
+# aligned: x[g, b, slot, :d] = pooled vector, byte 4*d of x[g, b, slot] = flag.
+FLAG_QUAD = 4  # floats
+
+
 class GpuEbBackend:
-    """The CUDA library. `run_into` pools one table's bags straight into the exchange buffer slots."""
+    """The CUDA library: a rank's tables in ONE persistent grouped launch (abftlp_eb_group_*) whose kernel writes
+    every bag straight into its destination slot -- the NCCL exchange buffer, or the peers' final buffers."""
 
-    def run_into(self, table, offsets, indices, weights, send, send_flags, slot: int) -> None:
-        from .embedding import eb_csr_scatter
-        G, Bg, Tg, d = (int(s) for s in send.shape)
-        outs = [send[g, 0, slot] for g in range(G)]
-        flags = [send_flags[g, 0, slot:] for g in range(G)]
-        eb_csr_scatter(table, offsets, indices, weights, outs, flags, ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
+    def __init__(self):
+        self.plan = None
 
-    def run_all_into(self, tables: list, bags: list, send, send_flags) -> None:
-        """All local tables (slot order) in ONE launch when they share type and dim (abftlp_eb_group_*)."""
-        from .embedding import eb_group_scatter
-        G, Bg, Tg, d = (int(s) for s in send.shape)
-        same = len({(t.elem, t.scale_dtype, t.dim()) for t in tables}) == 1 and \
-            len({w is None for _, _, w in bags}) == 1
-        if len(tables) < 2 or not same:
-            for slot, (table, (off, idx, w)) in enumerate(zip(tables, bags)):
-                self.run_into(table, off, idx, w, send, send_flags, slot)
-            return
-        outs = [[send[g, 0, slot] for g in range(G)] for slot in range(len(tables))]
-        flags = [[send_flags[g, 0, slot:] for g in range(G)] for slot in range(len(tables))]
-        eb_group_scatter(tables, bags, outs, flags, ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
+    def pool(self, tables: list, bags: list, out_dests: list, flag_dests: list, ld_out: int, flag_ld: int,
+             bags_per_dest: int, stream=None):
+        from .embedding import EbGroupPlan
+        if self.plan is None:
+            self.plan = EbGroupPlan(tables, out_dests, flag_dests, ld_out, flag_ld, bags_per_dest)
+        self.plan.bind(bags, stream)
+        self.plan.launch(True, stream)
+
+    def raise_on_status(self):
+        if self.plan is not None:
+            self.plan.raise_on_status()
+
+    # NCCL path: slot s of this rank -> x[g, :, s] for every destination rank g
+    def pool_into(self, tables: list, bags: list, x: torch.Tensor, d: int, stream=None):
+        G, Bg, Tg, D4 = (int(v) for v in x.shape)
+        base = x.data_ptr()
+        row = lambda g, s: base + ((g * Bg * Tg) + s) * D4 * 4  # noqa: E731  (byte address of x[g, 0, s, 0])
+        outs = [[row(g, s) for g in range(G)] for s in range(len(tables))]
+        flags = [[row(g, s) + 4 * d for g in range(G)] for s in range(len(tables))]
+        self.pool(tables, bags, outs, flags, ld_out=Tg * D4, flag_ld=Tg * D4 * 4, bags_per_dest=Bg, stream=stream)
 
 
 class PeerExchange:
-    """The table-wise all-to-all fused into the lookups over NVLink peer memory: every rank's receive
-    buffers [G, B/G, Tg, d] (+ flags) live in symmetric memory, and rank r's grouped lookup kernel writes bag b of
-    its table slot s straight into destination rank g = b // (B/G)'s buffer at [r, b % (B/G), s] -- no send buffer,
-    no separate all-to-all; one device-side barrier orders the peers' writes before the consumer reads."""
+    """The table-wise all-to-all fused into the lookups over NVLink peer memory: every rank's FINAL
+    buffers -- pooled vectors [B/G, T, d] and verdicts [B/G, T] of its samples -- live in symmetric memory, and
+    rank r's grouped lookup kernel writes bag b of table t straight into rank g = b // (B/G)'s out[b % (B/G), t]:
+    no send buffer, no collective, no reassembly. One device-side barrier before the launch (every peer has
+    consumed the previous step's outputs) and one after (all peers' writes landed) order the exchange."""
 
-    def __init__(self, G: int, Bg: int, Tg: int, d: int, group, device):
+    def __init__(self, Bg: int, T: int, d: int, group, device):
         import torch.distributed._symmetric_memory as symm
-        self.G, self.Bg, self.Tg, self.d = G, Bg, Tg, d
-        self.recv = symm.empty(G, Bg, Tg, d, dtype=torch.float32, device=device)
-        self.recv_f = symm.empty(G, Bg, Tg, dtype=torch.uint8, device=device)
+        self.Bg, self.T, self.d = Bg, T, d
+        self.out = symm.empty(Bg, T, d, dtype=torch.float32, device=device)
+        self.flags = symm.empty(Bg, T, dtype=torch.uint8, device=device)
         name = (group or dist.group.WORLD).group_name
-        self.h = symm.rendezvous(self.recv, name)
-        self.hf = symm.rendezvous(self.recv_f, name)
+        self.h = symm.rendezvous(self.out, name)
+        self.hf = symm.rendezvous(self.flags, name)
         self.rank = self.h.rank
 
-    def destinations(self, slot: int):
-        """Per destination rank g: the address of peer g's recv[rank, 0, slot] (pooled rows) and recv_f[...] (flags)."""
-        r, Bg, Tg, d = self.rank, self.Bg, self.Tg, self.d
-        outs = [int(p) + ((r * Bg) * Tg + slot) * d * 4 for p in self.h.buffer_ptrs]
-        flags = [int(p) + (r * Bg) * Tg + slot for p in self.hf.buffer_ptrs]
-        return outs, flags
+    def destinations(self, t: int):
+        """Per destination rank g: the address of peer g's out[0, t] (pooled rows) and flags[0, t] (verdicts)."""
+        return ([int(p) + t * self.d * 4 for p in self.h.buffer_ptrs],
+                [int(p) + t for p in self.hf.buffer_ptrs])
 
     def barrier(self):
         self.h.barrier()
@@ -147,7 +156,12 @@ class PeerExchange:
 class ShardedEmbeddingBags:
     """Table-wise sharded checked EmbeddingBag for a batch of `batch` samples over `num_tables` tables.
     `tables` maps this rank's table ids (t % G == rank) to their tables. Returns, for this rank's slice of
-    the batch (samples [rank*B/G, (rank+1)*B/G)), pooled outputs [B/G, T, d] and verdicts [B/G, T]."""
+    the batch (samples [rank*B/G, (rank+1)*B/G)), pooled outputs [B/G, T, d] and verdicts [B/G, T].
+
+    exchange="nccl": the grouped lookup kernel writes into a persistent exchange buffer [G, B/G, Tg, d + 4]
+    (vector + flag quad), ONE all_to_all_single moves it, and one copy kernel reorders the received slots into
+    table order (table t = slot * G + g). exchange="peer": the kernel writes into the owners' final buffers over
+    NVLink (PeerExchange); the returned tensors are views of those buffers, valid until the next call."""
 
     def __init__(self, tables: dict, num_tables: int, batch: int, dim: int, group=None, backend=None,
                  device: torch.device | str | None = None, exchange: str = "nccl"):
@@ -159,58 +173,68 @@ class ShardedEmbeddingBags:
         if sorted(tables) != mine:
             raise ValueError(f"ShardedEmbeddingBags: rank {self.rank} must own tables {mine}")
         self.tables, self.T, self.B, self.d = tables, num_tables, batch, dim
+        self.order = sorted(tables)
         self.Tg = -(-num_tables // self.world)  # slots per rank (padded when T % G != 0)
         self.backend = backend or GpuEbBackend()
         self.device = torch.device(device) if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
         if exchange not in ("nccl", "peer"):
             raise ValueError("ShardedEmbeddingBags: exchange must be 'nccl' or 'peer'")
-        # "peer": lookups write straight into the destination ranks' symmetric buffers (GPU backend only)
-        self.peer = PeerExchange(self.world, self.B // self.world, self.Tg, dim, group, self.device) \
-            if exchange == "peer" else None
+        G, Bg = self.world, self.B // self.world
+        self.peer = None
+        if exchange == "peer":  # lookups write straight into the destination ranks' final buffers (GPU backend only)
+            self.peer = PeerExchange(Bg, num_tables, dim, group, self.device)
+        else:  # persistent exchange buffers; flag quads zeroed once (only their first byte is ever written)
+            self.xsend = torch.zeros((G, Bg, self.Tg, dim + FLAG_QUAD), dtype=torch.float32, device=self.device)
+            self.xrecv = torch.zeros_like(self.xsend) if G > 1 else self.xsend
+            self.out = torch.empty((Bg, self.Tg, G, dim), dtype=torch.float32, device=self.device)
+            self.flags = torch.empty((Bg, self.Tg, G), dtype=torch.uint8, device=self.device)
 
-    def __call__(self, bags: dict) -> tuple[torch.Tensor, torch.Tensor]:
+    def __call__(self, bags: dict, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
         """bags[t] = (offsets[B+1], indices, weights-or-None) for every local table t."""
-        G, Bg, Tg, d = self.world, self.B // self.world, self.Tg, self.d
-        order = sorted(self.tables)
-        for t in order:
+        try:
+            return self.launch(bags, stream)
+        finally:
+            self.backend.raise_on_status()  # (after the exchange: a failing rank never strands its peers)
+
+    def launch(self, bags: dict, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+        """The step without any host synchronisation (CUDA-graph capturable once bound): lookups, exchange and
+        reordering are enqueued; index errors are left in the backend's status word."""
+        for t in self.order:
             if len(bags[t][0]) != self.B + 1:
                 raise ValueError("ShardedEmbeddingBags: every table needs one bag per sample")
+        tabs = [self.tables[t] for t in self.order]
+        tbags = [bags[t] for t in self.order]
         if self.peer is not None:  # lookups + exchange in one grouped launch over peer memory
-            from .embedding import eb_group_scatter
-            dst = [self.peer.destinations(slot) for slot in range(len(order))]
+            dst = [self.peer.destinations(t) for t in self.order]
             self.peer.barrier()  # every peer has consumed its previous exchange before it is overwritten
-            eb_group_scatter([self.tables[t] for t in order], [bags[t] for t in order], [o for o, _ in dst],
-                             [f for _, f in dst], ld_out=Tg * d, flag_ld=Tg, bags_per_dest=Bg)
-            self.peer.barrier()
-            return self._gather(self.peer.recv, self.peer.recv_f)
-        send = torch.zeros((G, Bg, Tg, d), dtype=torch.float32, device=self.device)
-        send_f = torch.zeros((G, Bg, Tg), dtype=torch.uint8, device=self.device)
-        if hasattr(self.backend, "run_all_into"):  # all local tables in one launch
-            self.backend.run_all_into([self.tables[t] for t in order], [bags[t] for t in order], send, send_f)
-        else:
-            for slot, t in enumerate(order):
-                off, idx, w = bags[t]
-                self.backend.run_into(self.tables[t], off, idx, w, send, send_f, slot)
-        if G > 1:
-            recv = torch.empty_like(send)
-            recv_f = torch.empty_like(send_f)
-            dist.all_to_all_single(recv, send, group=self.group)
-            dist.all_to_all_single(recv_f, send_f, group=self.group)
-        else:
-            recv, recv_f = send, send_f
-        return self._gather(recv, recv_f)
+            try:
+                self.backend.pool(tabs, tbags, [o for o, _ in dst], [f for _, f in dst], ld_out=self.T * self.d,
+                                  flag_ld=self.T, bags_per_dest=self.B // self.world, stream=stream)
+            finally:
+                self.peer.barrier()  # always reached, so a failing rank cannot strand its peers in the barrier
+            return self.peer.out, self.peer.flags
+        self.backend.pool_into(tabs, tbags, self.xsend, self.d, stream=stream)
+        if self.world > 1:
+            dist.all_to_all_single(self.xrecv, self.xsend, group=self.group)
+        return unpack_exchange(self.xrecv, self.T, self.d, self.out, self.flags)
 
-    def _gather(self, recv, recv_f):
-        """[G, B/G, Tg, d] received slots -> this rank's samples [B/G, T, d] in table order."""
-        G, Bg, d = self.world, self.B // self.world, self.d
-        out = torch.empty((Bg, self.T, d), dtype=torch.float32, device=self.device)
-        flags = torch.empty((Bg, self.T), dtype=torch.uint8, device=self.device)
-        for g in range(G):
-            for slot, t in enumerate(local_tables(self.T, G, g)):
-                out[:, t] = recv[g, :, slot]
-                flags[:, t] = recv_f[g, :, slot]
-        return out, flags
+
+def unpack_exchange(x: torch.Tensor, T: int, d: int, out: torch.Tensor | None = None,
+                    flags: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Received exchange buffer [G, B/G, Tg, d + 4] (slot s of sender g = table s * G + g) -> this rank's samples
+    [B/G, T, d] and verdicts [B/G, T] in table order: the (slot, g) -> t transpose is one permuted copy each."""
+    G, Bg, Tg = (int(v) for v in x.shape[:3])
+    if out is None:
+        out = torch.empty((Bg, Tg, G, d), dtype=torch.float32, device=x.device)
+    if flags is None:
+        flags = torch.empty((Bg, Tg, G), dtype=torch.uint8, device=x.device)
+    out.copy_(x[..., :d].permute(1, 2, 0, 3))
+    flags.copy_(x.view(torch.uint8)[..., 4 * d].permute(1, 2, 0))
+    o, f = out.view(Bg, Tg * G, d), flags.view(Bg, Tg * G)
+    if Tg * G != T:
+        o, f = o[:, :T], f[:, :T]
+    return o, f
 
 
 def sample_slice(batch: int, world: int, rank: int) -> slice:
@@ -219,4 +243,5 @@ def sample_slice(batch: int, world: int, rank: int) -> slice:
 
 
 __all__: Sequence[str] = ["column_shard", "ShardedAbftGemm", "ShardedGemmResult", "GpuGemmBackend", "table_owner",
-                          "local_tables", "GpuEbBackend", "ShardedEmbeddingBags", "sample_slice"]
+                          "local_tables", "GpuEbBackend", "PeerExchange", "ShardedEmbeddingBags", "sample_slice",
+                          "FLAG_QUAD", "unpack_exchange"]

@@ -298,3 +298,27 @@ def test_production_path_agrees_with_dual_encoded_oracle(G):  # P:tests/test_gem
         dual[i, j] += after - before
         assert O.dual_check(dual) == (1, i, j)
         assert G.verify_checksums(res.cTemp) > 0
+
+
+@pytest.mark.parametrize("m,n,k,tiling,helpers", [(5, 300, 520, None, "1"), (16, 256, 1024, None, "1"),
+                                                  (300, 512, 1000, "128", "0"), (300, 500, 1000, "128", "0"),
+                                                  (8192, 64, 2048, None, "1"), (8192, 64, 2048, "64", "0")])
+def test_checksum_sign_bit_flip_all_paths(G, m, n, k, tiling, helpers, monkeypatch):
+    """A flipped sign bit of checksum-column elements (inject_weight_B at j == n; B' is int8, so cs becomes
+    negative) multiplies as a SIGNED value on every path that forms C'[:, n]: the small-m GEMV, the epilogue's
+    CUDA-core share (n % BN == 0), the tensor-core column (n % BN != 0) and the idle-pair GEMV helpers. C' and
+    the verdicts equal the oracle's abft_gemm with the same corrupted checksums."""
+    if tiling:
+        monkeypatch.setenv("ABFTLP_GEMM_TILING", tiling)
+    monkeypatch.setenv("ABFTLP_GEMV_HELPERS", helpers)
+    a, b = rnd(m * 7 + n + k, m, n, k)
+    pb = G.PackedEncodedWeight(b)
+    cs = O.row_checksums(b).copy()
+    for i in (0, k // 3, k - 1):
+        pb.flip_bit(i, n, 7)
+        cs[i] = np.int8(np.uint8(cs[i].view(np.uint8) ^ 0x80).view(np.int8))
+        assert pb.at(i, n) == int(cs[i]) < 0
+    res = G.abft_gemm(a, pb)
+    ct, fl, err = O.abft_gemm(a, b, cs=cs)
+    assert np.array_equal(res.cTemp.data.cpu().numpy(), ct)
+    assert np.array_equal(res.rowFlags.cpu().numpy(), fl) and res.errCount == err

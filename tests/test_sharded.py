@@ -43,13 +43,21 @@ class OracleGemmBackend:
 
 
 class OracleEbBackend:
-    def run_into(self, table, offsets, indices, weights, send, send_flags, slot):
+    """Writes the exchange buffer exactly as the GPU grouped scatter launch does: x[g, b, slot, :d] = pooled vector
+    of sample g*Bg + b, byte 4*d of x[g, b, slot] = its verdict (the flag quad)."""
+
+    def pool_into(self, tables, bags, x, d, stream=None):
         import oracle_api as O
-        rows, sc, bi, sums = table
-        r, _, _, e = O.eb(rows, sc, bi, offsets, indices, weights, row_sums_=sums)
-        G, Bg, _, d = send.shape
-        send[:, :, slot, :] = torch.from_numpy(r).view(G, Bg, d)
-        send_flags[:, :, slot] = torch.from_numpy(np.asarray(e, dtype=np.uint8)).view(G, Bg)
+        G, Bg = x.shape[0], x.shape[1]
+        xb = x.view(torch.uint8)
+        for slot, (table, (offsets, indices, weights)) in enumerate(zip(tables, bags)):
+            rows, sc, bi, sums = table
+            r, _, _, e = O.eb(rows, sc, bi, offsets, indices, weights, row_sums_=sums)
+            x[:, :, slot, :d] = torch.from_numpy(r).view(G, Bg, d)
+            xb[:, :, slot, 4 * d] = torch.from_numpy(np.asarray(e, dtype=np.uint8)).view(G, Bg)
+
+    def raise_on_status(self):
+        pass
 
 
 # ---------------------------------------------------------------- workers
