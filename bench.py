@@ -877,11 +877,15 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
         del bfull, bsh
 
     def phase_eb():
-        eb.backend.pool_into([tables[t] for t in eb.order], [bags[t] for t in eb.order], eb.xsend, d)
+        if eb.local is not None:  # one GPU: the grouped lookups write the final [B, 64, 128] layout directly
+            eb.launch(bags)
+        else:
+            eb.backend.pool_into([tables[t] for t in eb.order], [bags[t] for t in eb.order], eb.xsend, d)
 
     def phase_x():
-        if G > 1:
-            dist.all_to_all_single(eb.xrecv, eb.xsend)
+        if eb.local is not None:
+            return eb.local
+        dist.all_to_all_single(eb.xrecv, eb.xsend)
         return S.unpack_exchange(eb.xrecv, T, d, eb.out, eb.flags)
 
     def phase_mlp():
@@ -915,50 +919,47 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
         step()
     sync_all()
     eb.backend.raise_on_status()
-    # per-phase device times (eager, events on the step's stream)
-    phase_us = {}
-    for name, fn in (("eb_lookups", phase_eb), ("exchange", phase_x), ("mlp", phase_mlp), ("verdict_or", phase_or)):
+
+    def graph_us(fn, reps):
+        """Median device time of fn replayed as a CUDA graph (eager when capture fails), max over ranks."""
+        sync_all()
+        g, how = None, "CUDA graph replay"
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            g.replay()
+            sync_all()
+        except Exception as e:  # noqa: BLE001  (capture unsupported here: time it eagerly)
+            g, how = None, f"eager (graph capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
+        run = g.replay if g is not None else fn
         ts = []
-        for _ in range(5):
+        for _ in range(reps):
             sync_all()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            fn()
+            run()
             e1.record(stream)
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) * 1e3)
-        phase_us[name] = maxr(statistics.median(ts[1:]))
-    # the whole step, replayed as a CUDA graph when the step (incl. NCCL) captures
-    graph, how = None, "eager"
-    try:
-        sync_all()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            step()
-        g.replay()
-        sync_all()
-        graph, how = g, "CUDA graph replay"
-    except Exception as e:  # noqa: BLE001  (capture unsupported here: time the eager step)
-        how = f"eager (graph capture failed: {type(e).__name__})"
-        torch.cuda.synchronize()
-    run = graph.replay if graph is not None else step
-    ts = []
-    for _ in range(steps):
-        sync_all()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ts.append(maxr(e0.elapsed_time(e1) * 1e3))
-    step_us = statistics.median(ts)
+            ts.append(maxr(e0.elapsed_time(e1) * 1e3))
+        del g
+        return statistics.median(ts), how
+
+    # per-phase device times (each phase captured alone), then the whole step
+    phase_us = {}
+    for name, fn in (("eb_lookups", phase_eb), ("exchange", phase_x), ("mlp", phase_mlp), ("verdict_or", phase_or)):
+        phase_us[name] = graph_us(fn, 5)[0]
+    step_us, how = graph_us(step, steps)
     sync_all()
     flagged_mlp = int(mflags.to(torch.int64).sum().item())
-    out, fl = S.unpack_exchange(eb.xrecv, T, d, eb.out, eb.flags)
+    out, fl = phase_x()
     flagged_eb = int(fl.to(torch.int64).sum().item())
     lookups_rank = len(mine) * B * pool
+    # per lookup: the 128-B row, its 16-B metadata record (scale, bias, row sum), the 8-B index; per bag: offsets and
+    # the pooled vector (+ its verdict quad in the exchange layout)
     alg_eb = lookups_rank * (d + 16 + 8) + len(mine) * (8 * (B + 1) + 4 * B * (d + S.FLAG_QUAD))
-    x_bytes = int(eb.xsend.numel() * 4 * (G - 1) // max(G, 1))
+    x_bytes = int(eb.xsend.numel() * 4 * (G - 1) // G) if eb.local is None else 0
     ops = sum(2 * m * n_loc * k for k, n_loc, *_ in mlp)
     mlp_alg = sum(m * k + k * (n_loc + 1) + 4 * m * (n_loc + 1) + m for k, n_loc, *_ in mlp)
     for k, n_loc, w, *_ in mlp:

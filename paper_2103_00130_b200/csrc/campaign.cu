@@ -26,60 +26,6 @@ namespace abftk {
 
 namespace {
 
-std::string trim(const std::string& s) {
-    const size_t a = s.find_first_not_of(" \t\r\n");
-    if (a == std::string::npos) return "";
-    const size_t b = s.find_last_not_of(" \t\r\n");
-    return s.substr(a, b - a + 1);
-}
-
-uint64_t parse_u64(const std::string& key, const std::string& v) {
-    try {
-        size_t pos = 0;
-        const unsigned long long r = std::stoull(v, &pos);
-        if (pos != v.size()) throw std::invalid_argument(v);
-        return r;
-    } catch (const std::exception&) {
-        throw std::invalid_argument("campaign config: bad integer for '" + key + "': " + v);
-    }
-}
-
-GemmShape parse_shape(const std::string& s) {
-    std::istringstream in(s);
-    GemmShape sh;
-    char x1 = 0, x2 = 0;
-    if (!(in >> sh.m >> x1 >> sh.n >> x2 >> sh.k) || x1 != 'x' || x2 != 'x' || sh.m == 0 || sh.n == 0 || sh.k == 0)
-        throw std::invalid_argument("campaign config: bad shape '" + s + "' (want MxNxK)");
-    return sh;
-}
-
-FaultTarget parse_target(const std::string& v) {
-    if (v == "weight_b") return FaultTarget::weight_B;
-    if (v == "intermediate_c") return FaultTarget::intermediate_C;
-    if (v == "eb_table") return FaultTarget::eb_table;
-    if (v == "none") return FaultTarget::none;
-    throw std::invalid_argument("campaign config: unknown fault target '" + v + "'");
-}
-
-const char* target_name(FaultTarget t) {
-    switch (t) {
-        case FaultTarget::weight_B: return "weight_b";
-        case FaultTarget::intermediate_C: return "intermediate_c";
-        case FaultTarget::eb_table: return "eb_table";
-        case FaultTarget::none: return "none";
-    }
-    return "?";
-}
-const char* model_name(FaultModel m) { return m == FaultModel::single_bit_flip ? "single_bit_flip" : "random_value"; }
-const char* range_name(BitRange r) {
-    switch (r) {
-        case BitRange::all: return "all";
-        case BitRange::high4: return "high4";
-        case BitRange::low4: return "low4";
-    }
-    return "?";
-}
-
 // draw_bit_index (P:src/fault_lab.cpp:89-96)
 unsigned draw_bit(SplitMix64& rng, BitRange range, unsigned width) {
     switch (range) {
@@ -108,6 +54,34 @@ struct DevBuf {
     }
 };
 
+// The campaign report from per-trial verdicts: trials [g * per_group, (g+1) * per_group) form row g. A trial's
+// verdict counts as a detection, or -- for the control campaign (target none) -- as a false positive.
+template <typename Flag>
+CampaignReport tally(const FaultSpec& spec, const std::vector<Flag>& verdicts, const std::vector<std::string>& labels,
+                     uint64_t per_group, std::string notes) {
+    CampaignReport rep;
+    rep.target = fault_target_name(spec.target);
+    rep.model = fault_model_name(spec.model);
+    rep.bitRange = bit_range_name(spec.bitRange);
+    rep.notes = std::move(notes);
+    const bool control = spec.target == FaultTarget::none;
+    rep.perShape.resize(labels.size());
+    for (size_t g = 0; g < labels.size(); ++g) {
+        ShapeStats& row = rep.perShape[g];
+        row.label = labels[g];
+        row.trials = per_group;
+        const uint64_t hits = static_cast<uint64_t>(
+            std::count_if(verdicts.begin() + g * per_group, verdicts.begin() + (g + 1) * per_group,
+                          [](Flag f) { return f != 0; }));
+        (control ? row.falsePositives : row.detected) = hits;
+        rep.trials += row.trials;
+        rep.detected += row.detected;
+        rep.falsePositives += row.falsePositives;
+    }
+    rep.notDetected = rep.trials - rep.detected;
+    return rep;
+}
+
 struct StreamGuard {
     cudaStream_t s = nullptr;
     StreamGuard() { ABFT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -119,140 +93,7 @@ struct StreamGuard {
     }
 };
 
-std::string csv_row(const CampaignReport& rep, const std::string& label, uint64_t trials, uint64_t detected,
-                    uint64_t fp) {
-    std::ostringstream out;
-    const double rate = trials ? static_cast<double>(detected) / static_cast<double>(trials) : 0.0;
-    const WilsonInterval ci = wilson_interval(detected, trials);
-    out << rep.target << ',' << rep.model << ',' << rep.bitRange << ',' << label << ',' << trials << ',' << detected
-        << ',' << (trials - detected) << ',' << fp << ',' << std::setprecision(10) << rate << ',' << ci.low << ','
-        << ci.high << '\n';
-    return out.str();
-}
-
 }  // namespace
-
-// ============================================================ config (P:src/campaign_config.cpp:62-154)
-CampaignConfig parse_campaign_config(const std::string& text) {
-    CampaignConfig cfg;
-    std::string section;
-    std::map<std::string, std::string> values;
-    std::istringstream in(text);
-    std::string line;
-    while (std::getline(in, line)) {
-        const size_t hash = line.find('#');
-        if (hash != std::string::npos) line.erase(hash);
-        line = trim(line);
-        if (line.empty()) continue;
-        if (line.front() == '[') {
-            if (line.back() != ']') throw std::invalid_argument("campaign config: malformed section '" + line + "'");
-            section = trim(line.substr(1, line.size() - 2));
-            continue;
-        }
-        const size_t eq = line.find('=');
-        if (eq == std::string::npos)
-            throw std::invalid_argument("campaign config: expected key=value, got '" + line + "'");
-        values[(section.empty() ? "" : section + ".") + trim(line.substr(0, eq))] = trim(line.substr(eq + 1));
-    }
-    auto take = [&](const std::string& key) -> std::optional<std::string> {
-        auto it = values.find(key);
-        if (it == values.end()) return std::nullopt;
-        std::string v = it->second;
-        values.erase(it);
-        return v;
-    };
-    auto require = [&](const std::string& key) {
-        auto v = take(key);
-        if (!v) throw std::invalid_argument("campaign config: missing '" + key + "'");
-        return *v;
-    };
-    if (auto t = take("threads")) cfg.threads = parse_u64("threads", *t);
-    const std::string kind = require("workload.kind");
-    if (kind == "gemm") {
-        GemmWorkload wl;
-        wl.trialsPerShape = parse_u64("trials_per_shape", require("workload.trials_per_shape"));
-        std::istringstream shapes(require("workload.shapes"));
-        std::string item;
-        while (std::getline(shapes, item, ',')) {
-            item = trim(item);
-            if (!item.empty()) wl.shapes.push_back(parse_shape(item));
-        }
-        if (wl.shapes.empty()) throw std::invalid_argument("campaign config: workload.shapes is empty");
-        cfg.gemm = wl;
-    } else if (kind == "eb") {
-        EbWorkload wl;
-        wl.tableRows = parse_u64("table_rows", require("workload.table_rows"));
-        wl.tableDim = parse_u64("table_dim", require("workload.table_dim"));
-        wl.pooling = parse_u64("pooling", require("workload.pooling"));
-        wl.batch = parse_u64("batch", require("workload.batch"));
-        wl.trials = parse_u64("trials", require("workload.trials"));
-        cfg.eb = wl;
-    } else {
-        throw std::invalid_argument("campaign config: unknown workload.kind '" + kind + "'");
-    }
-    cfg.fault.target = parse_target(require("fault.target"));
-    if (auto m = take("fault.model")) {
-        if (*m == "single_bit_flip")
-            cfg.fault.model = FaultModel::single_bit_flip;
-        else if (*m == "random_value")
-            cfg.fault.model = FaultModel::random_value;
-        else
-            throw std::invalid_argument("campaign config: unknown fault model '" + *m + "'");
-    }
-    if (auto r = take("fault.bit_range")) {
-        if (*r == "all")
-            cfg.fault.bitRange = BitRange::all;
-        else if (*r == "high4")
-            cfg.fault.bitRange = BitRange::high4;
-        else if (*r == "low4")
-            cfg.fault.bitRange = BitRange::low4;
-        else
-            throw std::invalid_argument("campaign config: unknown bit_range '" + *r + "'");
-    }
-    if (auto s = take("fault.seed")) cfg.fault.seed = parse_u64("seed", *s);
-    if (!values.empty()) throw std::invalid_argument("campaign config: unknown key '" + values.begin()->first + "'");
-    return cfg;
-}
-
-// ============================================================ reports (P:src/campaign_config.cpp:164-195)
-WilsonInterval wilson_interval(uint64_t successes, uint64_t trials) {
-    if (trials == 0) throw std::invalid_argument("wilson_interval: zero trials");
-    const double z = 1.959963984540054;
-    const double n = static_cast<double>(trials);
-    const double p = static_cast<double>(successes) / n;
-    const double z2 = z * z;
-    const double denom = 1.0 + z2 / n;
-    const double center = (p + z2 / (2.0 * n)) / denom;
-    const double half = z * std::sqrt(p * (1.0 - p) / n + z2 / (4.0 * n * n)) / denom;
-    return {std::max(0.0, center - half), std::min(1.0, center + half)};
-}
-
-std::string report_to_csv(const CampaignReport& rep) {
-    std::string out =
-        "target,model,bit_range,shape_or_dims,trials,detected,not_detected,false_positives,detection_rate,ci_low,"
-        "ci_high\n";
-    for (const ShapeStats& st : rep.perShape) out += csv_row(rep, st.label, st.trials, st.detected, st.falsePositives);
-    if (rep.perShape.size() > 1) out += csv_row(rep, "total", rep.trials, rep.detected, rep.falsePositives);
-    return out;
-}
-
-std::string report_to_table(const CampaignReport& rep) {
-    std::ostringstream out;
-    out << "campaign: target=" << rep.target << " model=" << rep.model << " bit_range=" << rep.bitRange << "\n";
-    if (!rep.notes.empty()) out << "note: " << rep.notes << "\n";
-    out << std::left << std::setw(24) << "shape_or_dims" << std::right << std::setw(8) << "trials" << std::setw(10)
-        << "detected" << std::setw(8) << "fp" << std::setw(10) << "rate" << std::setw(18) << "wilson95\n";
-    auto row = [&](const std::string& label, uint64_t trials, uint64_t detected, uint64_t fp) {
-        const double rate = trials ? static_cast<double>(detected) / static_cast<double>(trials) : 0.0;
-        const WilsonInterval ci = wilson_interval(detected, trials);
-        out << std::left << std::setw(24) << label << std::right << std::setw(8) << trials << std::setw(10) << detected
-            << std::setw(8) << fp << std::setw(10) << std::fixed << std::setprecision(4) << rate << "   [" << ci.low
-            << ", " << ci.high << "]\n";
-    };
-    for (const ShapeStats& st : rep.perShape) row(st.label, st.trials, st.detected, st.falsePositives);
-    if (rep.perShape.size() > 1) row("total", rep.trials, rep.detected, rep.falsePositives);
-    return out.str();
-}
 
 // ============================================================ GEMM campaign (P:src/fault_lab.cpp:168-225)
 CampaignReport run_gemm_campaign(const CampaignConfig& cfg) {
@@ -320,31 +161,10 @@ CampaignReport run_gemm_campaign(const CampaignConfig& cfg) {
     ABFT_CUDA(cudaMemcpyAsync(h.data(), errs.p, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     ABFT_CUDA(cudaStreamSynchronize(st));
 
-    CampaignReport rep;
-    rep.target = target_name(cfg.fault.target);
-    rep.model = model_name(cfg.fault.model);
-    rep.bitRange = range_name(cfg.fault.bitRange);
-    rep.notes = "checksum column excluded from weight_B injection";
-    const bool control = cfg.fault.target == FaultTarget::none;
-    for (size_t s = 0; s < wl.shapes.size(); ++s) {
-        ShapeStats ss;
-        const GemmShape& sh = wl.shapes[s];
-        ss.label = std::to_string(sh.m) + "x" + std::to_string(sh.n) + "x" + std::to_string(sh.k);
-        ss.trials = wl.trialsPerShape;
-        for (uint64_t t = 0; t < wl.trialsPerShape; ++t) {
-            const bool d = h[s * wl.trialsPerShape + t] > 0;
-            if (control)
-                ss.falsePositives += d;
-            else
-                ss.detected += d;
-        }
-        rep.perShape.push_back(ss);
-        rep.trials += ss.trials;
-        rep.detected += ss.detected;
-        rep.falsePositives += ss.falsePositives;
-    }
-    rep.notDetected = rep.trials - rep.detected;
-    return rep;
+    std::vector<std::string> labels;
+    for (const GemmShape& sh : wl.shapes)
+        labels.push_back(std::to_string(sh.m) + "x" + std::to_string(sh.n) + "x" + std::to_string(sh.k));
+    return tally(cfg.fault, h, labels, wl.trialsPerShape, "checksum column excluded from weight_B injection");
 }
 
 // ============================================================ EB campaign (P:src/fault_lab.cpp:227-285)
@@ -406,27 +226,9 @@ CampaignReport run_eb_campaign(const CampaignConfig& cfg) {
     ABFT_CUDA(cudaStreamSynchronize(st));
     if (table.meta) cudaFree(table.meta);
 
-    CampaignReport rep;
-    rep.target = target_name(cfg.fault.target);
-    rep.model = model_name(cfg.fault.model);
-    rep.bitRange = range_name(cfg.fault.bitRange);
-    ShapeStats ss;
-    ss.label = "R" + std::to_string(wl.tableRows) + "_d" + std::to_string(wl.tableDim) + "_p" +
-               std::to_string(wl.pooling) + "_b" + std::to_string(wl.batch);
-    ss.trials = wl.trials;
-    const bool control = cfg.fault.target == FaultTarget::none;
-    for (uint8_t f : h) {
-        if (control)
-            ss.falsePositives += f;
-        else
-            ss.detected += f;
-    }
-    rep.perShape.push_back(ss);
-    rep.trials = ss.trials;
-    rep.detected = ss.detected;
-    rep.falsePositives = ss.falsePositives;
-    rep.notDetected = rep.trials - rep.detected;
-    return rep;
+    const std::string label = "R" + std::to_string(wl.tableRows) + "_d" + std::to_string(wl.tableDim) + "_p" +
+                              std::to_string(wl.pooling) + "_b" + std::to_string(wl.batch);
+    return tally(cfg.fault, h, {label}, wl.trials, "");
 }
 
 CampaignReport run_campaign(const CampaignConfig& cfg) {
@@ -573,102 +375,6 @@ BenchTimes bench_eb(uint64_t rows, uint64_t dim, uint64_t pooling, uint64_t batc
         abft.push_back(time_ns(st, ev, abft_run));
     }
     return {median(base), median(abft)};
-}
-
-// ============================================================ ABEB files (P:src/embedding_abft.cpp:93-145)
-namespace {
-template <typename T>
-T read_pod(std::ifstream& in) {
-    T v{};
-    in.read(reinterpret_cast<char*>(&v), sizeof(T));
-    if (!in) throw std::runtime_error("table file truncated");
-    return v;
-}
-}  // namespace
-
-HostTable load_table_file(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("cannot open table file: " + path);
-    char magic[4];
-    in.read(magic, 4);
-    if (!in || std::memcmp(magic, "ABEB", 4) != 0) throw std::runtime_error("not an embedding table file: " + path);
-    if (read_pod<uint16_t>(in) != 1) throw std::runtime_error("unsupported table file version");
-    HostTable t;
-    t.rows = read_pod<uint64_t>(in);
-    t.dim = read_pod<uint32_t>(in);
-    if (t.rows == 0 || t.dim == 0) throw std::runtime_error("table file has empty dimensions");
-    t.data.resize(t.rows * t.dim);
-    t.scales.resize(t.rows);
-    t.biases.resize(t.rows);
-    t.rowSums.resize(t.rows);
-    for (uint64_t i = 0; i < t.rows; ++i) {
-        in.read(reinterpret_cast<char*>(t.data.data() + i * t.dim), t.dim);
-        if (!in) throw std::runtime_error("table file truncated");
-        t.scales[i] = read_pod<float>(in);
-        t.biases[i] = read_pod<float>(in);
-    }
-    in.read(reinterpret_cast<char*>(t.rowSums.data()), static_cast<std::streamsize>(t.rows * 4));
-    if (!in) throw std::runtime_error("table file truncated");
-    return t;
-}
-
-void save_table_file(const HostTable& t, const std::string& path) {
-    std::ofstream out(path, std::ios::binary);
-    if (!out) throw std::runtime_error("cannot open table file for writing: " + path);
-    out.write("ABEB", 4);
-    const uint16_t ver = 1;
-    const uint64_t r = t.rows;
-    const uint32_t d = t.dim;
-    out.write(reinterpret_cast<const char*>(&ver), 2);
-    out.write(reinterpret_cast<const char*>(&r), 8);
-    out.write(reinterpret_cast<const char*>(&d), 4);
-    for (uint64_t i = 0; i < r; ++i) {
-        out.write(reinterpret_cast<const char*>(t.data.data() + i * d), d);
-        out.write(reinterpret_cast<const char*>(&t.scales[i]), 4);
-        out.write(reinterpret_cast<const char*>(&t.biases[i]), 4);
-    }
-    out.write(reinterpret_cast<const char*>(t.rowSums.data()), static_cast<std::streamsize>(r * 4));
-    if (!out) throw std::runtime_error("failed writing table file: " + path);
-}
-
-// Bag file: one bag per line, tokens "idx" or "idx:weight", '#' comments, blank lines skipped
-// (P:src/capi.cpp:198-227). A bag with any weighted token is weighted; its plain tokens weigh
-// 1.0f, which is bit-identical to the unweighted path, so the batch is uploaded as one CSR array.
-bool parse_bag_lines(std::istream& in, HostBags& bags, std::string& error) {
-    std::string line;
-    std::vector<float> w_all;
-    while (std::getline(in, line)) {
-        const size_t hash = line.find('#');
-        if (hash != std::string::npos) line.erase(hash);
-        std::istringstream ls(line);
-        std::vector<int64_t> idx;
-        std::vector<float> w;
-        bool weighted = false;
-        std::string tok;
-        while (ls >> tok) {
-            const size_t colon = tok.find(':');
-            try {
-                if (colon == std::string::npos) {
-                    idx.push_back(static_cast<int64_t>(std::stoull(tok)));
-                    w.push_back(1.0f);
-                } else {
-                    idx.push_back(static_cast<int64_t>(std::stoull(tok.substr(0, colon))));
-                    w.push_back(std::stof(tok.substr(colon + 1)));
-                    weighted = true;
-                }
-            } catch (const std::exception&) {
-                error = "bad index token: " + tok;
-                return false;
-            }
-        }
-        if (idx.empty() && line.find_first_not_of(" \t\r") == std::string::npos) continue;
-        bags.weighted |= weighted;
-        bags.indices.insert(bags.indices.end(), idx.begin(), idx.end());
-        w_all.insert(w_all.end(), w.begin(), w.end());
-        bags.offsets.push_back(static_cast<int64_t>(bags.indices.size()));
-    }
-    if (bags.weighted) bags.weights = std::move(w_all);
-    return true;
 }
 
 std::vector<EbResultHost> check_bags_on_device(const HostTable& t, const HostBags& bags, bool validate) {

@@ -53,7 +53,10 @@ struct WilsonInterval {
     double low = 0.0, high = 0.0;
 };
 
-CampaignConfig parse_campaign_config(const std::string& text);
+CampaignConfig parse_campaign_config(const std::string& text);  // hostio.cpp
+const char* fault_target_name(FaultTarget t);                    // spellings of the config file / report
+const char* fault_model_name(FaultModel m);
+const char* bit_range_name(BitRange r);
 CampaignReport run_campaign(const CampaignConfig& cfg);
 CampaignReport run_gemm_campaign(const CampaignConfig& cfg);
 CampaignReport run_eb_campaign(const CampaignConfig& cfg);

@@ -182,8 +182,12 @@ class ShardedEmbeddingBags:
             raise ValueError("ShardedEmbeddingBags: exchange must be 'nccl' or 'peer'")
         G, Bg = self.world, self.B // self.world
         self.peer = None
+        self.local = None
         if exchange == "peer":  # lookups write straight into the destination ranks' final buffers (GPU backend only)
             self.peer = PeerExchange(Bg, num_tables, dim, group, self.device)
+        elif G == 1 and hasattr(self.backend, "pool"):  # one rank: the lookups write the final layout directly
+            self.local = (torch.empty((Bg, num_tables, dim), dtype=torch.float32, device=self.device),
+                          torch.empty((Bg, num_tables), dtype=torch.uint8, device=self.device))
         else:  # persistent exchange buffers; flag quads zeroed once (only their first byte is ever written)
             self.xsend = torch.zeros((G, Bg, self.Tg, dim + FLAG_QUAD), dtype=torch.float32, device=self.device)
             self.xrecv = torch.zeros_like(self.xsend) if G > 1 else self.xsend
@@ -205,6 +209,12 @@ class ShardedEmbeddingBags:
                 raise ValueError("ShardedEmbeddingBags: every table needs one bag per sample")
         tabs = [self.tables[t] for t in self.order]
         tbags = [bags[t] for t in self.order]
+        if self.local is not None:  # world size 1: no exchange, bag b of table t -> out[b, t]
+            out, flags = self.local
+            self.backend.pool(tabs, tbags, [[out.data_ptr() + t * self.d * 4] for t in self.order],
+                              [[flags.data_ptr() + t] for t in self.order], ld_out=self.T * self.d, flag_ld=self.T,
+                              bags_per_dest=self.B, stream=stream)
+            return out, flags
         if self.peer is not None:  # lookups + exchange in one grouped launch over peer memory
             dst = [self.peer.destinations(t) for t in self.order]
             self.peer.barrier()  # every peer has consumed its previous exchange before it is overwritten
