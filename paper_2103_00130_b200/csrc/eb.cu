@@ -18,6 +18,7 @@
 //                   in the reference's sequential order otherwise -- bit-identical either way.
 #include <cuda_fp16.h>
 #include <cstdlib>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "abft_internal.h"
@@ -363,6 +364,19 @@ struct AsyncRing {
 #endif
     static constexpr int NST = SLICE <= 32 ? ABFT_EB_NST32 : SLICE <= 64 ? ABFT_EB_NST64 : SLICE <= 128 ? ABFT_EB_NST128 : 2;
 };
+// Per-lookup constants of the chunk being consumed, formed lane-parallel once per chunk (lane l: lookup l) so the
+// column loop reads them with two 16-byte shared loads and does no conversion work:
+//   s_lo/s_hi and c_lo/c_hi  the "splice" multipliers: a column value v (< 2^8) spliced into the mantissa of 2^23
+//                            as the float 2^23 + v' gives s*v in ONE rounding as fma(2^23 + v', s', -s'*2^23) when
+//                            s'*2^23 is exact (u8: v' = v, s' = s; u4 high nibble: v' = 16 v taken in place,
+//                            s' = s/16); s8 uses the magic subtraction instead (see the column loop)
+//   b, w                     bias and bag weight (1 when unweighted)
+//   term                     the lookup's cSum term (P:src/embedding_abft.cpp:69-76)
+struct __align__(16) LookupConst {
+    float s_lo, s_hi, c_lo, c_hi;
+    float b, w;
+    double term;
+};
 template <int BPL>
 struct AsyncStage {
     static constexpr int NST = AsyncRing<BPL>::NST;
@@ -370,8 +384,30 @@ struct AsyncStage {
     uint4 meta[NST][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B); zero = neutral slot
     float w[NST][kChunk];
     int64_t off[kChunk];                  // row byte offsets of the chunk being issued, -1 = none
-    double term[kChunk];                  // cSum terms of the chunk being consumed
+    LookupConst k[kChunk];                // constants of the chunk being consumed
 };
+
+// The splice multiplication is exact when s*2^23 and s/16 are exact normal floats (and s is finite); a zero scale
+// is fine too (every product is then +-0, and a signed zero term never changes a sum that starts at +0).
+__device__ __forceinline__ bool splice_safe(float s) {
+    const float a = fabsf(s);
+    return a == 0.0f || (a >= 0x1p-100f && a <= 0x1p100f);
+}
+// Columns c, c+1 of a lane word spliced for the FMA form (u4: low nibble v, high nibble 16 v in place; u8: bytes).
+template <int ELEM, typename W>
+__device__ __forceinline__ unsigned long long splice_pair_bits(W w, int c) {
+    if constexpr (ELEM == kEbU4) {
+        const uint32_t byte = static_cast<uint32_t>(w >> (4 * c)) & 0xFFu;
+        return static_cast<unsigned long long>(0x4B000000u | (byte & 0x0Fu)) |
+               (static_cast<unsigned long long>(0x4B000000u | (byte & 0xF0u)) << 32);
+    } else {
+        const uint32_t half = (sizeof(W) == 8 && c >= 4) ? static_cast<uint32_t>(static_cast<uint64_t>(w) >> 32)
+                                                         : static_cast<uint32_t>(w);
+        const uint32_t bsel = static_cast<uint32_t>(c & 3);
+        return static_cast<unsigned long long>(__byte_perm(half, 0x4B000000u, 0x7540u | bsel)) |
+               (static_cast<unsigned long long>(__byte_perm(half, 0x4B000000u, 0x7540u | (bsel + 1))) << 32);
+    }
+}
 
 template <int SCALE>
 __device__ __forceinline__ void smem_meta(const uint4& m, float& s, float& b, int32_t& rs) {
@@ -564,7 +600,7 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
                 if (lane < cnt && !valid) oob = true;
                 S.off[lane] = valid ? ix * tv.row_stride + slice_byte : -1;
                 if (valid) {
-                    if constexpr (SCALE == kEbF32)
+                    if (SCALE == kEbF32 || p.l2_only)  // (packed records leave 16 B after the f16 metadata)
                         cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
                     else
                         cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
@@ -579,7 +615,12 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
                     const int piece = lane + 32 * i;
                     const int r = piece / PIECES, q = piece % PIECES;
                     const int64_t o = S.off[r];
-                    if (o >= 0) cp_async16_l1(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
+                    if (o >= 0) {
+                        if (p.l2_only)
+                            cp_async16(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
+                        else
+                            cp_async16_l1(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
+                    }
                 }
                 __syncwarp();  // S.off is reused by the next issue
             }
@@ -611,82 +652,111 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
             if (tr && lane == 0 && ch == 0 && nb_done < 4) tr[2 + 3 * nb_done] = globaltimer();
             const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
             const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
-            if constexpr (CHECKED) {
-                if (slice == 0) {  // the chunk's cSum terms, lane-parallel (a neutral slot's term is +0.0)
-                    float s, b;
-                    int32_t rs;
-                    smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
-                    S.term[lane] = csum_term(s, b, rs, WEIGHTED ? S.w[sl][lane] : 1.0f, dd, WEIGHTED);
-                }
+            // the chunk's per-lookup constants, lane-parallel (a neutral slot has s = b = 0, w = 1: term +0.0)
+            bool fast;
+            {
+                float s, b;
+                int32_t rs;
+                smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
+                const float w = WEIGHTED ? S.w[sl][lane] : 1.0f;
+                LookupConst kc;
+                kc.s_lo = s;
+                kc.s_hi = ELEM == kEbU4 ? s * 0.0625f : s;
+                kc.c_lo = -(kc.s_lo * 8388608.0f);
+                kc.c_hi = -(kc.s_hi * 8388608.0f);
+                kc.b = b;
+                kc.w = w;
+                kc.term = (CHECKED && slice == 0) ? csum_term(s, b, rs, w, dd, WEIGHTED) : 0.0;
+                S.k[lane] = kc;
+                // u8 / u4 chunks whose every scale admits the exact splice FMA take the short column path
+                fast = ELEM != kEbS8 && __all_sync(0xffffffffu, splice_safe(s));
                 __syncwarp();
             }
             const int tmax = (cnt + 3) & ~3;  // slots cnt..tmax-1 are neutral
             // Four lookups per step with the instruction-level parallelism spelled out: every shared-memory
             // load of the four first, then their (independent) column values, then the accumulations in
             // lookup order -- the only loop-carried chains are the per-column fp32 adds and the cSum DADD.
+            // Per column, in the reference's rounding: x = s*q (one rounding), x += b, x *= w (weighted), r += x.
             using Word = typename LaneWord<BPL>::T;
             constexpr int NP = CPL >= 2 ? CPL / 2 : 1;
+            auto column_loop = [&](auto fast_tag) {
+                constexpr bool FAST = decltype(fast_tag)::value;
 #pragma unroll 1
-            for (int t0 = 0; t0 < tmax; t0 += 4) {
-                uint4 mt[4];
-                Word wd[4];
-                float wt[4];
-                double tm[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    mt[u] = S.meta[sl][t0 + u];
-                    wd[u] = lds_word<BPL>(&S.rows[sl][t0 + u][lane * BPL]);
-                    wt[u] = WEIGHTED ? S.w[sl][t0 + u] : 1.0f;
-                    if constexpr (CHECKED) tm[u] = S.term[t0 + u];
-                }
-                if constexpr (CPL >= 2) {
-                    unsigned long long xv[4][NP];
+                for (int t0 = 0; t0 < tmax; t0 += 4) {
+                    Word wd[4];
+                    float4 ka[4];   // s_lo, s_hi, c_lo, c_hi
+                    float4 kb[4];   // b, w, term
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        float s, b;
-                        int32_t rs;
-                        smem_meta<SCALE>(mt[u], s, b, rs);
-                        const unsigned long long s2 = f2_pack(s, s), b2 = f2_pack(b, b);
-                        const unsigned long long w2 = f2_pack(wt[u], wt[u]);
-#pragma unroll
-                        for (int c = 0; c < CPL; c += 2) {
-                            const unsigned long long q2 = f2_add(decode_pair_bits<ELEM>(wd[u], c), magic2);
-                            unsigned long long x2 = f2_add(f2_fma(s2, q2, nz2), b2);
-                            if constexpr (WEIGHTED) x2 = f2_fma(w2, x2, nz2);
-                            xv[u][c / 2] = x2;
-                        }
+                        wd[u] = lds_word<BPL>(&S.rows[sl][t0 + u][lane * BPL]);
+                        ka[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].s_lo);
+                        kb[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].b);
                     }
+                    if constexpr (CPL >= 2) {
+                        unsigned long long xv[4][NP];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned long long b2 = f2_pack(kb[u].x, kb[u].x);
+                            const unsigned long long w2 = f2_pack(kb[u].y, kb[u].y);
 #pragma unroll
-                        for (int c = 0; c < NP; ++c) acc2[c] = f2_add(acc2[c], xv[u][c]);
-                } else {
-                    float xv[4][CPL];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float s, b;
-                        int32_t rs;
-                        smem_meta<SCALE>(mt[u], s, b, rs);
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) {
-                            float x = __fadd_rn(__fmul_rn(s, decode_fast<ELEM>(wd[u], c)), b);
-                            if constexpr (WEIGHTED) x = __fmul_rn(wt[u], x);
-                            xv[u][c] = x;
+                            for (int c = 0; c < CPL; c += 2) {
+                                unsigned long long x2;
+                                if constexpr (FAST) {  // s*q in one FMA on the spliced column values
+                                    x2 = f2_fma(splice_pair_bits<ELEM>(wd[u], c), f2_pack(ka[u].x, ka[u].y),
+                                                f2_pack(ka[u].z, ka[u].w));
+                                } else {  // exact q by the magic subtraction, then s*q (fma with -0: no contraction)
+                                    const unsigned long long q2 = f2_add(decode_pair_bits<ELEM>(wd[u], c), magic2);
+                                    x2 = f2_fma(f2_pack(ka[u].x, ka[u].x), q2, nz2);
+                                }
+                                x2 = f2_add(x2, b2);
+                                if constexpr (WEIGHTED) x2 = f2_fma(w2, x2, nz2);
+                                xv[u][c / 2] = x2;
+                            }
                         }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int c = 0; c < NP; ++c) acc2[c] = f2_add(acc2[c], xv[u][c]);
+                    } else {
+                        float xv[4][CPL];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) {
+                                float x;
+                                if constexpr (FAST)
+                                    x = __fmaf_rn(__uint_as_float(static_cast<uint32_t>(splice_pair_bits<ELEM>(wd[u], c))),
+                                                  ka[u].x, ka[u].z);
+                                else
+                                    x = __fmul_rn(ka[u].x, decode_fast<ELEM>(wd[u], c));
+                                x = __fadd_rn(x, kb[u].x);
+                                if constexpr (WEIGHTED) x = __fmul_rn(kb[u].y, x);
+                                xv[u][c] = x;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+#pragma unroll
+                            for (int c = 0; c < CPL; ++c) acc[c] = __fadd_rn(acc[c], xv[u][c]);
                     }
+                    // cSum in the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), kept by every
+                    // lane of the slice-0 warp (same terms, same order, same value). A neutral slot's +0.0 term is
+                    // an exact no-op (cSum starts at +0.0 and never becomes -0.0 in round-to-nearest).
+                    if constexpr (CHECKED)
+                        if (slice == 0) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-#pragma unroll
-                        for (int c = 0; c < CPL; ++c) acc[c] = __fadd_rn(acc[c], xv[u][c]);
+                            for (int u = 0; u < 4; ++u)
+                                csum = __dadd_rn(csum, __hiloint2double(__float_as_int(kb[u].w), __float_as_int(kb[u].z)));
+                        }
                 }
-                // cSum in the reference's sequential fp64 order (P:src/embedding_abft.cpp:69-76), kept by every
-                // lane of the slice-0 warp (same terms, same order, same value). A neutral slot's +0.0 term is
-                // an exact no-op (cSum starts at +0.0 and never becomes -0.0 in round-to-nearest).
-                if constexpr (CHECKED)
-                    if (slice == 0) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) csum = __dadd_rn(csum, tm[u]);
-                    }
+            };
+            if constexpr (ELEM != kEbS8) {
+                if (fast)
+                    column_loop(std::true_type{});
+                else
+                    column_loop(std::false_type{});
+            } else {
+                column_loop(std::false_type{});
             }
             __syncwarp();  // slot `sl` may be refilled by a later issue
         }

@@ -49,6 +49,8 @@ elif cfg == "E3":
 else:
     R, d, nb, elem, sct = 8_000_000, 64, 4096, 2, 1
     lens = rng.integers(1, 151, nb)
+    if cfg == "E4sorted":  # the same bags, longest first (scheduling-order probe)
+        lens = np.sort(lens)[::-1].copy()
     if cfg == "E4fixed":  # same total lookups, every bag the mean length (load-balance probe)
         lens = np.full(nb, int(round(lens.mean())))
     if cfg == "E4short":  # same total lookups in 4x as many 4x shorter bags

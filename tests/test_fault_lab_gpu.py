@@ -62,11 +62,15 @@ def test_campaign_matches_reference_csv(F, ref):
         h, r = C.c_void_p(), C.c_void_p()
         assert R.abftlp_campaign_parse(text.encode(), C.byref(h)) == 0
         assert R.abftlp_campaign_run(h, C.byref(r)) == 0
+        mine = F.run_campaign(text)
         with tempfile.TemporaryDirectory() as d:
             p1, p2 = os.path.join(d, "ref.csv"), os.path.join(d, "mine.csv")
             R.abftlp_report_write_csv(r, p1.encode())
-            F.run_campaign(text).write_csv(p2)
+            mine.write_csv(p2)
             assert open(p1).read() == open(p2).read()
+        out = C.c_char_p()
+        assert R.abftlp_report_render(r, C.byref(out)) == 0
+        assert out.value.decode() == mine.render()  # the aligned table, byte for byte
 
 
 def test_workload_target_mismatch(F):  # P:tests/test_fault_lab.cpp:189-202
