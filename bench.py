@@ -875,6 +875,13 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
         er = torch.zeros(1, dtype=torch.int32, device=dev)
         mlp.append((k, n1 - n0, w, a, c, cs, er))
         del bfull, bsh
+    # the 9 MLP layers as ONE heterogeneous grouped launch (abftlp_gemm_group_*): same outputs as 9 launches
+    probs = (L.GemmProblem * len(mlp))()
+    for q, (k, n_loc, w, a, c, cs, er) in enumerate(mlp):
+        probs[q] = L.GemmProblem(a.data_ptr(), m, k, w.value, c.data_ptr(), n_loc, cs.data_ptr(), 1,
+                                 mflags[q].data_ptr(), er.data_ptr())
+    mlp_group = C.c_void_p()
+    L.call("abftlp_gemm_group_create", probs, len(mlp), 1, C.byref(mlp_group))
 
     def phase_eb():
         if eb.local is not None:  # one GPU: the grouped lookups write the final [B, 64, 128] layout directly
@@ -889,6 +896,9 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
         return S.unpack_exchange(eb.xrecv, T, d, eb.out, eb.flags)
 
     def phase_mlp():
+        L.call("abftlp_gemm_group_run", mlp_group, st)
+
+    def phase_mlp_separate():  # the same 9 checked GEMMs as 9 launches (what the grouped launch replaces)
         for q, (k, n_loc, w, a, c, cs, er) in enumerate(mlp):
             L.call("abftlp_gemm_checked", vp(a), m, k, w, vp(c), n_loc, vp(cs), 1, vp(mflags[q]), vp(er), None, st)
 
@@ -948,8 +958,17 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
 
     # per-phase device times (each phase captured alone), then the whole step
     phase_us = {}
-    for name, fn in (("eb_lookups", phase_eb), ("exchange", phase_x), ("mlp", phase_mlp), ("verdict_or", phase_or)):
+    for name, fn in (("eb_lookups", phase_eb), ("exchange", phase_x), ("mlp", phase_mlp),
+                     ("mlp_as_9_launches", phase_mlp_separate), ("verdict_or", phase_or)):
+        if name == "verdict_or" and G == 1:
+            phase_us[name] = 0.0  # no collective at one rank
+            continue
         phase_us[name] = graph_us(fn, 5)[0]
+    # the grouped MLP writes exactly what the 9 launches write (C', checksum column, verdicts)
+    c_sep = [c.clone() for *_x, c, _cs, _er in mlp]
+    phase_mlp()
+    torch.cuda.synchronize()
+    mlp_group_eq = all(torch.equal(c_sep[q], mlp[q][4]) for q in range(len(mlp)))
     step_us, how = graph_us(step, steps)
     sync_all()
     flagged_mlp = int(mflags.to(torch.int64).sum().item())
@@ -962,8 +981,10 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
     x_bytes = int(eb.xsend.numel() * 4 * (G - 1) // G) if eb.local is None else 0
     ops = sum(2 * m * n_loc * k for k, n_loc, *_ in mlp)
     mlp_alg = sum(m * k + k * (n_loc + 1) + 4 * m * (n_loc + 1) + m for k, n_loc, *_ in mlp)
+    L.lib.abftlp_gemm_group_free(mlp_group)
     for k, n_loc, w, *_ in mlp:
         L.lib.abftlp_gemm_weight_free(w)
+    shard = mlp_shard_leg(L, dev, st, vp, pk, graph_us) if G == 1 else None
     res = {
         "workload": f"D5 = BASELINE configs[4] on {G} GPU(s): 64 tables x 1M x 128 int8 (table-wise, {len(mine)} per GPU), "
                     f"batch {B}, pooling {pool}, Zipf(1.05); exchange to [B/G, 64, 128]; 9 checked MLP GEMMs m={m} "
@@ -975,13 +996,58 @@ def d5_leg(L, dev, st, vp, pk, rank, world, dist, steps=8):
         "exchange_bytes_out_per_gpu": x_bytes,
         "exchange_gbs_per_gpu": x_bytes / (phase_us["exchange"] * 1e-6) / 1e9 if G > 1 else None,
         "mlp_tops_per_gpu": ops / (phase_us["mlp"] * 1e-6) / 1e12,
+        "mlp_how": "the 9 checked layers in ONE heterogeneous grouped launch (abftlp_gemm_group_run); "
+                   "mlp_as_9_launches = the same GEMMs as 9 abftlp_gemm_checked launches",
+        "mlp_group_eq_separate": bool(mlp_group_eq),
+        "mlp_alg_bytes_per_gpu": mlp_alg,
         "mlp_hbm_frac": mlp_alg / (phase_us["mlp"] * 1e-6) / 1e9 / pk["hbm_gbs"],
         "flagged_bags_rank0_slice": flagged_eb, "flagged_mlp_rows": flagged_mlp,
         "group_fused": bool(group_ok),
     }
+    if shard is not None:
+        res["mlp_shard_g8"] = shard
     del tables, bags, eb
     torch.cuda.empty_cache()
     return res
+
+
+def mlp_shard_leg(L, dev, st, vp, pk, graph_us, G=8):
+    """One GPU's share of the D5 MLP at G=8 (the N-split layers m=8192, (k, n/8)), measured on this GPU: ONE grouped
+    launch vs 9 launches, against its HBM roof (A read once per layer, C' and verdicts written)."""
+    import torch
+    m = 8192
+    mlp, ws = [], []
+    for q, (k, n) in enumerate([(k, n // G) for k in (512, 1024, 2048) for n in (512, 1024, 2048)]):
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(7000 + q)
+        b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev, generator=gen)
+        a = torch.randint(0, 256, (m, k), dtype=torch.uint8, device=dev, generator=gen)
+        w = C.c_void_p()
+        L.call("abftlp_gemm_encode", vp(b), k, n, n, st, C.byref(w))
+        mlp.append((k, n, w, a, torch.empty((m, n), dtype=torch.int32, device=dev),
+                    torch.empty(m, dtype=torch.int32, device=dev), torch.empty(m, dtype=torch.uint8, device=dev),
+                    torch.zeros(1, dtype=torch.int32, device=dev)))
+    probs = (L.GemmProblem * len(mlp))()
+    for q, (k, n, w, a, c, cs, fl, er) in enumerate(mlp):
+        probs[q] = L.GemmProblem(a.data_ptr(), m, k, w.value, c.data_ptr(), n, cs.data_ptr(), 1, fl.data_ptr(),
+                                 er.data_ptr())
+    grp = C.c_void_p()
+    L.call("abftlp_gemm_group_create", probs, len(mlp), 1, C.byref(grp))
+
+    def sep():
+        for k, n, w, a, c, cs, fl, er in mlp:
+            L.call("abftlp_gemm_checked", vp(a), m, k, w, vp(c), n, vp(cs), 1, vp(fl), vp(er), None, st)
+    t_grp = graph_us(lambda: L.call("abftlp_gemm_group_run", grp, st), 8)[0]
+    t_sep = graph_us(sep, 8)[0]
+    alg = sum(m * k + k * (n + 1) + 4 * m * (n + 1) + m for k, n, *_ in mlp)
+    ops = sum(2 * m * n * k for k, n, *_ in mlp)
+    L.lib.abftlp_gemm_group_free(grp)
+    for _, _, w, *_ in mlp:
+        L.lib.abftlp_gemm_weight_free(w)
+    return {"grouped_us": t_grp, "as_9_launches_us": t_sep, "alg_bytes": alg, "hbm_roof_us": alg / pk["hbm_gbs"] / 1e3,
+            "hbm_frac": alg / (t_grp * 1e-6) / 1e9 / pk["hbm_gbs"], "tops": ops / (t_grp * 1e-6) / 1e12,
+            "how": "9 checked GEMMs m=8192, (k, n/8), k, n in {512,1024,2048}: one abftlp_gemm_group_run vs 9 "
+                   "abftlp_gemm_checked launches, each as a CUDA graph; seeded synthetic A and B"}
 
 
 def eb_secondary(L, dev, st, vp, pk):

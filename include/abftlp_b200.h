@@ -253,6 +253,30 @@ abftlp_status abftlp_eb_group_set_bags(abftlp_eb_group* g, const int64_t* const*
                                        const int64_t* const* d_indices, const float* const* d_weights /* nullable */,
                                        abftlp_stream stream);
 
+/* ------------------------------------------------------------------ heterogeneous grouped GEMM
+ * Several checked (or plain) GEMMs of DIFFERENT shapes -- each its own A (u8, 16-byte aligned, lda % 16 == 0),
+ * encoded weight, C', checksum column, row flags and count -- in ONE persistent launch (abft_gemm per problem,
+ * P:src/gemm_abft.cpp:93-124; e.g. the layers of a DLRM MLP, BASELINE configs[4]). _create validates the problems,
+ * picks one tile width for all of them and uploads their parameters and tensor maps once; _run launches (stream-
+ * ordered, CUDA-graph capturable). Results are identical to one abftlp_gemm_checked / _unchecked call per problem.
+ * A group is run on one stream at a time (its per-row verdict scratch is its own). At most 16 problems. */
+typedef struct {
+    const uint8_t* d_a;
+    uint64_t m, lda;
+    const abftlp_gemm_weight* w;
+    int32_t* d_c;
+    uint64_t ldc;
+    int32_t* d_csum;      /* checked only: C'[:, n] (stride csum_ld) */
+    uint64_t csum_ld;
+    uint8_t* d_row_flags; /* checked only */
+    uint32_t* d_err_count;/* checked only */
+} abftlp_gemm_problem;
+typedef struct abftlp_gemm_group_s abftlp_gemm_group;
+abftlp_status abftlp_gemm_group_create(const abftlp_gemm_problem* problems, uint32_t count, int checked,
+                                       abftlp_gemm_group** out);
+abftlp_status abftlp_gemm_group_run(const abftlp_gemm_group* g, abftlp_stream stream);
+void abftlp_gemm_group_free(abftlp_gemm_group* g);
+
 /* ------------------------------------------------------------------ fault injection */
 /* XOR bit `bit` of element `index` of an array of `elem_bytes`-wide integers
  * (flip_bit, P:src/fault_lab.hpp:87-93). */

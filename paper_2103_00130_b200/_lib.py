@@ -74,6 +74,13 @@ class BatchFault(C.Structure):
                 ("bit", C.c_uint32)]
 
 
+class GemmProblem(C.Structure):
+    """abftlp_gemm_problem (one problem of a heterogeneous grouped GEMM)."""
+    _fields_ = [("d_a", C.c_void_p), ("m", C.c_uint64), ("lda", C.c_uint64), ("w", C.c_void_p), ("d_c", C.c_void_p),
+                ("ldc", C.c_uint64), ("d_csum", C.c_void_p), ("csum_ld", C.c_uint64), ("d_row_flags", C.c_void_p),
+                ("d_err_count", C.c_void_p)]
+
+
 class Fault(C.Structure):
     _fields_ = [("active", i32), ("row", u64), ("col", u64), ("bit", u32)]
 
@@ -128,6 +135,9 @@ _SIGS = {
     "abftlp_row_sums_u8": (i32, [vp, u64, u64, u64, vp, vp]),
     "abftlp_gemm_weight_col_sums": (i32, [vp, vp, vp]),
     "abftlp_eb_group_create": (i32, [vp, u32, vp, vp, vp, vp, vp, vp]),
+    "abftlp_gemm_group_create": (i32, [vp, u32, i32, P(vp)]),
+    "abftlp_gemm_group_run": (i32, [vp, vp]),
+    "abftlp_gemm_group_free": (None, [vp]),
     "abftlp_eb_group_checked_scatter": (i32, [vp, u64, u64, u64, u64, vp, vp, vp]),
     "abftlp_eb_group_unchecked_scatter": (i32, [vp, u64, u64, u64, vp, vp]),
     "abftlp_eb_group_set_bags": (i32, [vp, vp, vp, vp, vp]),

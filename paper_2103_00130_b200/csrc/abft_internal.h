@@ -36,14 +36,15 @@ constexpr int kBK = 128;      // K bytes per k-block = one 128-byte swizzle span
 constexpr int kRowAlign = 256;  // B' rows are padded to a multiple of this
 
 // Encoded weight: B stored transposed, K-block-major, for the mainloop's TMA requests:
-//   bt[kb][j][kk] = B[kb*128 + kk][j]   for j < n, zero for n <= j < n_pad and kb*128 + kk >= k.
+//   bt[kb][j][kk] = B[kb*128 + kk][j]   for j < n, cs[kb*128 + kk] for j == n, zero for n < j < n_pad and
+//                                       kb*128 + kk >= k.
 // One k-block slab of a tile (rows j0..j0+R) is contiguous (R*128 bytes), so each TMA request is
 // one long burst. The checksum column of the reference's [B | cs] (P:src/gemm_abft.cpp:73-85) is
 // kept as the vector cs (k_pad bytes, zero beyond k): C'[:, n] = A*cs is a GEMV, computed exactly on
 // CUDA cores by the epilogue warps (each N tile takes a K share), so it never costs an MMA tile.
 struct GemmWeight {
     int64_t k = 0, n = 0;          // logical sizes (PackedEncodedWeight::k()/n())
-    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad >= n
+    int64_t k_pad = 0, n_pad = 0;  // k_pad % 128 == 0, n_pad % 256 == 0, n_pad > n (column n = cs)
     int8_t* bt = nullptr;          // k_pad/128 x n_pad x 128
     int8_t* cs = nullptr;          // k_pad (WeightChecksum::values, each in [0,126]; zero pad)
     int32_t* cs_acc = nullptr;     // k_pad x batch encoder scratch: per-row sums of column-block residues (zeroed)
@@ -72,6 +73,7 @@ struct RequantDev {
 };
 
 constexpr int kMaxGemmFaults = 8;  // C' faults one launch can inject (grouped jobs)
+constexpr int kMaxGemmGroup = 16;  // problems of different shapes in one grouped launch
 
 struct GemmParams {
     int m, n, k;       // logical sizes (n excludes the checksum column)
@@ -126,6 +128,14 @@ struct GemmParams {
     int nfaults;
     int fault_b[kMaxGemmFaults], fault_row[kMaxGemmFaults], fault_col[kMaxGemmFaults], fault_bit[kMaxGemmFaults];
     unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
+    // heterogeneous grouped launch (group_n > 0): problems of different (m, n, k) sharing one tile width; tile t
+    // belongs to problem i with grp_tile_start[i] <= t < grp_tile_start[i + 1], whose fields (a single problem,
+    // batch 1) are grp_params[i] and whose tensor maps (A, B', C) are grp_maps[3i .. 3i+2] in global memory
+    int group_n;
+    int grp_tile_start[kMaxGemmGroup + 1];
+    const struct GemmParams* grp_params;
+    const CUtensorMap* grp_maps;  // [3 * group_n] A, B', C per problem, then (grp_apf) [group_n] A L2-prefetch views
+    int grp_apf;
 };
 
 // C' write-out: TMA store of 32x32 chunks; coalesced st.global.v4 after a swizzled smem transpose

@@ -40,6 +40,9 @@ struct abftlp_gemm_weight_s {
 struct abftlp_eb_table_s {
     abftk::EbTable* t;
 };
+struct abftlp_gemm_group_s {
+    abftk::GemmGroup* g;
+};
 struct abftlp_eb_group_s {
     abftk::EbGroup* g;
 };
@@ -807,6 +810,45 @@ abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t
                             d_status, as_stream(stream));
         return ABFTLP_OK;
     });
+}
+
+// ============================================================ heterogeneous grouped GEMM
+abftlp_status abftlp_gemm_group_create(const abftlp_gemm_problem* problems, uint32_t count, int checked,
+                                       abftlp_gemm_group** out) {
+    if (!problems || !out || count == 0) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        std::vector<abftk::GemmProblem> ps(count);
+        for (uint32_t i = 0; i < count; ++i) {
+            const abftlp_gemm_problem& q = problems[i];
+            if (!q.w) throw std::invalid_argument("null argument");
+            ps[i].a = q.d_a;
+            ps[i].m = static_cast<int64_t>(q.m);
+            ps[i].lda = static_cast<int64_t>(q.lda);
+            ps[i].w = q.w->w;
+            ps[i].c = q.d_c;
+            ps[i].ldc = static_cast<int64_t>(q.ldc);
+            ps[i].csum = q.d_csum;
+            ps[i].csum_ld = static_cast<int64_t>(q.csum_ld);
+            ps[i].flags = q.d_row_flags;
+            ps[i].err_count = q.d_err_count;
+        }
+        *out = new abftlp_gemm_group_s{abftk::gemm_group_create(ps.data(), static_cast<int>(count), checked != 0)};
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_group_run(const abftlp_gemm_group* g, abftlp_stream stream) {
+    if (!g) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        abftk::gemm_group_run(*g->g, as_stream(stream));
+        return ABFTLP_OK;
+    });
+}
+
+void abftlp_gemm_group_free(abftlp_gemm_group* g) {
+    if (!g) return;
+    abftk::gemm_group_free(g->g);
+    delete g;
 }
 
 // ============================================================ fault injection

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "abft_internal.h"
 #include "ptx.cuh"
@@ -330,7 +331,7 @@ struct PairCfg {
     static_assert(kBBytes % 1024 == 0 && kABytes % 1024 == 0, "SW128 tiles must stay 1024-byte aligned");
 };
 
-template <int BN, bool CHECKED, int EPI, int EW>
+template <int BN, bool CHECKED, int EPI, int EW, bool GROUPED = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const GemmParams p) {
@@ -355,12 +356,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     const int pair = static_cast<int>(cluster_id_x()), npairs = static_cast<int>(nclusters_x());
     const int num_units = p.num_tiles * p.split;
     // unit -> (tile, k range); see GemmParams::split
+    // b: the problem of a batched launch (coordinate of the 4-D maps, stride index) -- or, GROUPED, the problem
+    // index into grp_params / grp_maps (each of those a single problem, batch coordinate 0)
     struct Unit {
         int tile, b, mt, nt, kh, kb0, steps;
     };
     const int tiles_per_problem = p.m_tiles * p.n_tiles;
     auto unit_of = [&](int u) {
         Unit x;
+        if constexpr (GROUPED) {
+            int i = 0;
+            while (i + 1 < p.group_n && u >= p.grp_tile_start[i + 1]) ++i;
+            const GemmParams& q = p.grp_params[i];
+            const int tl = u - p.grp_tile_start[i];
+            x.tile = u;
+            x.b = i;
+            x.kh = 0;
+            x.kb0 = 0;
+            x.mt = tl / q.n_tiles;
+            x.nt = tl - x.mt * q.n_tiles;
+            x.steps = (q.k_blocks + KS - 1) / KS;
+            return x;
+        }
         x.kh = (p.split == 2 && u < p.num_tiles) ? 1 : 0;
         x.tile = p.split == 2 && !x.kh ? u - p.num_tiles : u;
         x.b = x.tile / tiles_per_problem;
@@ -372,7 +389,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
         x.steps = (cnt + KS - 1) / KS;
         return x;
     };
+    // the unit's problem parameters, tensor maps and batch coordinate
+    auto prm = [&](const Unit& x) -> const GemmParams& {
+        if constexpr (GROUPED) return p.grp_params[x.b];
+        return p;
+    };
+    auto map_a = [&](const Unit& x) -> const CUtensorMap* {
+        if constexpr (GROUPED) return p.grp_maps + 3 * x.b;
+        return &tmA;
+    };
+    auto map_b = [&](const Unit& x) -> const CUtensorMap* {
+        if constexpr (GROUPED) return p.grp_maps + 3 * x.b + 1;
+        return &tmB;
+    };
+    auto map_c = [&](const Unit& x) -> const CUtensorMap* {
+        if constexpr (GROUPED) return p.grp_maps + 3 * x.b + 2;
+        return &tmC;
+    };
+    auto bcoord = [&](const Unit& x) { return GROUPED ? 0 : x.b; };
+#ifdef ABFT_TRACE_TILES  // (debug: per-tile MMA / epilogue timestamps, 64 slots per CTA, first 16 tiles)
+    unsigned long long* const tt = p.trace ? p.trace + 64ull * blockIdx.x : nullptr;
+    unsigned long long* trace = nullptr;
+#else
     unsigned long long* trace = p.trace ? p.trace + 16ull * blockIdx.x : nullptr;
+#endif
     if (trace && threadIdx.x == 0) trace[0] = globaltimer();
 
     if (threadIdx.x == 0) {
@@ -389,9 +429,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     }
     if (warp == 0 && lane == 0) {
         griddep_launch_dependents();  // the next kernel's prologue may overlap this grid
-        tma_prefetch(&tmA);
-        tma_prefetch(&tmB);
-        if (EPI == kEpiTmaStore) tma_prefetch(&tmC);
+        if constexpr (GROUPED) {  // the maps of this pair's first problem
+            if (pair < num_units) {
+                const Unit x0 = unit_of(pair);
+                tma_prefetch(map_a(x0));
+                tma_prefetch(map_b(x0));
+                if (EPI == kEpiTmaStore) tma_prefetch(map_c(x0));
+            }
+        } else {
+            tma_prefetch(&tmA);
+            tma_prefetch(&tmB);
+            if (EPI == kEpiTmaStore) tma_prefetch(&tmC);
+        }
     }
     // Barriers must be visible to the peer before any TMA / commit targets them; TMEM is allocated
     // afterwards by the MMA warp so the producer's first loads overlap the allocation.
@@ -404,17 +453,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     if (is_producer && lane == 0 && pair < num_units) {
         const int role = warp == 0 ? 0 : warp - 5;
         const Unit x = unit_of(pair);
+        const GemmParams& q = prm(x);
         const int pre = x.steps < STAGES ? x.steps : STAGES;
         const int rot = x.nt % x.steps;
         for (int ks0 = 0; ks0 < pre; ++ks0) {
             const int kb = x.kb0 + ((ks0 + rot) % x.steps) * KS;
-            if (role < Cfg::NA && p.a_exact)
-                tma_prefetch_l2_3d(&tmA, (kb + role * (KS / Cfg::NA)) * kBK, x.mt * kPairM + static_cast<int>(rank) * kBM, x.b);
+            if (role < Cfg::NA && q.a_exact)
+                tma_prefetch_l2_3d(map_a(x), (kb + role * (KS / Cfg::NA)) * kBK, x.mt * kPairM + static_cast<int>(rank) * kBM,
+                                   bcoord(x));
             else if (role < Cfg::NA)
-                tma_prefetch_l2_4d(&tmA, 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA), x.b);
+                tma_prefetch_l2_4d(map_a(x), 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA),
+                                   bcoord(x));
             else
-                tma_prefetch_l2_4d(&tmB, 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
-                                   kb + (role - Cfg::NA) * (KS / Cfg::NB), p.b_shared ? 0 : x.b);
+                tma_prefetch_l2_4d(map_b(x), 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
+                                   kb + (role - Cfg::NA) * (KS / Cfg::NB), q.b_shared ? 0 : bcoord(x));
         }
     }
     uint32_t tmem = 0;
@@ -450,6 +502,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             int it = 0;
             for (int u = pair; u < num_units; u += npairs) {
                 const Unit x = unit_of(u);
+                const GemmParams& q = prm(x);
+                const CUtensorMap* mA = map_a(x);
+                const CUtensorMap* mB = map_b(x);
+                const int bc = bcoord(x);
+                if constexpr (GROUPED) {
+                    // A streams from HBM once per problem row block here (few N tiles share it): warm L2 with the
+                    // whole slab of this unit (first unit) and of the next one in long per-row runs (1 KB boxes of
+                    // the prefetch view grp_maps[3 * group_n + i]) -- DRAM-friendlier than the mainloop's 128-byte
+                    // k-block pieces, and a unit ahead of them
+                    if (rank == 0 && role == 0 && p.grp_apf) {
+                        auto warm = [&](const Unit& y) {
+                            const GemmParams& qy = prm(y);
+                            const CUtensorMap* mp = p.grp_maps + 3 * p.group_n + y.b;
+                            for (int c0 = 0; c0 < qy.k / 4; c0 += 256) tma_prefetch_l2_2d(mp, c0, y.mt * kPairM);
+                        };
+                        if (u == pair) warm(x);
+                        if (u + npairs < num_units) warm(unit_of(u + npairs));
+                    }
+                }
                 // Tiles of one M block read the same A rows; starting each tile at a different K step
                 // spreads those reads over all of A's L2 lines instead of hammering one k-block's lines
                 // (integer accumulation is exact, so the K order does not change the result).
@@ -462,18 +533,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
                     if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
-                    if (is_a && p.a_exact) {
+                    if (is_a && q.a_exact) {
 #pragma unroll
-                        for (int q = 0; q < KA; ++q)  // exact-extent view: one k-block per request
-                            tma_load_3d_pair(st + (grp * KA + q) * Cfg::kABytes, &tmA, &full[s], (kb + grp * KA + q) * kBK,
-                                             x.mt * kPairM + static_cast<int>(rank) * kBM, x.b, pol);
+                        for (int qq = 0; qq < KA; ++qq)  // exact-extent view: one k-block per request
+                            tma_load_3d_pair(st + (grp * KA + qq) * Cfg::kABytes, mA, &full[s], (kb + grp * KA + qq) * kBK,
+                                             x.mt * kPairM + static_cast<int>(rank) * kBM, bc, pol);
                     } else if (is_a)
-                        tma_load_4d_pair(st + grp * KA * Cfg::kABytes, &tmA, &full[s], 0,
-                                         x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, x.b, pol);
+                        tma_load_4d_pair(st + grp * KA * Cfg::kABytes, mA, &full[s], 0,
+                                         x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, bc, pol);
                     else
-                        tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, &tmB, &full[s], 0,
+                        tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, mB, &full[s], 0,
                                          x.nt * BN + static_cast<int>(rank) * (BN / 2), kb + grp * KB,
-                                         p.b_shared ? 0 : x.b, pol);
+                                         q.b_shared ? 0 : bc, pol);
                 }
             }
         }
@@ -490,6 +561,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 if (trace && local == 8) trace[11] = globaltimer();
 #endif
                 mbar_wait(&tempty[acc], aph ^ 1);
+#ifdef ABFT_TRACE_TILES
+                if (tt && local < 16) tt[local] = globaltimer();
+#endif
 #ifdef ABFT_TRACE_STEADY
                 if (trace && local == 8) trace[12] = globaltimer();
 #endif
@@ -520,6 +594,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     mma_commit_pair(&empty[s]);  // frees the slot in both CTAs once these MMAs read it
                 }
                 mma_commit_pair(&tfull[acc]);  // accumulator complete, both CTAs' epilogues may read
+#ifdef ABFT_TRACE_TILES
+                if (tt && local < 16) tt[16 + local] = globaltimer();
+#endif
                 if (trace && local == 0) trace[3] = globaltimer();
             }
         }
@@ -533,6 +610,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
         for (int u = pair; u < num_units; u += npairs, ++local) {
             const Unit x = unit_of(u);
             const int mt = x.mt, nt = x.nt;
+            const GemmParams& pq = prm(x);  // this tile's problem (the launch's own fields unless GROUPED)
+            const int bb = bcoord(x);
+            // the tile's hot fields in registers (GROUPED: the problem's parameters live in global memory and would be
+            // re-read after every memory clobber of the chunk loop)
+            const int pn = pq.n, pm = pq.m;
+            const int64_t pldc = pq.ldc;
+            uint8_t* const prq = pq.rq_out;
             const int acc = local & 1;
             const uint32_t aph = (local >> 1) & 1;
             const int row0 = mt * kPairM + static_cast<int>(rank) * kBM + q * 32;  // first row of this warp
@@ -540,15 +624,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             // This tile's share of the checksum column C'[row][n] = sum_p A[row][p]*cs[p]: K blocks
             // [kb0, kb1) of the GEMV, read from global while the tensor cores run the mainloop.
             uint32_t cs_part = 0;
-            if (CHECKED && x.kh == 0 && !p.gemv_helpers && !p.cs_mma) {
-                const int t0 = static_cast<int>(static_cast<long long>(nt) * p.k_blocks / p.n_tiles);
-                const int t1 = static_cast<int>(static_cast<long long>(nt + 1) * p.k_blocks / p.n_tiles);
+            if (CHECKED && x.kh == 0 && !p.gemv_helpers && !pq.cs_mma) {
+                const int t0 = static_cast<int>(static_cast<long long>(nt) * pq.k_blocks / pq.n_tiles);
+                const int t1 = static_cast<int>(static_cast<long long>(nt + 1) * pq.k_blocks / pq.n_tiles);
                 const int kb0 = t0 + (t1 - t0) * eg / Cfg::kEpiGroups;  // the groups split the tile's share
                 const int kb1 = t0 + (t1 - t0) * (eg + 1) / Cfg::kEpiGroups;
-                if (kb1 > kb0 && row < p.m) cs_part = csum_share(p, x.b, row, kb0 * kBK, min(kb1 * kBK, p.k));
+                if (kb1 > kb0 && row < pm) cs_part = csum_share(pq, bb, row, kb0 * kBK, min(kb1 * kBK, pq.k));
             }
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
+#ifdef ABFT_TRACE_TILES
+            if (tt && local < 16 && threadIdx.x == 64) tt[32 + local] = globaltimer();
+#endif
             if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
 #ifdef ABFT_TRACE_STEADY
             if (trace && local == 8 && threadIdx.x == 64) trace[9] = globaltimer();
@@ -609,14 +696,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 spart = reinterpret_cast<const uint4*>(smem);
             }
             bool fault_here = false;  // some injected fault hits a data column of this row
-            for (int f = 0; f < p.nfaults; ++f)
-                fault_here |= x.b == p.fault_b[f] && row == p.fault_row[f] && p.fault_col[f] < p.n;
-            int32_t* const cb = p.c + x.b * p.c_bstride;  // this problem's C
+            for (int f = 0; f < pq.nfaults; ++f)
+                fault_here |= bb == pq.fault_b[f] && row == pq.fault_row[f] && pq.fault_col[f] < pn;
+            int32_t* const cb = pq.c + bb * pq.c_bstride;  // this problem's C
             long long rsum = 0;
 #pragma unroll 1
             for (int c = eg; c < BN / 32; c += Cfg::kEpiGroups) {
                 const int col0 = n0 + c * 32;
-                if (col0 >= p.n) break;  // warp-uniform
+                if (col0 >= pn) break;  // warp-uniform
                 uint32_t v[32];
 #ifdef ABFT_TRACE_CHUNKS
                 if (trace && local == 0 && threadIdx.x == 64 && c < 2) trace[12 + c] = globaltimer();
@@ -637,43 +724,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     }
                 }
                 if (fault_here) {
-                    for (int f = 0; f < p.nfaults; ++f) {
-                        if (x.b != p.fault_b[f] || row != p.fault_row[f]) continue;
-                        const int fc = p.fault_col[f];
-                        const uint32_t fm = 1u << p.fault_bit[f];
+                    for (int f = 0; f < pq.nfaults; ++f) {
+                        if (bb != pq.fault_b[f] || row != pq.fault_row[f]) continue;
+                        const int fc = pq.fault_col[f];
+                        const uint32_t fm = 1u << pq.fault_bit[f];
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             if (fc == col0 + j) v[j] ^= fm;
                     }
                 }
-                if (p.rq_out != nullptr && row < p.m) {
+                if (prq != nullptr && row < pm) {
                     // fused requantization of this row's 32 columns (the checksum column is never part
                     // of C, so it is excluded by construction), after any injected C' fault
-                    const RequantConsts rk = requant_consts(p.rq);
-                    const int32_t rsa = p.rq_row_sum_a[row];
+                    const RequantConsts rk = requant_consts(pq.rq);
+                    const int32_t rsa = pq.rq_row_sum_a[row];
                     uint32_t pk[8];
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) pk[q4] = 0u;
 #pragma unroll
                     for (int j = 0; j < 32; ++j)  // fully unrolled: v[] and pk[] must stay in registers
-                        if (col0 + j < p.n)
-                            pk[j >> 2] |= requant_one(static_cast<int32_t>(v[j]), rsa, __ldg(p.rq_col_sum_b + col0 + j), rk)
+                        if (col0 + j < pn)
+                            pk[j >> 2] |= requant_one(static_cast<int32_t>(v[j]), rsa, __ldg(pq.rq_col_sum_b + col0 + j), rk)
                                           << (8 * (j & 3));
-                    uint8_t* dst = p.rq_out + static_cast<int64_t>(row) * p.rq_ld + col0;
-                    if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    uint8_t* dst = prq + static_cast<int64_t>(row) * pq.rq_ld + col0;
+                    if (col0 + 32 <= pn && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                         reinterpret_cast<uint4*>(dst)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         reinterpret_cast<uint4*>(dst)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.n) dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
+                            if (col0 + j < pn) dst[j] = static_cast<uint8_t>(pk[j >> 2] >> (8 * (j & 3)));
                     }
                 }
 #ifdef ABFT_TRACE_CHUNKS
                 if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[9] = globaltimer();
 #endif
                 if constexpr (CHECKED) {
-                    if (col0 + 32 <= p.n) {
+                    if (col0 + 32 <= pn) {
                         // pairwise tree: 5 dependent int64 adds instead of a 32-long carry chain (exact in
                         // any order: |sum| < 32 * 2^31)
                         long long t[16];
@@ -688,7 +775,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     } else {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (col0 + j < p.n) rsum += static_cast<int32_t>(v[j]);
+                            if (col0 + j < pn) rsum += static_cast<int32_t>(v[j]);
                     }
                 }
                 if constexpr (EPI == kEpiTmaStore) {
@@ -711,7 +798,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[11] = globaltimer();
 #endif
                     if (lane == 0) {
-                        if (row0 < p.m && col0 < p.n) tma_store_3d(&tmC, buf, col0, row0, x.b);
+                        if (row0 < pm && col0 < pn) tma_store_3d(map_c(x), buf, col0, row0, bb);
                         bulk_commit();
                     }
                     ++chunk_ctr;
@@ -731,13 +818,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                         const int r = i * 4 + rsub;
                         const uint4 val = *reinterpret_cast<const uint4*>(buf + r * 128 + ((cq ^ (r & 7)) << 4));
                         const int grow = row0 + r;
-                        if (grow < p.m && gcol < p.n) {
-                            int32_t* dst = cb + static_cast<int64_t>(grow) * p.ldc + gcol;
-                            if (gcol + 3 < p.n) {
+                        if (grow < pm && gcol < pn) {
+                            int32_t* dst = cb + static_cast<int64_t>(grow) * pldc + gcol;
+                            if (gcol + 3 < pn) {
                                 *reinterpret_cast<uint4*>(dst) = val;
                             } else {
                                 const uint32_t e4[4] = {val.x, val.y, val.z, val.w};
-                                for (int e = 0; e < 4 && gcol + e < p.n; ++e) dst[e] = static_cast<int32_t>(e4[e]);
+                                for (int e = 0; e < 4 && gcol + e < pn; ++e) dst[e] = static_cast<int32_t>(e4[e]);
                             }
                         }
                     }
@@ -745,16 +832,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 } else if constexpr (EPI == kEpiDirect) {
                     // straight from the registers (no shared-memory staging, whose traffic competes with the
                     // mainloop's operand reads): 16-byte stores when the row segment is aligned
-                    if (row < p.m) {
-                        int32_t* crow = cb + static_cast<int64_t>(row) * p.ldc + col0;
-                        if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 31) == 0) {
+                    if (row < pm) {
+                        int32_t* crow = cb + static_cast<int64_t>(row) * pldc + col0;
+                        if (col0 + 32 <= pn && (reinterpret_cast<uintptr_t>(crow) & 31) == 0) {
 #pragma unroll
                             for (int q8 = 0; q8 < 4; ++q8)  // 32-byte stores: full sectors (STG.256)
                                 asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + 8 * q8),
                                              "r"(v[8 * q8]), "r"(v[8 * q8 + 1]), "r"(v[8 * q8 + 2]), "r"(v[8 * q8 + 3]),
                                              "r"(v[8 * q8 + 4]), "r"(v[8 * q8 + 5]), "r"(v[8 * q8 + 6]), "r"(v[8 * q8 + 7])
                                              : "memory");
-                        } else if (col0 + 32 <= p.n && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+                        } else if (col0 + 32 <= pn && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
 #pragma unroll
                             for (int q4 = 0; q4 < 8; ++q4)
                                 reinterpret_cast<uint4*>(crow)[q4] =
@@ -762,15 +849,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                         } else {
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
-                                if (col0 + j < p.n) crow[j] = static_cast<int32_t>(v[j]);
+                                if (col0 + j < pn) crow[j] = static_cast<int32_t>(v[j]);
                         }
                     }
                 }
             }
             if constexpr (CHECKED) {
                 // C'[row][n] = A*cs computed by the tensor cores (B' column n) when this tile covers column n
-                if (p.cs_mma && eg == 0 && n0 <= p.n && p.n < n0 + BN) {
-                    cs_part = tmem_ld_32x32b_x1(t_row + static_cast<uint32_t>(p.n - n0));
+                if (pq.cs_mma && eg == 0 && n0 <= pn && pn < n0 + BN) {
+                    cs_part = tmem_ld_32x32b_x1(t_row + static_cast<uint32_t>(pn - n0));
                     tmem_wait_ld();
                 }
             }
@@ -797,14 +884,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 // brings arrival n_tiles holds the complete row and finalizes it -- no fences, no
                 // counters, no second pass.
                 int fin = 0, flag = 0;
-                if (row < p.m)
-                    row_arrive(p, x.b, row,
+                if (row < pm)
+                    row_arrive(pq, bb, row,
                                (static_cast<unsigned long long>(p.gemv_helpers ? 0u : cs_part) << 32) |
                                    (1ull << kRowAccCountShift) | static_cast<unsigned long long>(mod127(rsum)),
                                fin, flag);
                 if (trace && local == 0 && threadIdx.x == 64) trace[8] = globaltimer();
-                warp_publish(p, x.b, fin, flag);
+                warp_publish(pq, bb, fin, flag);
             }
+#ifdef ABFT_TRACE_TILES
+            if (tt && local < 16 && threadIdx.x == 64) tt[48 + local] = globaltimer();
+#endif
         }
         if constexpr (EPI == kEpiTmaStore) {
             if (lane == 0) bulk_wait<0>();
@@ -869,11 +959,11 @@ __global__ void __launch_bounds__(256) verify_kernel(const int32_t* __restrict__
 }
 
 // ============================================================ host launchers
-template <int BN, bool CHECKED, int EPI, int EW>
+template <int BN, bool CHECKED, int EPI, int EW, bool GROUPED = false>
 static cudaError_t launch_one(int pairs, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                               const GemmParams& p, cudaStream_t st) {
     using Cfg = PairCfg<BN, EW>;
-    auto kern = gemm_pair_kernel<BN, CHECKED, EPI, EW>;
+    auto kern = gemm_pair_kernel<BN, CHECKED, EPI, EW, GROUPED>;
     static bool attr_done[kMaxDevices] = {};  // per device; benign race: idempotent attribute set
     const int dev = current_device();
     if (!attr_done[dev]) {
@@ -918,6 +1008,27 @@ cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs,
     if (bn == 256) return launch_epi<256, false>(epi, ew, pairs, a, b, c, p, st);
     if (bn == 128) return launch_epi<128, false>(epi, ew, pairs, a, b, c, p, st);
     return launch_epi<64, false>(epi, ew, pairs, a, b, c, p, st);
+}
+
+// Heterogeneous grouped launch (GemmParams::group_n problems; tensor maps in p.grp_maps): TMA-store or direct
+// epilogue, 4 epilogue warps.
+template <int BN, bool CHECKED>
+static cudaError_t launch_grouped_bn(int epi, int pairs, const GemmParams& p, cudaStream_t st) {
+    CUtensorMap none;
+    std::memset(&none, 0, sizeof(none));
+    if (epi == kEpiTmaStore) return launch_one<BN, CHECKED, kEpiTmaStore, 4, true>(pairs, none, none, none, p, st);
+    if (epi == kEpiStg) return launch_one<BN, CHECKED, kEpiStg, 4, true>(pairs, none, none, none, p, st);
+    return launch_one<BN, CHECKED, kEpiDirect, 4, true>(pairs, none, none, none, p, st);
+}
+cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int pairs, const GemmParams& p, cudaStream_t st) {
+    if (checked) {
+        if (bn == 256) return launch_grouped_bn<256, true>(epi, pairs, p, st);
+        if (bn == 128) return launch_grouped_bn<128, true>(epi, pairs, p, st);
+        return launch_grouped_bn<64, true>(epi, pairs, p, st);
+    }
+    if (bn == 256) return launch_grouped_bn<256, false>(epi, pairs, p, st);
+    if (bn == 128) return launch_grouped_bn<128, false>(epi, pairs, p, st);
+    return launch_grouped_bn<64, false>(epi, pairs, p, st);
 }
 
 int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }

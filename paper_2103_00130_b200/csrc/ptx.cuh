@@ -293,6 +293,12 @@ __device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap* map, int32
                  "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
 }
+// L2 prefetch of a 2D tensor box.
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // L2 prefetch of a 3D tensor box.
 __device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2) {
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
@@ -341,6 +347,11 @@ __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
 __host__ __device__ __forceinline__ int32_t mod127(int64_t v) {
     int64_t r = v % 127;
     return static_cast<int32_t>(r < 0 ? r + 127 : r);
+}
+// Same residue for a 32-bit value (32-bit arithmetic only).
+__host__ __device__ __forceinline__ uint32_t mod127_i32(int32_t v) {
+    const int32_t r = v % 127;
+    return static_cast<uint32_t>(r < 0 ? r + 127 : r);
 }
 
 }  // namespace abftk

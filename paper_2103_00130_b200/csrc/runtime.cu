@@ -180,9 +180,9 @@ void encode_weight_into(GemmWeight& w, const int8_t* d_b, int64_t k, int64_t n, 
     if (ldb < n) throw std::invalid_argument("abftlp_gemm_encode: ldb < n");
     if (batch < 1) throw std::invalid_argument("abftlp_gemm_encode: batch < 1");
     if (batch > 1 && b_bstride < ldb * (k - 1) + n) throw std::invalid_argument("abftlp_gemm_encode: batch stride too small");
-    // When n_pad > n, B' column n holds the checksum column (PackedEncodedWeight's [B | cs],
-    // P:src/gemm_abft.hpp:30-59), so a tile that covers it gets C'[:, n] from the tensor cores (GemmParams::cs_mma)
-    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n, kRowAlign);
+    // B' column n holds the checksum column (PackedEncodedWeight's [B | cs], P:src/gemm_abft.hpp:30-59): n_pad leaves
+    // room for it at every n, so a tile that covers it gets C'[:, n] from the tensor cores (GemmParams::cs_mma)
+    const int64_t k_pad = round_up(k, kBK), n_pad = round_up(n + 1, kRowAlign);
     const size_t per_bt = static_cast<size_t>(n_pad * k_pad);
     const size_t need_bt = per_bt * static_cast<size_t>(batch), need_cs = static_cast<size_t>(k_pad * batch);
     if (!w.bt || need_bt > w.bt_cap || need_cs > w.cs_cap) {
@@ -370,7 +370,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
                                                                   : kGemvMaxRows;
     const int mr = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : m <= 8 ? 8 : 16;
     if (nb == 1 && !rq && !force && m <= gemv_rows && m <= 16 && d_c &&
-        mr * w.k_pad + 8 * mr * 32 * 4 <= 160 * 1024 && (w.n + 31) / 32 <= kMaxCheckedNTiles) {
+        (mr + 1) * w.k_pad + 8 * mr * 32 * 4 + 8 * mr * 32 * 4 <= 160 * 1024 && (w.n + 31) / 32 <= kMaxCheckedNTiles) {
         if (checked) {
             grow(ws.row_acc, ws.rows_cap, m, st);
             grow(ws.err_pack, ws.err_pack_cap, 1, st);
@@ -529,6 +529,181 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (p.gemv_helpers) pairs = all_pairs;
     cuda_check(launch_gemm_kernel(t.bn, checked, t.epi, ew, pairs, map_a, w.map_b[bn_index(t.bn)], map_c, p, st),
                "gemm_pair_kernel");
+}
+
+// ------------------------------------------------------------------ heterogeneous grouped GEMM
+GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
+    if (n < 1 || n > kMaxGemmGroup) throw std::invalid_argument("gemm_group: 1 to 16 problems");
+    if (!probs) throw std::invalid_argument("null argument");
+    bool tma_c = true;
+    for (int i = 0; i < n; ++i) {
+        const GemmProblem& q = probs[i];
+        if (!q.w || !q.a || !q.c) throw std::invalid_argument("null argument");
+        if (checked && (!q.csum || !q.flags || !q.err_count)) throw std::invalid_argument("null argument");
+        if (q.w->batch != 1) throw std::invalid_argument("gemm_group: batched weights are not supported");
+        if (q.m < 1 || q.m > (int64_t{1} << 31) - 1) throw std::invalid_argument("gemm_group: m out of range");
+        if (q.lda < q.w->k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
+        if (q.ldc < q.w->n) throw std::invalid_argument("abft_gemm: ldc < n");
+        if ((q.lda % 16) != 0 || (reinterpret_cast<uintptr_t>(q.a) % 16) != 0)
+            throw std::invalid_argument("gemm_group: A needs a 16-byte aligned base and lda % 16 == 0");
+        tma_c = tma_c && (q.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(q.c) % 16) == 0;
+    }
+    // Tile width: the cost model of choose_tiling summed over the problems (shared-memory-bound mainloop per
+    // k-block, TMEM drain per tile) plus the longest tile as the tail; every problem's checksum column rides in
+    // its last N tile on the tensor cores (B' column n exists at every n).
+    const int pairs_all = std::max(1, device_sm_count() / 2);
+    int best_bn = 64;
+    double best = 1e300;
+    for (int bn : {256, 128, 64}) {
+        const double per_kb = std::max(2.0 * (kBM + bn / 2), 4.0 * (bn == 64 ? 46 : bn == 128 ? 64 : 128));
+        const double drain = double(kBM) * bn * 4 / 31.0 + 1500.0;
+        double sum = 0.0, longest = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const GemmProblem& q = probs[i];
+            // checksum column: always in the MMA (B' column n), adding a tile when the last one has no room --
+            // measured cheaper than the CUDA-core GEMV share on these short-K tiles (D5 share at G=8: 53 vs 58 us)
+            const int64_t nt = (q.w->n + (checked ? 1 : 0) + bn - 1) / bn;
+            const double tiles = double((q.m + kPairM - 1) / kPairM) * double(nt);
+            const double t = double(q.w->k_pad / kBK) * per_kb + drain;
+            sum += tiles * t;
+            longest = std::max(longest, t);
+        }
+        const double cost = sum / pairs_all + longest;
+        if (cost < best * 0.97) {
+            best = cost;
+            best_bn = bn;
+        }
+    }
+    if (const char* e = std::getenv("ABFTLP_GEMM_GROUP_BN")) {
+        const int f = std::atoi(e);
+        if (f == 64 || f == 128 || f == 256) best_bn = f;
+    }
+    auto* g = new GemmGroup();
+    g->n = n;
+    g->bn = best_bn;
+    g->checked = checked;
+    g->epi = tma_c ? kEpiTmaStore : kEpiDirect;
+    if (const char* e = std::getenv("ABFTLP_GEMM_GROUP_EPI")) {  // 0 TMA store, 1 st.global after smem transpose, 2 direct
+        const int f = std::atoi(e);
+        if (f == kEpiDirect || (tma_c && (f == kEpiTmaStore || f == kEpiStg))) g->epi = f;
+    }
+    // longest mainloops first (the persistent pairs take tiles round-robin, so the long tiles start early)
+    g->order.resize(n);
+    for (int i = 0; i < n; ++i) g->order[i] = i;
+    std::stable_sort(g->order.begin(), g->order.end(),
+                     [&](int x, int y) { return probs[x].w->k_pad > probs[y].w->k_pad; });
+    std::vector<GemmParams> hp(n);
+    std::vector<CUtensorMap> hm(4 * n);
+    int64_t rows_total = 0;
+    for (int i = 0; i < n; ++i) rows_total += probs[i].m;
+    try {
+        if (checked) {
+            cuda_check(cudaMalloc(&g->row_acc, sizeof(unsigned long long) * rows_total), "cudaMalloc(group rows)");
+            cuda_check(cudaMemset(g->row_acc, 0, sizeof(unsigned long long) * rows_total), "cudaMemset(group rows)");
+            cuda_check(cudaMalloc(&g->err_pack, sizeof(unsigned long long) * n), "cudaMalloc(group counts)");
+            cuda_check(cudaMemset(g->err_pack, 0, sizeof(unsigned long long) * n), "cudaMemset(group counts)");
+        }
+        int64_t row_off = 0, tiles = 0;
+        GemmParams& L = g->launch;
+        L.group_n = n;
+        L.batch = 1;
+        L.split = 1;
+        for (int s = 0; s < n; ++s) {
+            const GemmProblem& q = probs[g->order[s]];
+            const GemmWeight& w = *q.w;
+            GemmParams& P = hp[s];
+            const int64_t kb = w.k_pad / kBK;
+            P.m = static_cast<int>(q.m);
+            P.n = static_cast<int>(w.n);
+            P.k = static_cast<int>(w.k);
+            P.k_blocks = static_cast<int>(kb);
+            P.m_tiles = static_cast<int>((q.m + kPairM - 1) / kPairM);
+            P.n_tiles = static_cast<int>((w.n + (checked ? 1 : 0) + best_bn - 1) / best_bn);
+            P.num_tiles = P.m_tiles * P.n_tiles;
+            P.batch = 1;
+            P.b_shared = 1;
+            P.split = 1;
+            P.a_exact = (w.k % kBK) != 0 ? 1 : 0;
+            P.cs_mma = checked ? 1 : 0;
+            P.gemv_helpers = 0;
+            P.row_arrivals = P.n_tiles;
+            if (checked && P.row_arrivals > kMaxCheckedNTiles)
+                throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
+            P.c = q.c;
+            P.ldc = q.ldc;
+            P.a = q.a;
+            P.lda = q.lda;
+            P.cs = w.cs;
+            P.csum = q.csum;
+            P.csum_ld = q.csum_ld;
+            P.flags = q.flags;
+            P.err_count = q.err_count;
+            P.row_acc = checked ? g->row_acc + row_off : nullptr;
+            P.err_pack = checked ? g->err_pack + s : nullptr;
+            P.trace = g_trace;
+            row_off += q.m;
+            L.grp_tile_start[s] = static_cast<int>(tiles);
+            tiles += P.num_tiles;
+            if (tiles > (int64_t{1} << 30)) throw std::invalid_argument("abft_gemm: too many tiles");
+            hm[3 * s] = P.a_exact ? make_map_rows(q.a, static_cast<uint64_t>(w.k), static_cast<uint64_t>(q.m),
+                                                  static_cast<uint64_t>(q.lda), 1, 0)
+                                  : make_map_kblocks(q.a, static_cast<uint64_t>(q.m), static_cast<uint64_t>(kb),
+                                                     static_cast<uint64_t>(q.lda), kBK, kBM, gemm_box_a(best_bn), 1, 0);
+            hm[3 * s + 1] = w.map_b[bn_index(best_bn)];
+            if (g->epi == kEpiTmaStore)
+                hm[3 * s + 2] = make_map_c(q.c, static_cast<uint64_t>(w.n), static_cast<uint64_t>(q.m),
+                                           static_cast<uint64_t>(q.ldc), 1, 0);
+            else
+                std::memset(&hm[3 * s + 2], 0, sizeof(CUtensorMap));
+        }
+        // A prefetch views: {k/4 words, m rows}, 1 KB x 256-row boxes (SWIZZLE_NONE), for the L2 warm-up of each
+        // unit's A slab (k % 4 == 0 needed; ABFTLP_GEMM_GROUP_APF=0 disables)
+        bool apf = !std::getenv("ABFTLP_GEMM_GROUP_APF") || std::atoi(std::getenv("ABFTLP_GEMM_GROUP_APF")) != 0;
+        for (int s = 0; s < n && apf; ++s) apf = (probs[g->order[s]].w->k % 4) == 0;
+        for (int s = 0; s < n && apf; ++s) {
+            const GemmProblem& q = probs[g->order[s]];
+            CUtensorMap map;
+            std::memset(&map, 0, sizeof(map));
+            const cuuint64_t dims[2] = {static_cast<cuuint64_t>(q.w->k / 4), static_cast<cuuint64_t>(q.m)};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(q.lda)};
+            const cuuint32_t box[2] = {static_cast<cuuint32_t>(std::min<int64_t>(256, q.w->k / 4)),
+                                       static_cast<cuuint32_t>(std::min<int64_t>(256, q.m))};
+            const cuuint32_t estr[2] = {1, 1};
+            CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(q.a), dims, strides, box,
+                                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) apf = false;
+            hm[3 * n + s] = map;
+        }
+        L.grp_apf = apf ? 1 : 0;
+        L.grp_tile_start[n] = static_cast<int>(tiles);
+        L.num_tiles = static_cast<int>(tiles);
+        L.trace = g_trace;
+        cuda_check(cudaMalloc(&g->d_params, sizeof(GemmParams) * n), "cudaMalloc(group params)");
+        cuda_check(cudaMalloc(&g->d_maps, sizeof(CUtensorMap) * 4 * n), "cudaMalloc(group maps)");
+        cuda_check(cudaMemcpy(g->d_params, hp.data(), sizeof(GemmParams) * n, cudaMemcpyHostToDevice), "cudaMemcpy");
+        cuda_check(cudaMemcpy(g->d_maps, hm.data(), sizeof(CUtensorMap) * 4 * n, cudaMemcpyHostToDevice), "cudaMemcpy");
+        L.grp_params = g->d_params;
+        L.grp_maps = g->d_maps;
+        g->pairs = static_cast<int>(std::min<int64_t>(tiles, pairs_all));
+    } catch (...) {
+        gemm_group_free(g);
+        throw;
+    }
+    return g;
+}
+
+void gemm_group_run(const GemmGroup& g, cudaStream_t st) {
+    cuda_check(launch_gemm_grouped(g.bn, g.checked, g.epi, g.pairs, g.launch, st), "gemm_pair_kernel (grouped)");
+}
+
+void gemm_group_free(GemmGroup* g) {
+    if (!g) return;
+    cudaFree(g->d_params);
+    cudaFree(g->d_maps);
+    cudaFree(g->row_acc);
+    cudaFree(g->err_pack);
+    delete g;
 }
 
 void check_requant_params(const RequantDev& q) {

@@ -61,6 +61,33 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,
           cudaStream_t st, const GemmTiling* force = nullptr, const RequantArgs* rq = nullptr,
           const GemmBatch* batch = nullptr);
+// Heterogeneous grouped GEMM: problems of different (m, n, k), each with its own A, encoded weight and outputs, in
+// ONE persistent launch (the D5 MLP layers). Built once (tensor maps and per-problem parameters uploaded), run any
+// number of times on one stream at a time (the per-row verdict scratch belongs to the group).
+struct GemmProblem {
+    const uint8_t* a = nullptr;
+    int64_t m = 0, lda = 0;
+    const GemmWeight* w = nullptr;
+    int32_t* c = nullptr;
+    int64_t ldc = 0;
+    int32_t* csum = nullptr;  // checked only
+    int64_t csum_ld = 1;
+    uint8_t* flags = nullptr;
+    uint32_t* err_count = nullptr;
+};
+struct GemmGroup {
+    int n = 0, bn = 64, epi = kEpiTmaStore, pairs = 1;
+    bool checked = true;
+    std::vector<int> order;        // problem launched at group slot s
+    GemmParams launch{};           // launch-wide fields: tile table and device pointers
+    GemmParams* d_params = nullptr;
+    CUtensorMap* d_maps = nullptr;
+    unsigned long long* row_acc = nullptr;
+    unsigned long long* err_pack = nullptr;
+};
+GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked);
+void gemm_group_run(const GemmGroup& g, cudaStream_t st);
+void gemm_group_free(GemmGroup* g);
 void requantize(const int32_t* d_c, int64_t ldc, int64_t m, int64_t n, const int32_t* d_row_sum_a,
                 const int32_t* d_col_sum_b, const RequantDev& q, uint8_t* d_out, int64_t ld_out, cudaStream_t st);
 void row_sums_u8(const uint8_t* d_a, int64_t m, int64_t k, int64_t lda, int32_t* d_out, cudaStream_t st);
@@ -132,6 +159,7 @@ void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
 // ---- launchers implemented in the .cu files
 cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b,
                                const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
+cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int pairs, const GemmParams& p, cudaStream_t st);
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st);
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st);
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,

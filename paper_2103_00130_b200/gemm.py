@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
+from typing import Sequence
 
 import torch
 
@@ -227,3 +228,43 @@ def abft_gemm_batched(a, pb, fault: tuple[int, int, int, int] | None = None, str
         f = C.byref(_lib.BatchFault(1, *fault)) if fault is not None else None
         _lib.call("abftlp_gemm_checked_batched", *args, f, stream_handle(stream))
     return ctemp, err, flags
+
+
+class AbftGemmGroup:
+    """Several checked (or plain) GEMMs of different shapes in ONE persistent launch (abftlp_gemm_group_*): the
+    layers of a DLRM MLP, each ``(A, PackedEncodedWeight)``. Each problem writes its own C (m x n), checksum column,
+    row flags and flag count -- exactly what one abft_gemm per problem writes (P:src/gemm_abft.cpp:93-124). The
+    plan (tile table, tensor maps) is built once; ``run()`` only launches."""
+
+    def __init__(self, problems: Sequence, checked: bool = True):
+        self.checked = checked
+        self._keep = []
+        arr = (_lib.GemmProblem * len(problems))()
+        self.outputs = []
+        for i, (a, pb) in enumerate(problems):
+            at = to_device(a, torch.uint8)
+            m, k = (int(s) for s in at.shape)
+            if k != pb.k():
+                raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "abft_gemm: dimension mismatch")
+            n = pb.n()
+            c = torch.zeros((m, n), dtype=torch.int32, device=device())
+            cs = torch.zeros(m, dtype=torch.int32, device=device()) if checked else None
+            fl = torch.zeros(m, dtype=torch.uint8, device=device()) if checked else None
+            err = torch.zeros(1, dtype=torch.int32, device=device()) if checked else None
+            arr[i] = _lib.GemmProblem(at.data_ptr(), m, k, pb.handle.value, c.data_ptr(), n,
+                                      cs.data_ptr() if checked else None, 1, fl.data_ptr() if checked else None,
+                                      err.data_ptr() if checked else None)
+            self._keep += [at, pb]
+            self.outputs.append((c, cs, fl, err))
+        h = C.c_void_p()
+        _lib.call("abftlp_gemm_group_create", arr, len(problems), 1 if checked else 0, C.byref(h))
+        self._h = h
+
+    def run(self, stream=None):
+        _lib.call("abftlp_gemm_group_run", self._h, stream_handle(stream))
+        return self.outputs
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and _lib.lib is not None:
+            _lib.lib.abftlp_gemm_group_free(self._h)
+            self._h = None

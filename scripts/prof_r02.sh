@@ -12,7 +12,7 @@ export_rep() {
   gzip -c /tmp/$1_sass.csv > gpurun_out/r02/$1_sass.csv.gz
   rm -f /tmp/$1.ncu-rep /tmp/$1_sass.csv
 }
-for c in ${EB_CFGS:-E3 E4 D5}; do
+for c in ${EB_CFGS-E3 E4 D5}; do
   python scripts/prof_eb.py $c 1 4 > gpurun_out/r02/prof_eb_$c.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:eb_bag -s 3 -c 1 -o /tmp/ncu_eb_$c \
       python scripts/prof_eb.py $c 1 4 >> gpurun_out/r02/prof_eb_$c.log 2>&1
@@ -26,3 +26,8 @@ export_rep ncu_gemm_g2grouped
 fi
 du -sh gpurun_out
 echo done
+if [ -n "$MLP_G" ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_pair -s 2 -c 1 -o /tmp/ncu_mlp_group_g$MLP_G \
+      python scripts/mlp_group_prof.py $MLP_G > gpurun_out/r02/prof_mlp_g$MLP_G.log 2>&1
+  export_rep ncu_mlp_group_g$MLP_G
+fi

@@ -40,22 +40,27 @@ for m, n, k in SHAPES:
         run(True)
         run(False)
     res = {}
+    graphs = {}
     for ck in (True, False):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             run(ck)
-        with torch.cuda.stream(s):
-            g.replay()
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(5):
+        graphs[ck] = g
+    ts = {True: [], False: []}
+    with torch.cuda.stream(s):
+        for ck in (True, False):
+            graphs[ck].replay()
+        torch.cuda.synchronize()
+        for _ in range(9):  # interleaved checked / unchecked measurements, median of each
+            for ck in (True, False):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                g.replay()
+                graphs[ck].replay()
                 e1.record(s)
                 torch.cuda.synchronize()
-                ts.append(e0.elapsed_time(e1) * 1e3 / REPS)
-        res[ck] = statistics.median(ts)
+                ts[ck].append(e0.elapsed_time(e1) * 1e3 / REPS)
+    for ck in (True, False):
+        res[ck] = statistics.median(ts[ck])
     L.lib.abftlp_gemm_weight_free(w)
     ov = 100 * (res[True] - res[False]) / res[False]
     rows.append({"m": m, "n": n, "k": k, "checked_us": res[True], "unchecked_us": res[False], "overhead_pct": ov,

@@ -1,0 +1,61 @@
+"""Heterogeneous grouped GEMM (abftlp_gemm_group_*): problems of different (m, n, k) in one persistent
+launch -- the D5 MLP layers. Every problem's C', checksum column, row flags and count equal the oracle's abft_gemm
+(P:src/gemm_abft.cpp:93-124) bit for bit, for each forced tile width, across repeated runs (self-resetting
+verdict scratch), and a corrupted B' (inject_weight_B after encoding) is flagged in exactly its own problem."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1000, 512, 64), (1000, 1024, 128), (700, 2048, 256), (300, 640, 100), (2050, 512, 512), (257, 384, 1000),
+          (64, 4096, 96)]
+
+
+def _inputs(seed, m, k, n):
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, 256, (m, k)).astype(np.uint8), rng.integers(-128, 128, (k, n)).astype(np.int8)
+
+
+@pytest.mark.parametrize("bn", [None, "64", "128", "256"])
+def test_group_matches_oracle(bn, monkeypatch):
+    from paper_2103_00130_b200 import gemm as G
+    if bn:
+        monkeypatch.setenv("ABFTLP_GEMM_GROUP_BN", bn)
+    ins = [_inputs(17 * i + 3, m, k, n) for i, (m, k, n) in enumerate(SHAPES)]
+    grp = G.AbftGemmGroup([(a, G.PackedEncodedWeight(b)) for a, b in ins])
+    for _ in range(3):
+        outs = grp.run()
+        torch.cuda.synchronize()
+        for (a, b), (c, cs, fl, err) in zip(ins, outs):
+            ct, fl_ref, err_ref = O.abft_gemm(a, b)
+            assert np.array_equal(c.cpu().numpy(), ct[:, :-1])
+            assert np.array_equal(cs.cpu().numpy(), ct[:, -1])
+            assert np.array_equal(fl.cpu().numpy(), fl_ref) and int(err.item()) == err_ref == 0
+
+
+def test_group_unchecked_and_weight_fault():
+    from paper_2103_00130_b200 import gemm as G
+    ins = [_inputs(5 * i + 1, m, k, n) for i, (m, k, n) in enumerate(SHAPES[:5])]
+    pbs = [G.PackedEncodedWeight(b) for _, b in ins]
+    plain = G.AbftGemmGroup(list(zip([a for a, _ in ins], pbs)), checked=False)
+    for (a, b), (c, *_rest) in zip(ins, plain.run()):
+        assert np.array_equal(c.cpu().numpy(), O.abft_gemm(a, b)[0][:, :-1])
+    # flip one bit of problem 2's encoded B (after encoding): only its rows are flagged, exactly as the oracle
+    # flags C' = A [B* | cs] with the corrupted B* and the pristine checksums
+    i, j, bit = 37, 11, 6
+    pbs[2].flip_bit(i, j, bit)
+    grp = G.AbftGemmGroup(list(zip([a for a, _ in ins], pbs)))
+    outs = grp.run()
+    torch.cuda.synchronize()
+    for q, ((a, b), (c, cs, fl, err)) in enumerate(zip(ins, outs)):
+        bb = b.copy()
+        cs_ref = O.row_checksums(b)
+        if q == 2:
+            bb[i, j] = np.int8(np.uint8(bb[i, j].view(np.uint8) ^ (1 << bit)).view(np.int8))
+        ct, fl_ref, err_ref = O.abft_gemm(a, bb, cs=cs_ref)
+        assert np.array_equal(c.cpu().numpy(), ct[:, :-1]) and np.array_equal(cs.cpu().numpy(), ct[:, -1])
+        assert np.array_equal(fl.cpu().numpy(), fl_ref) and int(err.item()) == err_ref
+        assert (err_ref > 0) == (q == 2)
