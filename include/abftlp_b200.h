@@ -253,6 +253,22 @@ abftlp_status abftlp_eb_group_set_bags(abftlp_eb_group* g, const int64_t* const*
                                        const int64_t* const* d_indices, const float* const* d_weights /* nullable */,
                                        abftlp_stream stream);
 
+/* ------------------------------------------------------------------ dual-encoded locate / correct
+ * After a checked GEMM flagged rows: the exact column checks of the dual encoding (column sums of A times B against
+ * the column sums of C', P:tests/dual_check.hpp:23-73) find the corrupted column; with the single flagged row that is
+ * the corrupted cell, and `correct` restores it (C -= delta) and re-runs the row check. status: 0 clean; 1 one cell
+ * located (row, col, delta = corrupted - clean); 2 the checksum column C'[row][n] was hit (recomputed when
+ * correcting); 3 not locatable (several errors); 4 a column mismatch with no flagged row (an error the mod-127 row
+ * check aliases). Synchronizes `stream`. Correction is beyond the reference (it stops at detection). */
+typedef struct {
+    int32_t status;
+    int64_t row, col, delta;
+    uint64_t rows_flagged, cols_mismatched;
+} abftlp_locate_result;
+abftlp_status abftlp_gemm_locate(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w, int32_t* d_c,
+                                 uint64_t ldc, int32_t* d_csum, uint64_t csum_ld, uint8_t* d_row_flags, int correct,
+                                 abftlp_locate_result* out, abftlp_stream stream);
+
 /* ------------------------------------------------------------------ heterogeneous grouped GEMM
  * Several checked (or plain) GEMMs of DIFFERENT shapes -- each its own A (u8, 16-byte aligned, lda % 16 == 0),
  * encoded weight, C', checksum column, row flags and count -- in ONE persistent launch (abft_gemm per problem,

@@ -81,6 +81,12 @@ class GemmProblem(C.Structure):
                 ("d_err_count", C.c_void_p)]
 
 
+class LocateResult(C.Structure):
+    """abftlp_locate_result."""
+    _fields_ = [("status", C.c_int32), ("row", C.c_int64), ("col", C.c_int64), ("delta", C.c_int64),
+                ("rows_flagged", C.c_uint64), ("cols_mismatched", C.c_uint64)]
+
+
 class Fault(C.Structure):
     _fields_ = [("active", i32), ("row", u64), ("col", u64), ("bit", u32)]
 
@@ -137,6 +143,7 @@ _SIGS = {
     "abftlp_eb_group_create": (i32, [vp, u32, vp, vp, vp, vp, vp, vp]),
     "abftlp_gemm_group_create": (i32, [vp, u32, i32, P(vp)]),
     "abftlp_gemm_group_run": (i32, [vp, vp]),
+    "abftlp_gemm_locate": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, i32, vp, vp]),
     "abftlp_gemm_group_free": (None, [vp]),
     "abftlp_eb_group_checked_scatter": (i32, [vp, u64, u64, u64, u64, vp, vp, vp]),
     "abftlp_eb_group_unchecked_scatter": (i32, [vp, u64, u64, u64, vp, vp]),

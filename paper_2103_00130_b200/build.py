@@ -19,7 +19,7 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = REPO / "build" / "abftlp"
 LIB = PKG / "libabftlp_b200.so"
-SOURCES = ["gemm.cu", "gemv.cu", "eb.cu", "lab.cu", "quant.cu", "runtime.cu", "campaign.cu", "hostio.cpp", "capi.cpp"]
+SOURCES = ["gemm.cu", "gemv.cu", "locate.cu", "eb.cu", "lab.cu", "quant.cu", "runtime.cu", "campaign.cu", "hostio.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -812,6 +812,25 @@ abftlp_status abftlp_eb_group_checked_scatter(const abftlp_eb_group* g, uint64_t
     });
 }
 
+// ============================================================ dual-encoded locate / correct
+abftlp_status abftlp_gemm_locate(const uint8_t* d_a, uint64_t m, uint64_t lda, const abftlp_gemm_weight* w, int32_t* d_c,
+                                 uint64_t ldc, int32_t* d_csum, uint64_t csum_ld, uint8_t* d_row_flags, int correct,
+                                 abftlp_locate_result* out, abftlp_stream stream) {
+    if (!w || !out) return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::LocateResult r =
+            abftk::gemm_locate(d_a, static_cast<int64_t>(m), static_cast<int64_t>(lda), *w->w, d_c, static_cast<int64_t>(ldc),
+                               d_csum, static_cast<int64_t>(csum_ld), d_row_flags, correct != 0, as_stream(stream));
+        out->status = r.status;
+        out->row = r.row;
+        out->col = r.col;
+        out->delta = r.delta;
+        out->rows_flagged = static_cast<uint64_t>(r.rows_flagged);
+        out->cols_mismatched = static_cast<uint64_t>(r.cols_mismatched);
+        return ABFTLP_OK;
+    });
+}
+
 // ============================================================ heterogeneous grouped GEMM
 abftlp_status abftlp_gemm_group_create(const abftlp_gemm_problem* problems, uint32_t count, int checked,
                                        abftlp_gemm_group** out) {

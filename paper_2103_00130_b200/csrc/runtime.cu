@@ -706,6 +706,94 @@ void gemm_group_free(GemmGroup* g) {
     delete g;
 }
 
+// ------------------------------------------------------------------ dual-encoded locate / correct
+LocateResult gemm_locate(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc,
+                         int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, bool correct, cudaStream_t st) {
+    if (!d_a || !d_c || !d_csum || !d_flags) throw std::invalid_argument("null argument");
+    if (w.batch != 1) throw std::invalid_argument("gemm_locate: batched weights are not supported");
+    if (m < 1 || lda < w.k || ldc < w.n || csum_ld < 1) throw std::invalid_argument("gemm_locate: bad dimensions");
+    if (m > (int64_t{1} << 24)) throw std::invalid_argument("gemm_locate: m too large");
+    LocateResult res;
+    std::vector<uint8_t> flags(static_cast<size_t>(m));
+    cuda_check(cudaMemcpyAsync(flags.data(), d_flags, static_cast<size_t>(m), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    constexpr int kRec = 8;
+    struct Scratch {
+        void* p = nullptr;
+        ~Scratch() { cudaFree(p); }
+    } sc;
+    const size_t col_bytes = sizeof(uint32_t) * static_cast<size_t>(w.k_pad);
+    cuda_check(cudaMalloc(&sc.p, col_bytes + 64 + kRec * 16 + 16), "cudaMalloc(locate scratch)");
+    uint32_t* colsum = static_cast<uint32_t*>(sc.p);
+    uint8_t* tail = static_cast<uint8_t*>(sc.p) + col_bytes;
+    uint32_t* nbad = reinterpret_cast<uint32_t*>(tail);
+    int32_t* row_cs = reinterpret_cast<int32_t*>(tail + 16);
+    int64_t* bad_col = reinterpret_cast<int64_t*>(tail + 64);
+    long long* bad_delta = reinterpret_cast<long long*>(tail + 64 + kRec * 8);
+    cuda_check(cudaMemsetAsync(nbad, 0, 4, st), "cudaMemsetAsync");
+    cuda_check(launch_locate_colsum_a(d_a, m, w.k, lda, colsum, w.k_pad, st), "locate_colsum_a_kernel");
+    cuda_check(launch_locate_columns(colsum, w, d_c, m, ldc, nbad, bad_col, bad_delta, kRec, st), "locate_columns_kernel");
+    uint32_t hb = 0;
+    int64_t hcol[kRec];
+    long long hdel[kRec];
+    cuda_check(cudaMemcpyAsync(&hb, nbad, 4, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(hcol, bad_col, sizeof(hcol), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(hdel, bad_delta, sizeof(hdel), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    int64_t row = -1;
+    for (int64_t i = 0; i < m; ++i)
+        if (flags[static_cast<size_t>(i)]) {
+            ++res.rows_flagged;
+            row = i;
+        }
+    res.cols_mismatched = hb;
+    if (res.rows_flagged == 0 && hb == 0) return res;  // clean
+    if (res.rows_flagged == 1 && hb == 1) {
+        res.status = 1;
+        res.row = row;
+        res.col = hcol[0];
+        res.delta = hdel[0];
+        if (correct) {
+            int32_t* cell = d_c + row * ldc + res.col;
+            int32_t v = 0;
+            cuda_check(cudaMemcpyAsync(&v, cell, 4, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+            cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            // the corrupted element differs from the clean one by exactly delta (both int32)
+            v = static_cast<int32_t>(static_cast<int64_t>(v) - res.delta);
+            cuda_check(cudaMemcpyAsync(cell, &v, 4, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync");
+        }
+    } else if (res.rows_flagged == 1 && hb == 0) {
+        res.status = 2;  // every data column checks out: C'[row][n] itself was hit
+        res.row = row;
+        res.col = w.n;
+        if (correct) {
+            cuda_check(launch_locate_row_checksum(d_a + row * lda, w.k, w.cs, row_cs, st), "locate_row_checksum_kernel");
+            cuda_check(cudaMemcpyAsync(d_csum + row * csum_ld, row_cs, 4, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+        }
+    } else if (res.rows_flagged == 0) {
+        res.status = 4;
+        res.col = hcol[0];
+        return res;
+    } else {
+        res.status = 3;
+        return res;
+    }
+    if (correct) {  // re-check the repaired row (the reference's comparison); it must pass now
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(tail + 32);
+        Workspace& ws = ws_for(st);
+        {
+            std::lock_guard<std::mutex> g(ws.mu);
+            cuda_check(launch_verify(d_c + row * ldc, ldc, d_csum + row * csum_ld, csum_ld, 1, w.n, d_flags + row, cnt,
+                                     ws.small + 2, ws.small + 3, st),
+                       "verify_kernel");
+        }
+        uint32_t left = 1;
+        cuda_check(cudaMemcpyAsync(&left, cnt, 4, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+        cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        if (left != 0) res.status = 3;  // the repair did not restore the row: more than one error
+    }
+    return res;
+}
+
 void check_requant_params(const RequantDev& q) {
     if (!(q.sC > 0.0)) throw std::invalid_argument("requantize: scaleC must be positive");
 }

@@ -88,6 +88,17 @@ struct GemmGroup {
 GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked);
 void gemm_group_run(const GemmGroup& g, cudaStream_t st);
 void gemm_group_free(GemmGroup* g);
+// Dual-encoded locate / correct of a checked result (locate.cu): the flagged row from the mod-127 row checks plus the
+// exact column checks against the column sums of A. status: 0 clean, 1 one cell located (corrected when asked),
+// 2 the checksum column itself corrupted (recomputed when asked), 3 not locatable (several rows / columns),
+// 4 column mismatch without a flagged row (an error the mod-127 row check aliases).
+struct LocateResult {
+    int status = 0;
+    int64_t row = -1, col = -1, delta = 0;
+    int64_t rows_flagged = 0, cols_mismatched = 0;
+};
+LocateResult gemm_locate(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc,
+                         int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, bool correct, cudaStream_t st);
 void requantize(const int32_t* d_c, int64_t ldc, int64_t m, int64_t n, const int32_t* d_row_sum_a,
                 const int32_t* d_col_sum_b, const RequantDev& q, uint8_t* d_out, int64_t ld_out, cudaStream_t st);
 void row_sums_u8(const uint8_t* d_a, int64_t m, int64_t k, int64_t lda, int32_t* d_out, cudaStream_t st);
@@ -160,6 +171,11 @@ void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
 cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b,
                                const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
 cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int pairs, const GemmParams& p, cudaStream_t st);
+cudaError_t launch_locate_colsum_a(const uint8_t* a, int64_t m, int64_t k, int64_t lda, uint32_t* out, int64_t k_pad,
+                                   cudaStream_t st);
+cudaError_t launch_locate_columns(const uint32_t* colsum_a, const GemmWeight& w, const int32_t* c, int64_t m, int64_t ldc,
+                                  uint32_t* nbad, int64_t* bad_col, long long* bad_delta, int max_record, cudaStream_t st);
+cudaError_t launch_locate_row_checksum(const uint8_t* a_row, int64_t k, const int8_t* cs, int32_t* out, cudaStream_t st);
 cudaError_t launch_read_encoded(const GemmWeight& w, int8_t* out, cudaStream_t st);
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st);
 cudaError_t launch_verify(const int32_t* c, int64_t ldc, const int32_t* csum, int64_t csum_ld, int64_t m, int64_t n,

@@ -141,6 +141,21 @@ def abft_gemm(a, pb: PackedEncodedWeight, fault: tuple[int, int, int] | None = N
     return AbftGemmResult(IntermediateMatrix(ctemp, True), int(err.item()), flags)
 
 
+def locate_and_correct(a, pb: PackedEncodedWeight, res: AbftGemmResult, correct: bool = True, stream=None):
+    """Dual-encoded locate (and repair) of a flagged checked result in place (abftlp_gemm_locate; the reference's
+    dual-encoded oracle P:tests/dual_check.hpp:23-73 as a device operation). Returns the abftlp_locate_result."""
+    at = to_device(a, torch.uint8)
+    m, k = (int(s) for s in at.shape)
+    n = pb.n()
+    data = res.cTemp.data
+    out = _lib.LocateResult()
+    _lib.call("abftlp_gemm_locate", ptr(at), m, k, pb.handle, ptr(data), n + 1, C.c_void_p(data.data_ptr() + 4 * n),
+              n + 1, ptr(res.rowFlags), 1 if correct else 0, C.byref(out), stream_handle(stream))
+    if correct and out.status in (1, 2):
+        res.errCount = int(res.rowFlags.to(torch.int64).sum().item())
+    return out
+
+
 def plain_gemm(a, b) -> IntermediateMatrix:
     """Unchecked baseline (P:src/gemm_abft.cpp:102-111): the same kernel with checking compiled out."""
     at = to_device(a, torch.uint8)
