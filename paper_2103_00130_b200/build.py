@@ -19,6 +19,7 @@ REPO = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = REPO / "build" / "abftlp"
 LIB = PKG / "libabftlp_b200.so"
+CLI = PKG / "abft_cli"
 SOURCES = ["gemm.cu", "gemv.cu", "locate.cu", "eb.cu", "lab.cu", "quant.cu", "runtime.cu", "campaign.cu", "hostio.cpp", "capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -63,15 +64,30 @@ def build(force: bool = False, jobs: int | None = None) -> Path:
             o.unlink()
     with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(_compile, SOURCES))
-    if LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lpthread"]
+    if not (LIB.exists() and LIB.stat().st_mtime >= max(o.stat().st_mtime for o in objs)):
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", str(tmp)] + [str(o) for o in objs] + ["-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        os.replace(tmp, LIB)
+    build_cli()
+    return LIB
+
+
+def build_cli() -> Path:
+    """abft_cli (csrc/cli.cpp): the command-line front end, linked against the library (rpath $ORIGIN)."""
+    src = CSRC / "cli.cpp"
+    deps = [src, LIB, REPO / "include" / "abftlp.h"]
+    if CLI.exists() and CLI.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return CLI
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-I", str(REPO / "include"), str(src), "-o", str(CLI), "-L", str(PKG),
+           "-labftlp_b200", "-Wl,-rpath,$ORIGIN"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+        raise RuntimeError(f"abft_cli build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":
