@@ -336,6 +336,12 @@ __device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 #endif
 }
+// base + a * b with a, b unsigned 32-bit (one IMAD.WIDE.U32)
+__device__ __forceinline__ const uint8_t* mad_wide_u32(uint32_t a, uint32_t b, const uint8_t* base) {
+    unsigned long long r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(reinterpret_cast<unsigned long long>(base)));
+    return reinterpret_cast<const uint8_t*>(r);
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -377,14 +383,16 @@ struct __align__(16) LookupConst {
     float b, w;
     double term;
 };
-template <int BPL>
+// K16: s8 rows without bag weights need only (scale, bias, cSum term) per lookup -- 16 bytes, written over the
+// lookup's landed metadata record, so such kernels carry no separate constant array (three resident blocks per SM
+// at 128-byte slices instead of two).
+template <int BPL, bool K16, bool WEIGHTED>
 struct AsyncStage {
     static constexpr int NST = AsyncRing<BPL>::NST;
     uint8_t rows[NST][kChunk][32 * BPL];  // this warp's column slice of each gathered row
     uint4 meta[NST][kChunk];              // EbMetaF32 (16 B) or EbMetaF16 (first 8 B); zero = neutral slot
-    float w[NST][kChunk];
-    int64_t off[kChunk];                  // row byte offsets of the chunk being issued, -1 = none
-    LookupConst k[kChunk];                // constants of the chunk being consumed
+    float w[NST][WEIGHTED ? kChunk : 1];
+    LookupConst k[K16 ? 1 : kChunk];      // constants of the chunk being consumed (K16: in place in meta[])
 };
 
 // The splice multiplication is exact when s*2^23 and s/16 are exact normal floats (and s is finite); a zero scale
@@ -492,15 +500,21 @@ __device__ __forceinline__ unsigned long long decode_pair_bits(W w, int c) {
 #define ABFT_EB_MINB_SMALL 2  // resident blocks per SM asked of ptxas for 32-byte slices (E4-class rows)
 #endif
 template <int ELEM, int SCALE, int CPL, int WPB, bool WEIGHTED, bool CHECKED>
-__global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? ABFT_EB_MINB_SMALL : 2)
+#ifndef ABFT_EB_MINB_K16
+#define ABFT_EB_MINB_K16 3  // s8 unweighted 128-byte slices (D5): the in-place constants leave room for a third block
+#endif
+__global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? ABFT_EB_MINB_SMALL
+                                       : (ELEM == kEbS8 && !WEIGHTED && CPL == 4) ? ABFT_EB_MINB_K16 : 2)
     eb_bag_async_kernel(const EbParams p, int log2d) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
     constexpr int SLICE = 32 * BPL;        // bytes of a row this warp needs
     constexpr int PIECES = SLICE / 16;     // 16-B copies per row slice
     constexpr int PER_LANE = kChunk * PIECES / 32;
     constexpr int GROUPS = 8 / WPB;        // bag groups (WPB warps each) per block
+    constexpr bool K16 = ELEM == kEbS8 && !WEIGHTED;  // per-lookup constants fit the landed metadata slot
+    using Stage = AsyncStage<BPL, K16, WEIGHTED>;
     extern __shared__ __align__(16) uint8_t eb_smem[];
-    AsyncStage<BPL>& S = reinterpret_cast<AsyncStage<BPL>*>(eb_smem)[threadIdx.x >> 5];
+    Stage& S = reinterpret_cast<Stage*>(eb_smem)[threadIdx.x >> 5];
     __shared__ double part_sum[8];
     __shared__ int part_emax[8], part_umin[8];
     __shared__ long long grp_bag[GROUPS];
@@ -524,16 +538,21 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
     // Persistent bag groups: each takes the next bag from a global counter, so long and short bags
     // balance across SMs (the work per bag varies 150x in E4). The next bag id is requested while the
     // current one is processed, hiding the atomic's round trip.
-    constexpr int NST = AsyncStage<BPL>::NST;
+    constexpr int NST = Stage::NST;
     // The first bag of every group is static (its global group id); later ones come from the counter,
     // offset by the number of groups -- 2k simultaneous atomics on one address at launch cost ~2.5 us.
     const unsigned long long n_groups = static_cast<unsigned long long>(gridDim.x) * GROUPS;
+    // (inline PTX: with atomicAdd the compiler aggregates the warp's request and shuffles the RESULT out right
+    // after the atomic, which stalls the bag's start on the atomic's round trip; the ticket is only needed when
+    // the bag is done)
     auto fetch = [&]() -> unsigned long long {
-        unsigned long long b0 = 0;
-        if (slice == 0 && lane == 0) b0 = n_groups + atomicAdd(p.ws_bag_ctr, 1ull);
-        return b0;
+        unsigned long long ticket = 0;
+        if (slice == 0 && lane == 0)
+            asm volatile("atom.global.add.u64 %0, [%1], 1;" : "=l"(ticket) : "l"(p.ws_bag_ctr));
+        return ticket;
     };
-    auto share = [&](unsigned long long b0) -> int64_t {  // broadcast lane 0 / slice 0's id to the group
+    auto share = [&](unsigned long long ticket) -> int64_t {  // broadcast lane 0 / slice 0's id to the group
+        const unsigned long long b0 = n_groups + ticket;
         if constexpr (WPB == 1) {
             return static_cast<int64_t>(__shfl_sync(0xffffffffu, b0, 0));
         } else {
@@ -585,7 +604,22 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
         double csum = 0.0;
         bool oob = false;
         const int64_t beg = tv.offsets[lb], end = tv.offsets[lb + 1];
-        const int nchunks = static_cast<int>((end - beg + kChunk - 1) / kChunk);
+        // bag length in 32 bits; a table without rows (every lookup out of range) or an absurd length (corrupt
+        // offsets) reports out_of_range and pools nothing
+        int len = 0;
+        if (end > beg) {
+            if (tv.rows <= 0 || end - beg > (int64_t{1} << 30))
+                oob = true;
+            else
+                len = static_cast<int>(end - beg);
+        }
+        const int nchunks = (len + kChunk - 1) / kChunk;
+        const int64_t* const idx0 = tv.indices + beg + lane;
+        const float* const w0 = WEIGHTED ? tv.weights + beg + lane : nullptr;
+        const uint32_t meta_stride32 = static_cast<uint32_t>(tv.meta_stride);
+        // this lane's 16-byte part of a row slice (row 0) and the row stride (< 2^32: checked by the launcher)
+        const uint8_t* const src0 = tv.data + slice_byte + (lane % PIECES) * 16;
+        const uint32_t stride32 = static_cast<uint32_t>(tv.row_stride);
         // Issue the gathers of chunk `ch` (indices `ix`, one per lane) into ring slot ch % NST. Slots past
         // the bag or out of range get a neutral record (scale = bias = 0, weight 1): they add +0.0, an
         // exact no-op on the running sums (which start at +0.0 and never become -0.0 in round-to-nearest),
@@ -594,42 +628,35 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
         auto issue = [&](int ch, int64_t ix) {
             if (ch < nchunks) {
                 const int sl = ch % NST;
-                const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
-                const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+                const int cnt = min(kChunk, len - ch * kChunk);
                 const bool valid = lane < cnt && static_cast<uint64_t>(ix) < static_cast<uint64_t>(tv.rows);
                 if (lane < cnt && !valid) oob = true;
-                S.off[lane] = valid ? ix * tv.row_stride + slice_byte : -1;
+                // an out-of-range lookup gathers row 0 under its neutral record (a table without rows has no chunks)
+                const uint32_t rid = valid ? static_cast<uint32_t>(ix) : 0u;
                 if (valid) {
-                    if (SCALE == kEbF32 || p.l2_only)  // (packed records leave 16 B after the f16 metadata)
-                        cp_async16(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
+                    const uint8_t* const mrec = mad_wide_u32(rid, meta_stride32, reinterpret_cast<const uint8_t*>(tv.meta));
+                    if constexpr (SCALE == kEbF32)
+                        cp_async16(&S.meta[sl][lane], mrec);
                     else
-                        cp_async8(&S.meta[sl][lane], reinterpret_cast<const uint8_t*>(tv.meta) + ix * tv.meta_stride);
-                    if constexpr (WEIGHTED) cp_async4(&S.w[sl][lane], tv.weights + base + lane);
+                        cp_async8(&S.meta[sl][lane], mrec);
+                    if constexpr (WEIGHTED) cp_async4(&S.w[sl][lane], w0 + ch * kChunk);
                 } else {
                     S.meta[sl][lane] = make_uint4(0u, 0u, 0u, 0u);
                     if constexpr (WEIGHTED) S.w[sl][lane] = 1.0f;
                 }
-                __syncwarp();
+                // row pieces: piece = lane + 32 i covers row piece / PIECES, 16-byte part piece % PIECES; the row id
+                // comes from the lane that holds the lookup (one shuffle, one 32 x 32 -> 64-bit multiply-add)
+                uint8_t* const dst0 = &S.rows[sl][0][0] + lane * 16;
 #pragma unroll
                 for (int i = 0; i < PER_LANE; ++i) {
-                    const int piece = lane + 32 * i;
-                    const int r = piece / PIECES, q = piece % PIECES;
-                    const int64_t o = S.off[r];
-                    if (o >= 0) {
-                        if (p.l2_only)
-                            cp_async16(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
-                        else
-                            cp_async16_l1(&S.rows[sl][r][q * 16], tv.data + o + q * 16);
-                    }
+                    const int r = (lane + 32 * i) / PIECES;
+                    const uint32_t rr = __shfl_sync(0xffffffffu, rid, r);
+                    if (r < cnt) cp_async16_l1(dst0 + 512 * i, mad_wide_u32(rr, stride32, src0));
                 }
-                __syncwarp();  // S.off is reused by the next issue
             }
             cp_async_commit();
         };
-        auto index_of = [&](int ch) -> int64_t {
-            const int64_t e = beg + static_cast<int64_t>(ch) * kChunk + lane;
-            return e < end ? tv.indices[e] : -1;
-        };
+        auto index_of = [&](int ch) -> int64_t { return ch * kChunk + lane < len ? idx0[ch * kChunk] : -1; };
         // prologue: NST-1 chunks in flight, the index of the next one loaded ahead
         {
             int64_t ixs[NST - 1];
@@ -649,9 +676,10 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
             ix_ahead = ch + NST < nchunks ? index_of(ch + NST) : -1;
             cp_async_wait<NST - 1>();  // chunk ch has landed
             __syncwarp();
+#ifdef ABFT_EB_TRACE  // (debug build: when the bag's first chunk landed)
             if (tr && lane == 0 && ch == 0 && nb_done < 4) tr[2 + 3 * nb_done] = globaltimer();
-            const int64_t base = beg + static_cast<int64_t>(ch) * kChunk;
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(kChunk), end - base));
+#endif
+            const int cnt = min(kChunk, len - ch * kChunk);
             // the chunk's per-lookup constants, lane-parallel (a neutral slot has s = b = 0, w = 1: term +0.0)
             bool fast;
             {
@@ -659,15 +687,22 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
                 int32_t rs;
                 smem_meta<SCALE>(S.meta[sl][lane], s, b, rs);
                 const float w = WEIGHTED ? S.w[sl][lane] : 1.0f;
-                LookupConst kc;
-                kc.s_lo = s;
-                kc.s_hi = ELEM == kEbU4 ? s * 0.0625f : s;
-                kc.c_lo = -(kc.s_lo * 8388608.0f);
-                kc.c_hi = -(kc.s_hi * 8388608.0f);
-                kc.b = b;
-                kc.w = w;
-                kc.term = (CHECKED && slice == 0) ? csum_term(s, b, rs, w, dd, WEIGHTED) : 0.0;
-                S.k[lane] = kc;
+                const double term = (CHECKED && slice == 0) ? csum_term(s, b, rs, w, dd, WEIGHTED) : 0.0;
+                if constexpr (K16) {
+                    S.meta[sl][lane] = make_uint4(__float_as_uint(s), __float_as_uint(b),
+                                                  static_cast<uint32_t>(__double2loint(term)),
+                                                  static_cast<uint32_t>(__double2hiint(term)));
+                } else {
+                    LookupConst kc;
+                    kc.s_lo = s;
+                    kc.s_hi = ELEM == kEbU4 ? s * 0.0625f : s;
+                    kc.c_lo = -(kc.s_lo * 8388608.0f);
+                    kc.c_hi = -(kc.s_hi * 8388608.0f);
+                    kc.b = b;
+                    kc.w = w;
+                    kc.term = term;
+                    S.k[lane] = kc;
+                }
                 // u8 / u4 chunks whose every scale admits the exact splice FMA take the short column path
                 fast = ELEM != kEbS8 && __all_sync(0xffffffffu, splice_safe(s));
                 __syncwarp();
@@ -689,8 +724,14 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         wd[u] = lds_word<BPL>(&S.rows[sl][t0 + u][lane * BPL]);
-                        ka[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].s_lo);
-                        kb[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].b);
+                        if constexpr (K16) {  // (s, b, term) in the metadata slot
+                            const uint4 m = S.meta[sl][t0 + u];
+                            ka[u] = make_float4(__uint_as_float(m.x), 0.f, 0.f, 0.f);
+                            kb[u] = make_float4(__uint_as_float(m.y), 1.0f, __uint_as_float(m.z), __uint_as_float(m.w));
+                        } else {
+                            ka[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].s_lo);
+                            kb[u] = *reinterpret_cast<const float4*>(&S.k[t0 + u].b);
+                        }
                     }
                     if constexpr (CPL >= 2) {
                         unsigned long long xv[4][NP];
@@ -768,36 +809,51 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
         csum = __shfl_sync(0xffffffffu, csum, 0);
         if (__any_sync(0xffffffffu, oob) && lane == 0 && p.status) atomicOr(p.status, 1);
         float* dst = out_row(tv, lb) + slice * 32 * CPL + lane * CPL;
+        if (CPL % 4 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
+            for (int c = 0; c + 3 < CPL; c += 4)
+                *reinterpret_cast<float4*>(dst + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) dst[c] = acc[c];
+        }
         if constexpr (CHECKED) {
-            int emax = -100000, umin = 100000;
+            // Exactness of the order-free fp64 sum from the outputs' biased exponents alone: every nonzero output is a
+            // multiple of its ulp 2^(e - 150) and below 2^(e - 126) (denormals: e = 1), so with emax / emin over the
+            // bag's outputs every partial sum of the d values is a multiple of 2^(emin - 150) below
+            // 2^(emax - 126 + log2 d): exact in fp64 when emax - emin + 24 + log2 d <= 53.
+            uint32_t emax = 0u, emin = 255u;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) bit_span(acc[c], emax, umin);
+            for (int c = 0; c < CPL; ++c) {
+                const uint32_t bits = __float_as_uint(acc[c]) & 0x7FFFFFFFu;
+                const uint32_t e = max(bits >> 23, 1u);
+                if (bits) {
+                    emax = max(emax, e);
+                    emin = min(emin, e);
+                }
+            }
             double sm = 0.0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) sm = __dadd_rn(sm, static_cast<double>(acc[c]));
+            emax = __reduce_max_sync(0xffffffffu, emax);
+            emin = __reduce_min_sync(0xffffffffu, emin);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-                umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
-                sm = __dadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, o));
-            }
+            for (int o = 16; o > 0; o >>= 1) sm = __dadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, o));
             if constexpr (WPB > 1) {
                 if (lane == 0) {
                     part_sum[warp] = sm;
-                    part_emax[warp] = emax;
-                    part_umin[warp] = umin;
+                    part_emax[warp] = static_cast<int>(emax);
+                    part_umin[warp] = static_cast<int>(emin);
                 }
             }
             // only the WPB warps of this bag synchronise (their slices and outputs are complete)
             group_sync();
             if (slice == 0) {
-                int E = emax, U = umin;  // WPB == 1: the warp's own reduction, no shared-memory round trip
+                int E = static_cast<int>(emax), U = static_cast<int>(emin);  // WPB == 1: the warp's own reduction
                 double exact = sm;
                 if constexpr (WPB > 1) {
-                    E = -100000;
-                    U = 100000;
+                    E = 0;
+                    U = 255;
                     exact = 0.0;
 #pragma unroll
                     for (int s2 = 0; s2 < WPB; ++s2) {
@@ -807,9 +863,9 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
                     }
                 }
                 double rsum;
-                if (E == -100000) {
+                if (E == 0) {
                     rsum = 0.0;
-                } else if (E + 1 + log2d - U <= 53) {
+                } else if (E - U + 24 + log2d <= 53) {
                     rsum = exact;  // every partial sum is exact, so any order gives the reference's value
                 } else {
                     rsum = 0.0;  // the reference's sequential order over the stored outputs
@@ -1040,7 +1096,7 @@ static cudaError_t launch_bag_fast(const EbParams& p, bool checked, int log2d, c
 template <int ELEM, int SCALE, int CPL, int WPB, bool W, bool CK>
 static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t st) {
     constexpr int BPL = ELEM == kEbU4 ? CPL / 2 : CPL;
-    constexpr int smem = 8 * static_cast<int>(sizeof(AsyncStage<BPL>));
+    constexpr int smem = 8 * static_cast<int>(sizeof(AsyncStage<BPL, ELEM == kEbS8 && !W, W>));
     auto kern = eb_bag_async_kernel<ELEM, SCALE, CPL, WPB, W, CK>;
     static bool attr[kMaxDevices] = {};  // per device
     static int per_sm_dev[kMaxDevices] = {};
@@ -1126,7 +1182,9 @@ static cudaError_t launch_bag_elem(const EbParams& p, bool checked, int log2d, c
         const int64_t d32 = d / 32;  // columns per lane when one warp owns the whole row
         const int wpb = pick_wpb(p.num_bags, d32, ELEM == kEbU4);
         const int64_t cpl = d32 / wpb;
-        const bool async_ok = (p.row_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 16) == 0 &&
+        // (the gather kernel forms row addresses as a 32 x 32 -> 64-bit multiply-add)
+        const bool async_ok = (p.tables || (p.row_stride < (int64_t{1} << 32) && p.rows <= (int64_t{1} << 32))) &&
+                              (p.row_stride % 16) == 0 && (reinterpret_cast<uintptr_t>(p.data) % 16) == 0 &&
                               (reinterpret_cast<uintptr_t>(p.meta) % 16) == 0 && !std::getenv("ABFTLP_EB_SYNC");
         if (p.tables && !async_ok) return cudaErrorNotSupported;  // grouped tables: async kernel only
         if (async_ok) {
@@ -1173,6 +1231,9 @@ cudaError_t launch_eb_bags(int elem, int scale, const EbParams& p, bool checked,
     if (p.num_bags <= 0) return cudaSuccess;
     int log2d = 0;
     while ((int64_t{1} << log2d) < p.dim) ++log2d;
+#ifdef ABFT_EB_DEV  // (development: compile one element / scale type only, for quick SASS inspection)
+    return launch_bag_elem<ABFT_EB_DEV, kEbF32>(p, checked, log2d, st);
+#endif
     if (scale == kEbF32) {
         if (elem == kEbS8) return launch_bag_elem<kEbS8, kEbF32>(p, checked, log2d, st);
         if (elem == kEbU8) return launch_bag_elem<kEbU8, kEbF32>(p, checked, log2d, st);

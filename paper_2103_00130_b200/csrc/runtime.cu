@@ -943,14 +943,6 @@ uint64_t eb_table_validate(const EbTable& t, const int32_t* d_given_sums, cudaSt
     return h;
 }
 
-// Gather policy: L1-allocating gathers (Zipf-hot rows are then served by L1). Through L2 only (ABFTLP_EB_L2ONLY=1)
-// measured no faster for the packed 64-byte E4 records (26.6 us either way) and 1.3x / 2.3x slower for E3 / D5.
-static int eb_l2_only(const EbTable& t) {
-    (void)t;
-    if (const char* e = std::getenv("ABFTLP_EB_L2ONLY")) return std::atoi(e) != 0 ? 1 : 0;
-    return 0;
-}
-
 void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices, int64_t num_bags,
             const float* d_weights, float* d_out, int64_t ld_out, bool checked, uint8_t* d_flags, double* d_rsum,
             double* d_csum, uint32_t* d_flag_count, int32_t* d_status, cudaStream_t st, const EbScatter* scatter) {
@@ -991,7 +983,6 @@ void eb_run(const EbTable& t, const int64_t* d_offsets, const int64_t* d_indices
     p.ws_bag_ctr = reinterpret_cast<unsigned long long*>(ws.small + 6);
     p.trace = g_eb_trace;
     p.neg_zero = -0.0f;
-    p.l2_only = eb_l2_only(t);
     if (scatter) {
         p.out_dest = scatter->out_dest;
         p.flag_dest = checked ? scatter->flag_dest : nullptr;
@@ -1039,7 +1030,8 @@ EbGroup* eb_group_create(const EbTable* const* tables, int64_t ntables, const in
         // the fused launch runs the 16-byte cp.async gather kernel for every table with table 0's strides
         const bool al = (reinterpret_cast<uintptr_t>(h[i].data) % 16) == 0 && (h[i].row_stride % 16) == 0 &&
                         (reinterpret_cast<uintptr_t>(h[i].meta) % 16) == 0;
-        fused = fused && al && t->dim % 32 == 0 && h[i].row_stride == h[0].row_stride &&
+        fused = fused && al && t->dim % 32 == 0 && h[i].row_stride == h[0].row_stride && h[i].rows <= (int64_t{1} << 32) &&
+                h[i].row_stride < (int64_t{1} << 32) &&
                 h[i].meta_stride == h[0].meta_stride && (t->packed != nullptr) == (tables[0]->packed != nullptr);
     }
     auto* g = new EbGroup();
@@ -1131,7 +1123,6 @@ void eb_group_run(const EbGroup& g, int64_t bags_per_table, int64_t ld_out, int6
     p.ws_bag_ctr = reinterpret_cast<unsigned long long*>(ws.small + 6);
     p.trace = g_eb_trace;
     p.neg_zero = -0.0f;
-    p.l2_only = eb_l2_only(t0);
     p.bags_per_dest = bags_per_dest;
     p.flag_ld = flag_ld;
     p.tables = g.d_desc;
