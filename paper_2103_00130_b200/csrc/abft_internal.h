@@ -209,6 +209,7 @@ struct EbParams {
     unsigned long long* ws_bag_ctr;  // persistent kernels' next-bag counter (self-resetting)
     unsigned long long* trace;       // debug: per-warp timeline (16 slots), nullptr = off
     float neg_zero;                  // -0.0f, passed at run time (see f2_fma in eb.cu)
+    int zero_rt;                     // 0, passed at run time (see the bag ticket in eb_bag_async_kernel)
     // scatter mode (table-wise sharded exchange fused into the lookups): when out_dest is set, bag b
     // writes out_dest[b / bags_per_dest] + (b % bags_per_dest) * ld_out and its flag to
     // flag_dest[b / bags_per_dest][(b % bags_per_dest) * flag_ld] (pointers may be NVLink peer memory)

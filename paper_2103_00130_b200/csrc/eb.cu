@@ -28,12 +28,31 @@ namespace abftk {
 int device_sm_count();
 
 // Output row / flag slot of a bag: local buffers, or a destination table (sharded exchange, EbParams).
+// (bag ids below 2^32 divide in 32 bits: a 64-bit divide is a ~40-instruction sequence on the per-bag path)
+__device__ __forceinline__ void dest_of(const EbParams& p, int64_t bag, int64_t& dest, int64_t& slot) {
+    if (bag <= 0xFFFFFFFFll && p.bags_per_dest <= 0xFFFFFFFFll) {
+        const uint32_t d = static_cast<uint32_t>(bag) / static_cast<uint32_t>(p.bags_per_dest);
+        dest = d;
+        slot = static_cast<uint32_t>(bag) - d * static_cast<uint32_t>(p.bags_per_dest);
+    } else {
+        dest = bag / p.bags_per_dest;
+        slot = bag - dest * p.bags_per_dest;
+    }
+}
 __device__ __forceinline__ float* out_row(const EbParams& p, int64_t bag) {
-    if (p.out_dest) return p.out_dest[bag / p.bags_per_dest] + (bag % p.bags_per_dest) * p.ld_out;
+    if (p.out_dest) {
+        int64_t d, sl;
+        dest_of(p, bag, d, sl);
+        return p.out_dest[d] + sl * p.ld_out;
+    }
     return p.out + bag * p.ld_out;
 }
 __device__ __forceinline__ uint8_t* flag_slot(const EbParams& p, int64_t bag) {
-    if (p.flag_dest) return p.flag_dest[bag / p.bags_per_dest] + (bag % p.bags_per_dest) * p.flag_ld;
+    if (p.flag_dest) {
+        int64_t d, sl;
+        dest_of(p, bag, d, sl);
+        return p.flag_dest[d] + sl * p.flag_ld;
+    }
     return p.flags ? p.flags + bag : nullptr;
 }
 
@@ -546,9 +565,18 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
     // after the atomic, which stalls the bag's start on the atomic's round trip; the ticket is only needed when
     // the bag is done)
     auto fetch = [&]() -> unsigned long long {
-        unsigned long long ticket = 0;
-        if (slice == 0 && lane == 0)
-            asm volatile("atom.global.add.u64 %0, [%1], 1;" : "=l"(ticket) : "l"(p.ws_bag_ctr));
+        // (atom.inc on the counter's low word; bag ids fit 32 bits -- the launcher refuses larger batches. The address
+        // carries laneid * zero_rt, zero at run time: on an address it can prove warp-uniform ptxas aggregates the
+        // atomic -- also an inline-PTX one -- and shuffles the result out at once, which stalls the bag's start on the
+        // atomic's round trip)
+        uint32_t ticket = 0;
+        if (slice == 0 && lane == 0) {
+            uint32_t lid;  // (read here: inside this branch the compiler knows `lane` is 0)
+            asm volatile("mov.u32 %0, %%laneid;" : "=r"(lid));
+            asm volatile("atom.global.inc.u32 %0, [%1], 0xffffffff;"
+                         : "=r"(ticket)
+                         : "l"(reinterpret_cast<uint32_t*>(p.ws_bag_ctr) + 2 * lid * p.zero_rt));
+        }
         return ticket;
     };
     auto share = [&](unsigned long long ticket) -> int64_t {  // broadcast lane 0 / slice 0's id to the group
@@ -573,11 +601,9 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
         EbParams tv = p;
         int64_t lb = bag;  // bag index within its table
         if (p.tables) {
-            // 32-bit division when the launch's bag ids fit (a 64-bit divide is a ~40-instruction sequence
-            // on the per-bag path)
-            const int64_t t = p.num_bags <= 0xFFFFFFFFll
-                                  ? static_cast<int64_t>(static_cast<uint32_t>(bag) / static_cast<uint32_t>(p.bags_per_table))
-                                  : bag / p.bags_per_table;
+            // 32-bit division: bag ids fit (the launcher refuses larger batches), and a 64-bit divide is a
+            // ~40-instruction sequence on the per-bag path
+            const int64_t t = static_cast<int64_t>(static_cast<uint32_t>(bag) / static_cast<uint32_t>(p.bags_per_table));
             lb = bag - t * p.bags_per_table;
             const EbTableDesc& dsc = p.tables[t];
             tv.data = dsc.data;
@@ -1112,6 +1138,7 @@ static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t s
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, smem);
         per_sm = (e != cudaSuccess || o < 1) ? 1 : o;
     }
+    if (p.num_bags >= (int64_t{1} << 31)) return cudaErrorInvalidValue;  // 32-bit bag tickets
     const int64_t need = (p.num_bags + (8 / WPB) - 1) / (8 / WPB);
     const int64_t cap = static_cast<int64_t>(per_sm) * device_sm_count();
     const unsigned blocks = static_cast<unsigned>(need < cap ? need : cap);
