@@ -78,7 +78,8 @@ constexpr int kMaxGemmGroup = 16;  // problems of different shapes in one groupe
 struct GemmParams {
     int m, n, k;       // logical sizes (n excludes the checksum column)
     int k_blocks;      // 128-byte K blocks
-    int n_tiles;       // N tiles of BN columns
+    int n_tiles;       // N tiles of tile_w columns
+    int tile_w;        // columns per N tile: BN, or (grouped launches) a multiple of 32 below it, the MMA's N
     int m_tiles;       // 256-row pair tiles
     int num_tiles;     // batch * m_tiles * n_tiles
     // batched GEMM (independent problems of one shape, one launch): tile t belongs to problem

@@ -338,6 +338,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     using Cfg = PairCfg<BN, EW>;
     constexpr int STAGES = Cfg::kStages;
     constexpr int KS = Cfg::KS;
+    // Grouped launches with 8 epilogue warps: the two groups take alternate TILES (group g drains accumulator buffer
+    // g), so the fixed per-tile latencies of the epilogue chain (parameter loads, accumulator hand-over, row verdict
+    // round trips) of consecutive tiles overlap; elsewhere two groups split each tile's column chunks.
+    constexpr bool TILE_ALT = GROUPED && EW == 8;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by pointer arithmetic on the __shared__ array (not through an integer round trip),
     // so the compiler keeps the shared state space: staging-buffer accesses compile to STS/LDS, not to
@@ -360,6 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     // index into grp_params / grp_maps (each of those a single problem, batch coordinate 0)
     struct Unit {
         int tile, b, mt, nt, kh, kb0, steps;
+        int tw;  // columns per N tile (BN unless GROUPED: the problem's tile_w)
     };
     const int tiles_per_problem = p.m_tiles * p.n_tiles;
     auto unit_of = [&](int u) {
@@ -376,8 +381,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             x.mt = tl / q.n_tiles;
             x.nt = tl - x.mt * q.n_tiles;
             x.steps = (q.k_blocks + KS - 1) / KS;
+            x.tw = q.tile_w;
             return x;
         }
+        x.tw = BN;
         x.kh = (p.split == 2 && u < p.num_tiles) ? 1 : 0;
         x.tile = p.split == 2 && !x.kh ? u - p.num_tiles : u;
         x.b = x.tile / tiles_per_problem;
@@ -407,7 +414,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
         return &tmC;
     };
     auto bcoord = [&](const Unit& x) { return GROUPED ? 0 : x.b; };
-#ifdef ABFT_TRACE_TILES  // (debug: per-tile MMA / epilogue timestamps, 64 slots per CTA, first 16 tiles)
+#ifdef ABFT_TRACE_TILES  // (debug: per-tile timestamps, 8 per tile for the CTA's first 8 tiles: MMA start / end,
+    // epilogue loop top / accumulator ready / chunks done / accumulator released / row verdicts / published)
     unsigned long long* const tt = p.trace ? p.trace + 64ull * blockIdx.x : nullptr;
     unsigned long long* trace = nullptr;
 #else
@@ -422,7 +430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 2 * Cfg::kEpiWarps);  // epilogue warps x 2 CTAs
+            mbar_init(&tempty[a], TILE_ALT ? 2 * 4 : 2 * Cfg::kEpiWarps);  // draining epilogue warps x 2 CTAs
         }
         mbar_init(xbar, 1);
         fence_mbar_init();
@@ -465,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 tma_prefetch_l2_4d(map_a(x), 0, x.mt * kPairM + static_cast<int>(rank) * kBM, kb + role * (KS / Cfg::NA),
                                    bcoord(x));
             else
-                tma_prefetch_l2_4d(map_b(x), 0, x.nt * BN + static_cast<int>(rank) * (BN / 2),
+                tma_prefetch_l2_4d(map_b(x), 0, x.nt * x.tw + static_cast<int>(rank) * (x.tw / 2),
                                    kb + (role - Cfg::NA) * (KS / Cfg::NB), q.b_shared ? 0 : bcoord(x));
         }
     }
@@ -543,7 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                                          x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, bc, pol);
                     else
                         tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, mB, &full[s], 0,
-                                         x.nt * BN + static_cast<int>(rank) * (BN / 2), kb + grp * KB,
+                                         x.nt * x.tw + static_cast<int>(rank) * (x.tw / 2), kb + grp * KB,
                                          q.b_shared ? 0 : bc, pol);
                 }
             }
@@ -551,10 +559,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
     } else if (warp == 1) {
         // ---------------- MMA issuer: leader CTA, one thread, for the whole pair
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = idesc_u8s8(kPairM, BN);
             int it = 0, local = 0;
             for (int u = pair; u < num_units; u += npairs, ++local) {
-                const int steps = unit_of(u).steps;
+                const Unit xu = unit_of(u);
+                const int steps = xu.steps;
+                // the MMA's N is the tile width: the pair's B' slabs hold tw / 2 rows each that matter
+                const uint32_t idesc = idesc_u8s8(kPairM, GROUPED ? static_cast<uint32_t>(xu.tw) : BN);
                 const int acc = local & 1;
                 const uint32_t aph = (local >> 1) & 1;
 #ifdef ABFT_TRACE_STEADY  // (debug: steady-state tile 8: how long the MMA waits for its accumulator)
@@ -562,7 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
 #endif
                 mbar_wait(&tempty[acc], aph ^ 1);
 #ifdef ABFT_TRACE_TILES
-                if (tt && local < 16) tt[local] = globaltimer();
+                if (tt && local < 8) tt[8 * local] = globaltimer();
 #endif
 #ifdef ABFT_TRACE_STEADY
                 if (trace && local == 8) trace[12] = globaltimer();
@@ -595,7 +605,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 }
                 mma_commit_pair(&tfull[acc]);  // accumulator complete, both CTAs' epilogues may read
 #ifdef ABFT_TRACE_TILES
-                if (tt && local < 16) tt[16 + local] = globaltimer();
+                if (tt && local < 8) tt[8 * local + 1] = globaltimer();
 #endif
                 if (trace && local == 0) trace[3] = globaltimer();
             }
@@ -608,6 +618,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         int local = 0, chunk_ctr = 0;
         for (int u = pair; u < num_units; u += npairs, ++local) {
+            if (TILE_ALT && (local & 1) != eg) continue;  // the other group's tile
+#ifdef ABFT_TRACE_TILES
+            if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 2] = globaltimer();
+#endif
             const Unit x = unit_of(u);
             const int mt = x.mt, nt = x.nt;
             const GemmParams& pq = prm(x);  // this tile's problem (the launch's own fields unless GROUPED)
@@ -627,20 +641,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             if (CHECKED && x.kh == 0 && !p.gemv_helpers && !pq.cs_mma) {
                 const int t0 = static_cast<int>(static_cast<long long>(nt) * pq.k_blocks / pq.n_tiles);
                 const int t1 = static_cast<int>(static_cast<long long>(nt + 1) * pq.k_blocks / pq.n_tiles);
-                const int kb0 = t0 + (t1 - t0) * eg / Cfg::kEpiGroups;  // the groups split the tile's share
-                const int kb1 = t0 + (t1 - t0) * (eg + 1) / Cfg::kEpiGroups;
+                const int kb0 = TILE_ALT ? t0 : t0 + (t1 - t0) * eg / Cfg::kEpiGroups;  // the groups split the tile's share
+                const int kb1 = TILE_ALT ? t1 : t0 + (t1 - t0) * (eg + 1) / Cfg::kEpiGroups;
                 if (kb1 > kb0 && row < pm) cs_part = csum_share(pq, bb, row, kb0 * kBK, min(kb1 * kBK, pq.k));
             }
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
 #ifdef ABFT_TRACE_TILES
-            if (tt && local < 16 && threadIdx.x == 64) tt[32 + local] = globaltimer();
+            if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 3] = globaltimer();
 #endif
             if (trace && local == 0 && threadIdx.x == 64) trace[4] = globaltimer();
 #ifdef ABFT_TRACE_STEADY
             if (trace && local == 8 && threadIdx.x == 64) trace[9] = globaltimer();
 #endif
-            const int n0 = nt * BN;
+            const int tw = x.tw;
+            const int n0 = nt * tw;
             const uint32_t t_row = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             // split-K exchange slot of this CTA's half tile (BN*128 int32): [BN/32 chunks][8 column quads]
             // [128 rows][4], so a warp moves 512 contiguous bytes per 16-byte access, in global memory (the
@@ -700,19 +715,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 fault_here |= bb == pq.fault_b[f] && row == pq.fault_row[f] && pq.fault_col[f] < pn;
             int32_t* const cb = pq.c + bb * pq.c_bstride;  // this problem's C
             long long rsum = 0;
-#pragma unroll 1
-            for (int c = eg; c < BN / 32; c += Cfg::kEpiGroups) {
+            // columns whose int32 sum cannot overflow (|C'| <= 255 * 128 * k): the row sum of a chunk is then plain
+            // 32-bit adds (3-input IADD3) instead of a 64-bit tree
+            const int sum32 = pq.k <= 2056 ? 32 : pq.k <= 4112 ? 16 : 0;
+            // One 32-column chunk of this warp's rows, already in registers.
+            auto chunk = [&](const int c, uint32_t (&v)[32]) {
                 const int col0 = n0 + c * 32;
-                if (col0 >= pn) break;  // warp-uniform
-                uint32_t v[32];
-#ifdef ABFT_TRACE_CHUNKS
-                if (trace && local == 0 && threadIdx.x == 64 && c < 2) trace[12 + c] = globaltimer();
-#endif
-                tmem_ld_32x32b_x32(t_row + c * 32, v);
-                tmem_wait_ld();
-#ifdef ABFT_TRACE_CHUNKS
-                if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[14] = globaltimer();
-#endif
                 if (spart != nullptr) {
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4) {
@@ -760,7 +768,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 if (trace && local == 0 && threadIdx.x == 64 && c == 0) trace[9] = globaltimer();
 #endif
                 if constexpr (CHECKED) {
-                    if (col0 + 32 <= pn) {
+                    if (col0 + 32 <= pn && sum32 == 32) {
+                        int32_t t[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            t[j] = static_cast<int32_t>(v[4 * j]) + static_cast<int32_t>(v[4 * j + 1]) +
+                                   static_cast<int32_t>(v[4 * j + 2]) + static_cast<int32_t>(v[4 * j + 3]);
+                        rsum += ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+                    } else if (col0 + 32 <= pn && sum32 == 16) {
+                        int32_t t[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            t[j] = static_cast<int32_t>(v[4 * j]) + static_cast<int32_t>(v[4 * j + 1]) +
+                                   static_cast<int32_t>(v[4 * j + 2]) + static_cast<int32_t>(v[4 * j + 3]);
+                        rsum += static_cast<long long>((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+                    } else if (col0 + 32 <= pn) {
                         // pairwise tree: 5 dependent int64 adds instead of a 32-long carry chain (exact in
                         // any order: |sum| < 32 * 2^31)
                         long long t[16];
@@ -853,10 +875,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                         }
                     }
                 }
+            };
+            // Chunks c = eg, eg + groups, ...: the TMEM load of the next chunk is in flight while the current one is
+            // reduced, staged and stored (two register buffers; tcgen05.wait::ld waits for every load issued, so the
+            // next load is issued right after the wait that completes the current one).
+            {
+                constexpr int G = TILE_ALT ? 1 : Cfg::kEpiGroups;
+                uint32_t va[32], vb[32];
+                int c = TILE_ALT ? 0 : eg;
+                auto live = [&](int cc) { return cc * 32 < tw && n0 + cc * 32 < pn; };  // warp-uniform
+                if constexpr (Cfg::kThreads <= 256) {
+                    if (live(c)) tmem_ld_32x32b_x32(t_row + c * 32, va);
+#pragma unroll 1
+                    while (live(c)) {
+                        tmem_wait_ld_tie(va);
+                        if (live(c + G)) tmem_ld_32x32b_x32(t_row + (c + G) * 32, vb);
+                        chunk(c, va);
+                        c += G;
+                        if (!live(c)) break;
+                        tmem_wait_ld_tie(vb);
+                        if (live(c + G)) tmem_ld_32x32b_x32(t_row + (c + G) * 32, va);
+                        chunk(c, vb);
+                        c += G;
+                    }
+                } else {  // (384 threads: 168 registers per thread, one chunk buffer)
+#pragma unroll 1
+                    for (; live(c); c += G) {
+                        tmem_ld_32x32b_x32(t_row + c * 32, va);
+                        tmem_wait_ld();
+                        chunk(c, va);
+                    }
+                }
             }
+#ifdef ABFT_TRACE_TILES
+            if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 4] = globaltimer();
+#endif
             if constexpr (CHECKED) {
                 // C'[row][n] = A*cs computed by the tensor cores (B' column n) when this tile covers column n
-                if (pq.cs_mma && eg == 0 && n0 <= pn && pn < n0 + BN) {
+                if (pq.cs_mma && (TILE_ALT || eg == 0) && n0 <= pn && pn < n0 + tw) {
                     cs_part = tmem_ld_32x32b_x1(t_row + static_cast<uint32_t>(pn - n0));
                     tmem_wait_ld();
                 }
@@ -876,6 +932,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 else
                     mbar_arrive_cluster(tempty_leader + static_cast<uint32_t>(acc * 8));
             }
+#ifdef ABFT_TRACE_TILES
+            if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 5] = globaltimer();
+#endif
             if constexpr (CHECKED) {
                 // mod is a ring homomorphism: the residue of the int64 row sum equals the sum of the
                 // per-tile residues mod 127 (P:src/gemm_abft.cpp:119-122 reduces the row sum once).
@@ -890,10 +949,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                                    (1ull << kRowAccCountShift) | static_cast<unsigned long long>(mod127(rsum)),
                                fin, flag);
                 if (trace && local == 0 && threadIdx.x == 64) trace[8] = globaltimer();
+#ifdef ABFT_TRACE_TILES
+                if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 6] = globaltimer();
+#endif
                 warp_publish(pq, bb, fin, flag);
             }
 #ifdef ABFT_TRACE_TILES
-            if (tt && local < 16 && threadIdx.x == 64) tt[48 + local] = globaltimer();
+            if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 7] = globaltimer();
 #endif
         }
         if constexpr (EPI == kEpiTmaStore) {
@@ -1013,22 +1075,23 @@ cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs,
 // Heterogeneous grouped launch (GemmParams::group_n problems; tensor maps in p.grp_maps): TMA-store or direct
 // epilogue, 4 epilogue warps.
 template <int BN, bool CHECKED>
-static cudaError_t launch_grouped_bn(int epi, int pairs, const GemmParams& p, cudaStream_t st) {
+static cudaError_t launch_grouped_bn(int epi, int ew, int pairs, const GemmParams& p, cudaStream_t st) {
     CUtensorMap none;
     std::memset(&none, 0, sizeof(none));
+    if (epi == kEpiTmaStore && ew == 8) return launch_one<BN, CHECKED, kEpiTmaStore, 8, true>(pairs, none, none, none, p, st);
     if (epi == kEpiTmaStore) return launch_one<BN, CHECKED, kEpiTmaStore, 4, true>(pairs, none, none, none, p, st);
     if (epi == kEpiStg) return launch_one<BN, CHECKED, kEpiStg, 4, true>(pairs, none, none, none, p, st);
     return launch_one<BN, CHECKED, kEpiDirect, 4, true>(pairs, none, none, none, p, st);
 }
-cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int pairs, const GemmParams& p, cudaStream_t st) {
+cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int ew, int pairs, const GemmParams& p, cudaStream_t st) {
     if (checked) {
-        if (bn == 256) return launch_grouped_bn<256, true>(epi, pairs, p, st);
-        if (bn == 128) return launch_grouped_bn<128, true>(epi, pairs, p, st);
-        return launch_grouped_bn<64, true>(epi, pairs, p, st);
+        if (bn == 256) return launch_grouped_bn<256, true>(epi, ew, pairs, p, st);
+        if (bn == 128) return launch_grouped_bn<128, true>(epi, ew, pairs, p, st);
+        return launch_grouped_bn<64, true>(epi, ew, pairs, p, st);
     }
-    if (bn == 256) return launch_grouped_bn<256, false>(epi, pairs, p, st);
-    if (bn == 128) return launch_grouped_bn<128, false>(epi, pairs, p, st);
-    return launch_grouped_bn<64, false>(epi, pairs, p, st);
+    if (bn == 256) return launch_grouped_bn<256, false>(epi, ew, pairs, p, st);
+    if (bn == 128) return launch_grouped_bn<128, false>(epi, ew, pairs, p, st);
+    return launch_grouped_bn<64, false>(epi, ew, pairs, p, st);
 }
 
 int gemm_ks(int bn) { return bn == 256 ? PairCfg<256>::KS : bn == 128 ? PairCfg<128>::KS : PairCfg<64>::KS; }

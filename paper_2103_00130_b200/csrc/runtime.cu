@@ -587,6 +587,12 @@ GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
         const int f = std::atoi(e);
         if (f == kEpiDirect || (tma_c && (f == kEpiTmaStore || f == kEpiStg))) g->epi = f;
     }
+    // 8 epilogue warps taking alternate tiles (TMA-store epilogue only); ABFTLP_GEMM_GROUP_EW=4|8 overrides
+    g->ew = g->epi == kEpiTmaStore ? 8 : 4;
+    if (const char* e = std::getenv("ABFTLP_GEMM_GROUP_EW")) {
+        const int f = std::atoi(e);
+        if (f == 4 || (f == 8 && g->epi == kEpiTmaStore)) g->ew = f;
+    }
     // longest mainloops first (the persistent pairs take tiles round-robin, so the long tiles start early)
     g->order.resize(n);
     for (int i = 0; i < n; ++i) g->order[i] = i;
@@ -618,7 +624,11 @@ GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
             P.k = static_cast<int>(w.k);
             P.k_blocks = static_cast<int>(kb);
             P.m_tiles = static_cast<int>((q.m + kPairM - 1) / kPairM);
-            P.n_tiles = static_cast<int>((w.n + (checked ? 1 : 0) + best_bn - 1) / best_bn);
+            // N tiles of equal width (a multiple of 32 up to the kernel's BN): n + 1 columns just over BN split into
+            // two balanced tiles instead of a full one plus a tile for the checksum column alone
+            const int64_t cols = w.n + (checked ? 1 : 0);
+            P.n_tiles = static_cast<int>((cols + best_bn - 1) / best_bn);
+            P.tile_w = static_cast<int>(((cols + P.n_tiles - 1) / P.n_tiles + 31) / 32 * 32);
             P.num_tiles = P.m_tiles * P.n_tiles;
             P.batch = 1;
             P.b_shared = 1;
@@ -694,7 +704,7 @@ GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
 }
 
 void gemm_group_run(const GemmGroup& g, cudaStream_t st) {
-    cuda_check(launch_gemm_grouped(g.bn, g.checked, g.epi, g.pairs, g.launch, st), "gemm_pair_kernel (grouped)");
+    cuda_check(launch_gemm_grouped(g.bn, g.checked, g.epi, g.ew, g.pairs, g.launch, st), "gemm_pair_kernel (grouped)");
 }
 
 void gemm_group_free(GemmGroup* g) {

@@ -76,7 +76,7 @@ struct GemmProblem {
     uint32_t* err_count = nullptr;
 };
 struct GemmGroup {
-    int n = 0, bn = 64, epi = kEpiTmaStore, pairs = 1;
+    int n = 0, bn = 64, epi = kEpiTmaStore, ew = 4, pairs = 1;
     bool checked = true;
     std::vector<int> order;        // problem launched at group slot s
     GemmParams launch{};           // launch-wide fields: tile table and device pointers
@@ -170,7 +170,7 @@ void l2_flush(void* d_buf, int64_t bytes, int salt, cudaStream_t st);
 // ---- launchers implemented in the .cu files
 cudaError_t launch_gemm_kernel(int bn, bool checked, int epi, int ew, int pairs, const CUtensorMap& a, const CUtensorMap& b,
                                const CUtensorMap& c, const GemmParams& p, cudaStream_t st);
-cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int pairs, const GemmParams& p, cudaStream_t st);
+cudaError_t launch_gemm_grouped(int bn, bool checked, int epi, int ew, int pairs, const GemmParams& p, cudaStream_t st);
 cudaError_t launch_locate_colsum_a(const uint8_t* a, int64_t m, int64_t k, int64_t lda, uint32_t* out, int64_t k_pad,
                                    cudaStream_t st);
 cudaError_t launch_locate_columns(const uint32_t* colsum_a, const GemmWeight& w, const int32_t* c, int64_t m, int64_t ldc,

@@ -40,9 +40,10 @@ L.lib.abftlp_debug_gemm_trace(None)
 t = tr.cpu().numpy().reshape(148, 64).astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, (t - t0) / 1000.0, np.nan)
+names = "mma0 mma1 top ready chunks release verdict publish".split()
 for cta in (0, 2, 70, 146):
-    print(f"CTA {cta}:")
-    for i in range(16):
-        if not np.isnan(t[cta, i]) or not np.isnan(t[cta, 32 + i]):
-            print(f"   tile {i:2d}: mma {t[cta, i]:7.2f} -> {t[cta, 16 + i]:7.2f}   epi {t[cta, 32 + i]:7.2f} -> {t[cta, 48 + i]:7.2f}")
-print("last epilogue end (all CTAs): max %.2f us" % np.nanmax(t[:, 48:64]))
+    print(f"CTA {cta}:   " + " ".join(f"{n:>8s}" for n in names))
+    for i in range(8):
+        if not np.isnan(t[cta, 8 * i]) or not np.isnan(t[cta, 8 * i + 3]):
+            print(f"   tile {i:2d}: " + " ".join(f"{t[cta, 8 * i + j]:8.2f}" for j in range(8)))
+print("last epilogue end (all CTAs): max %.2f us" % np.nanmax(t[:, 7::8]))
