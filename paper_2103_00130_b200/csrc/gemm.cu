@@ -73,55 +73,108 @@ __global__ void __launch_bounds__(256) encode_weight_kernel(const int8_t* __rest
     }
 }
 
-// 2-D encoder (the one above walks every column of a 64-row slab in one block: 64 blocks for k = 4096, ~150 GB/s):
-// one block per 64 x 64 tile of B -- coalesced 16-byte loads, a shared-memory transpose into B'[kb][j][p % 128]
-// (16-byte stores), and each row's partial sum over the tile's 64 columns reduced mod 127 and added to cs_acc[p]
-// (the residue of a sum is the sum of the residues: P:src/gemm_abft.cpp:60-71 reduces the int64 row sum once).
-// encode_finalize_kernel then writes cs (and B' column n) and re-zeroes cs_acc.
+// 2-D encoder (the one above walks every column of a 64-row slab in one block: 64 blocks for k = 4096, ~150 GB/s).
+// One block per (k-block, 128-column) tile of B: its slab of B' -- bt[kb][j0 .. j0 + 127][0 .. 127] -- is one
+// contiguous 16 KB run.
+//   load       128 rows x 128 bytes as 16-byte pieces (8 consecutive threads per row segment, 4 pieces per thread in
+//              flight), into shared memory with the 16-byte chunk index XOR-swizzled by the row's 16-row group, so
+//              the transposing reads below are bank-conflict free;
+//   row sums   dp4a over each piece, reduced over the row's 8 threads, residue mod 127 added to cs_acc[p] together
+//              with one arrival (the residue of a sum is the sum of the residues: P:src/gemm_abft.cpp:60-71 reduces
+//              the int64 row sum once). Atomics on one address are totally ordered, so the thread that brings the
+//              last column tile's arrival holds the row's complete residue: it writes cs[p] and B' column n and
+//              re-zeroes the scratch word -- no second kernel, no fence;
+//   transpose  a thread owns 16 rows x 4 columns: 16 word reads, 4 x (4x4 byte transposes by PRMT), four 16-byte
+//              stores (8 threads cover one column's 128 contiguous bytes).
+// Column n (the checksum column's slot) is written by the rows' finalizing threads only; the tile that contains it
+// zero-fills its rows past k.
+constexpr int kEncCountShift = 20;  // cs_acc word: arrivals << 20 | residue sum (tiles <= 2047, residues < 127 each)
+__device__ __forceinline__ void transpose4x4(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    // rows a, b, c, d of a 4x4 byte matrix (byte i of a = a[i]) -> columns
+    const uint32_t ab_lo = __byte_perm(a, b, 0x5140);  // a0 b0 a1 b1
+    const uint32_t ab_hi = __byte_perm(a, b, 0x7362);  // a2 b2 a3 b3
+    const uint32_t cd_lo = __byte_perm(c, d, 0x5140);  // c0 d0 c1 d1
+    const uint32_t cd_hi = __byte_perm(c, d, 0x7362);  // c2 d2 c3 d3
+    a = __byte_perm(ab_lo, cd_lo, 0x5410);             // a0 b0 c0 d0
+    b = __byte_perm(ab_lo, cd_lo, 0x7632);             // a1 b1 c1 d1
+    c = __byte_perm(ab_hi, cd_hi, 0x5410);             // a2 b2 c2 d2
+    d = __byte_perm(ab_hi, cd_hi, 0x7632);             // a3 b3 c3 d3
+}
 __global__ void __launch_bounds__(256) encode_tiles_kernel(const int8_t* __restrict__ b, int64_t k, int64_t n,
                                                            int64_t ldb, int8_t* __restrict__ bt, int64_t n_pad,
-                                                           int32_t* __restrict__ cs_acc) {
-    __shared__ __align__(16) int8_t tile[64][64 + 16];
+                                                           int32_t* __restrict__ cs_acc, int8_t* __restrict__ cs,
+                                                           int col_tiles) {
+    __shared__ __align__(16) uint4 tile[128][8];  // [row][swizzled 16-byte chunk]
     const int tid = threadIdx.x;
-    const int64_t p0 = static_cast<int64_t>(blockIdx.y) * 64, j0 = static_cast<int64_t>(blockIdx.x) * 64;
-    {
-        const int r = tid >> 2, q = tid & 3;  // row r, 16-byte segment q
-        const int64_t p = p0 + r, j = j0 + 16 * q;
-        alignas(16) int8_t v[16];
+    const int64_t kb = blockIdx.y, p0 = kb * kBK, j0 = static_cast<int64_t>(blockIdx.x) * 128;
+    const bool fast = (ldb % 16) == 0 && (reinterpret_cast<uintptr_t>(b) % 16) == 0;
+    // ---- load + row sums: piece = tid + 256 i -> row piece / 8, chunk piece % 8
+    uint4 v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int r = (tid >> 3) + 32 * i, c = tid & 7;
+        const int64_t p = p0 + r, j = j0 + 16 * c;
         const int8_t* src = b + p * ldb + j;
-        if (p < k && j + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
+        if (p < k && j + 16 <= n && fast) {
+            v[i] = __ldg(reinterpret_cast<const uint4*>(src));
         } else {
+            alignas(16) int8_t tmp[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = (p < k && j + e < n) ? src[e] : static_cast<int8_t>(0);
+            for (int e = 0; e < 16; ++e) tmp[e] = (p < k && j + e < n) ? src[e] : static_cast<int8_t>(0);
+            v[i] = *reinterpret_cast<const uint4*>(tmp);
         }
-        *reinterpret_cast<uint4*>(&tile[r][16 * q]) = *reinterpret_cast<const uint4*>(v);
-        int s = 0;
+    }
 #pragma unroll
-        for (int e = 0; e < 16; ++e) s += v[e];
+    for (int i = 0; i < 4; ++i) {
+        const int r = (tid >> 3) + 32 * i, c = tid & 7;
+        tile[r][c ^ ((r >> 4) & 7)] = v[i];
+        int s = __dp4a(static_cast<int>(v[i].x), 0x01010101, 0);
+        s = __dp4a(static_cast<int>(v[i].y), 0x01010101, s);
+        s = __dp4a(static_cast<int>(v[i].z), 0x01010101, s);
+        s = __dp4a(static_cast<int>(v[i].w), 0x01010101, s);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (q == 0 && p < k && j0 < n) atomicAdd(&cs_acc[p], mod127(s));
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        const int64_t p = p0 + r;
+        if (c == 0 && p < k && j0 < n) {
+            const int add = (1 << kEncCountShift) | mod127(s);
+            const int tot = atomicAdd(&cs_acc[p], add) + add;
+            if ((tot >> kEncCountShift) == col_tiles) {  // the row is complete
+                const int8_t cv = static_cast<int8_t>((tot & ((1 << kEncCountShift) - 1)) % 127);
+                cs[p] = cv;
+                bt[kb * n_pad * kBK + n * kBK + r] = cv;  // checksum column as B' column n
+                cs_acc[p] = 0;
+            }
+        }
     }
     __syncthreads();
-    {
-        const int c = tid >> 2, q = tid & 3;  // column c, rows [16 q, 16 q + 16)
-        alignas(16) int8_t v[16];
+    // ---- transpose: rows [16 q, 16 q + 16) x columns [4 g, 4 g + 4)
+    const int q = tid & 7, g = tid >> 3;
+    uint32_t w[4][4];  // w[h][e]: row 16 q + 4 h + e, columns 4 g .. 4 g + 3
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = tile[16 * q + e][c];
-        int8_t* dst = bt + (p0 / kBK) * n_pad * kBK + (j0 + c) * kBK + (p0 % kBK) + 16 * q;
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
-    }
-}
-
-__global__ void encode_finalize_kernel(int32_t* __restrict__ cs_acc, int8_t* __restrict__ cs, int8_t* __restrict__ bt,
-                                       int64_t k, int64_t k_pad, int64_t n, int64_t n_pad) {
-    for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < k_pad;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int8_t v = p < k ? static_cast<int8_t>(cs_acc[p] % 127) : static_cast<int8_t>(0);
-        cs[p] = v;
-        if (n < n_pad) bt[(p / kBK) * n_pad * kBK + n * kBK + (p % kBK)] = v;  // checksum column as B' column n
-        cs_acc[p] = 0;
+    for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int r = 16 * q + 4 * h + e;
+            w[h][e] = reinterpret_cast<const uint32_t*>(&tile[r][(g >> 2) ^ q])[g & 3];
+        }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) transpose4x4(w[h][0], w[h][1], w[h][2], w[h][3]);  // w[h][c]: column 4 g + c, rows 16 q + 4 h ..
+    int8_t* const slab = bt + kb * n_pad * kBK + j0 * kBK + 16 * q;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int64_t j = j0 + 4 * g + c;
+        int8_t* dst = slab + (4 * g + c) * kBK;
+        if (j == n) {  // the checksum column's slot: only the padding rows past k are ours
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                if (p0 + 16 * q + e >= k) {
+                    dst[e] = 0;
+                    cs[p0 + 16 * q + e] = 0;
+                }
+            continue;
+        }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0][c], w[1][c], w[2][c], w[3][c]);
     }
 }
 
@@ -294,7 +347,8 @@ struct PairCfg {
 #define ABFT_STAGING_BUFS 2
 #endif
     static constexpr int KS = BN == 64 ? ABFT_KS64 : BN == 128 ? ABFT_KS128 : ABFT_KS256;
-    static constexpr int kStagingBufs = ABFT_STAGING_BUFS;  // per epilogue warp
+    // per epilogue warp; one with 8 epilogue warps (a pipeline stage more: measured 44.5 -> 43.0 us on the D5 MLP share)
+    static constexpr int kStagingBufs = EW == 8 ? 1 : ABFT_STAGING_BUFS;
 #ifndef ABFT_NA64
 #define ABFT_NA64 2
 #endif
@@ -1121,12 +1175,11 @@ cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t 
         encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs);
         return cudaGetLastError();
     }
-    const dim3 grid(static_cast<unsigned>(w.n_pad / 64), static_cast<unsigned>(w.k_pad / 64));
-    encode_tiles_kernel<<<grid, 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs_acc);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    encode_finalize_kernel<<<static_cast<unsigned>((w.k_pad + 255) / 256), 256, 0, st>>>(w.cs_acc, w.cs, w.bt, k,
-                                                                                         w.k_pad, n, w.n_pad);
+    // (a weight wider than 2047 column tiles -- n > 262 016 -- would overflow the arrival field)
+    const int64_t col_tiles = (n + 127) / 128;
+    if (col_tiles >= (1 << (31 - kEncCountShift))) return cudaErrorInvalidValue;
+    const dim3 grid(static_cast<unsigned>(w.n_pad / 128), static_cast<unsigned>(w.k_pad / kBK));
+    encode_tiles_kernel<<<grid, 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs_acc, w.cs, static_cast<int>(col_tiles));
     return cudaGetLastError();
 }
 
