@@ -96,6 +96,14 @@ class PackedEncodedWeight:
         _lib.call("abftlp_gemm_weight_checksums", self._h, ptr(out), stream_handle())
         return WeightChecksum(out)
 
+    def reencode(self, b, stream=None) -> None:
+        """Encode a new B of the same shape into this handle, in place (abftlp_gemm_reencode; no allocation)."""
+        bt = to_device(b, torch.int8)
+        if tuple(int(s) for s in bt.shape) != (self._k, self._n):
+            raise _lib.InvalidArgument(_lib.ERR_INVALID_ARGUMENT, "PackedEncodedWeight.reencode: shape mismatch")
+        _lib.call("abftlp_gemm_reencode", self._h, ptr(bt), max(self._n, 1), stream_handle(stream))
+        self._view = None
+
     def encoded(self) -> torch.Tensor:
         """Logical k x (n+1) matrix [B | cs]."""
         out = torch.empty((self._k, self._n + 1), dtype=torch.int8, device=device())

@@ -31,3 +31,14 @@ if [ -n "$MLP_G" ]; then
       python scripts/mlp_group_prof.py $MLP_G > gpurun_out/r02/prof_mlp_g$MLP_G.log 2>&1
   export_rep ncu_mlp_group_g$MLP_G
 fi
+if [ -n "$EXTRA" ]; then
+  # the grouped D5 lookups (8 tables in one launch) and the one-kernel encoder
+  python scripts/prof_d5_group.py 3 > gpurun_out/r02/prof_d5_group.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:eb_bag -s 2 -c 1 -o /tmp/ncu_eb_D5_grouped \
+      python scripts/prof_d5_group.py 3 >> gpurun_out/r02/prof_d5_group.log 2>&1
+  export_rep ncu_eb_D5_grouped
+  python scripts/encoder_probe.py > gpurun_out/r02/encoder_probe_r02.txt 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:encode_tiles -s 4 -c 1 -o /tmp/ncu_encoder \
+      python scripts/encoder_probe.py >> gpurun_out/r02/encoder_probe_ncu.log 2>&1
+  export_rep ncu_encoder
+fi

@@ -76,6 +76,36 @@ def test_pack_round_trip(G):  # P:tests/test_gemm_abft.cpp:60-77 (at() contract)
         assert np.array_equal(enc[:, n], O.row_checksums(b))
 
 
+def test_encoder_tile_edges_and_reencode(G):
+    """The one-kernel encoder (128 x 128 tiles, residues and arrivals in one atomic word): the checksum column's slot at
+    a tile boundary (n % 128 == 0), padding rows inside the last k-block, the aligned 16-byte load path, and a second
+    encode into the same handle (the scratch words reset themselves)."""
+    rng = np.random.default_rng(21)
+    for k, n in [(100, 128), (128, 256), (129, 128), (384, 512), (512, 384), (1000, 1024), (257, 2000)]:
+        b = rng.integers(-128, 128, (k, n)).astype(np.int8)
+        pb = G.PackedEncodedWeight(b)
+        for _ in range(2):
+            enc = pb.encoded().cpu().numpy()
+            assert np.array_equal(enc[:, :n], b)
+            assert np.array_equal(enc[:, n], O.row_checksums(b))
+            pb.reencode(b)
+    # extreme rows: every partial residue at its maximum
+    b = np.full((256, 640), -128, np.int8)
+    b[::2] = 127
+    enc = G.PackedEncodedWeight(b).encoded().cpu().numpy()
+    assert np.array_equal(enc[:, 640], O.row_checksums(b))
+
+
+@pytest.mark.parametrize("k", [2056, 2057, 4112, 4113])
+def test_row_sum_extremes_at_the_int32_bounds(G, k):
+    """The epilogue sums a chunk's 32 (k <= 2056) or 16 (k <= 4112) columns in 32 bits: with every product at its
+    extreme (A = 255, B = -128 or 127) those sums sit just inside int32; one k further the 64-bit path takes over."""
+    for bv in (-128, 127):
+        a = np.full((40, k), 255, np.uint8)
+        b = np.full((k, 96), bv, np.int8)
+        assert check_against_oracle(G, a, b).errCount == 0
+
+
 def test_random_small_products_bit_exact(G):  # P:tests/test_gemm_abft.cpp:134-157 / acceptance 5
     rng = np.random.default_rng(14)
     for _ in range(120):

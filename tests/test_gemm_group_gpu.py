@@ -19,11 +19,15 @@ def _inputs(seed, m, k, n):
     return rng.integers(0, 256, (m, k)).astype(np.uint8), rng.integers(-128, 128, (k, n)).astype(np.int8)
 
 
+@pytest.mark.parametrize("ew", [None, "4"])
 @pytest.mark.parametrize("bn", [None, "64", "128", "256"])
-def test_group_matches_oracle(bn, monkeypatch):
+def test_group_matches_oracle(bn, ew, monkeypatch):
+    """(default: 8 epilogue warps taking alternate tiles; ABFTLP_GEMM_GROUP_EW=4: one group, pipelined TMEM loads)"""
     from paper_2103_00130_b200 import gemm as G
     if bn:
         monkeypatch.setenv("ABFTLP_GEMM_GROUP_BN", bn)
+    if ew:
+        monkeypatch.setenv("ABFTLP_GEMM_GROUP_EW", ew)
     ins = [_inputs(17 * i + 3, m, k, n) for i, (m, k, n) in enumerate(SHAPES)]
     grp = G.AbftGemmGroup([(a, G.PackedEncodedWeight(b)) for a, b in ins])
     for _ in range(3):
