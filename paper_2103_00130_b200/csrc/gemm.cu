@@ -588,6 +588,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 // spreads those reads over all of A's L2 lines instead of hammering one k-block's lines
                 // (integer accumulation is exact, so the K order does not change the result).
                 const int rot = x.nt % x.steps;
+                // GROUPED: the problem's B' map boxes exactly the tw / 2 rows of this CTA's half tile (k-blocks land
+                // tw / 2 * 128 bytes apart), so narrow tiles do not pull a full BN / 2-row slab through L2
+                const uint32_t b_kstride = GROUPED ? static_cast<uint32_t>(x.tw / 2) * kBK : Cfg::kBBytes;
+                const uint32_t tx_bytes = (GROUPED && !is_a) ? KB * b_kstride : bytes;
                 for (int ks0 = 0; ks0 < x.steps; ++ks0, ++it) {
                     const int ks = ks0 + rot < x.steps ? ks0 + rot : ks0 + rot - x.steps;
                     const int kb = x.kb0 + ks * KS;
@@ -595,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * Cfg::kStageBytes;
-                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * tx_bytes);
                     if (is_a && q.a_exact) {
 #pragma unroll
                         for (int qq = 0; qq < KA; ++qq)  // exact-extent view: one k-block per request
@@ -605,7 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                         tma_load_4d_pair(st + grp * KA * Cfg::kABytes, mA, &full[s], 0,
                                          x.mt * kPairM + static_cast<int>(rank) * kBM, kb + grp * KA, bc, pol);
                     else
-                        tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * Cfg::kBBytes, mB, &full[s], 0,
+                        tma_load_4d_pair(st + KS * Cfg::kABytes + grp * KB * b_kstride, mB, &full[s], 0,
                                          x.nt * x.tw + static_cast<int>(rank) * (x.tw / 2), kb + grp * KB,
                                          q.b_shared ? 0 : bc, pol);
                 }
@@ -620,6 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 const int steps = xu.steps;
                 // the MMA's N is the tile width: the pair's B' slabs hold tw / 2 rows each that matter
                 const uint32_t idesc = idesc_u8s8(kPairM, GROUPED ? static_cast<uint32_t>(xu.tw) : BN);
+                const uint32_t b_kstride = GROUPED ? static_cast<uint32_t>(xu.tw / 2) * kBK : Cfg::kBBytes;
                 const int acc = local & 1;
                 const uint32_t aph = (local >> 1) & 1;
 #ifdef ABFT_TRACE_STEADY  // (debug: steady-state tile 8: how long the MMA waits for its accumulator)
@@ -648,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
 #pragma unroll
                     for (int j = 0; j < KS; ++j) {
                         const uint64_t da = umma_desc_sw128(a0 + j * Cfg::kABytes);
-                        const uint64_t db = umma_desc_sw128(b0 + j * Cfg::kBBytes);
+                        const uint64_t db = umma_desc_sw128(b0 + j * b_kstride);
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; ++kk) {  // UMMA K = 32 bytes for 8-bit operands
 #ifndef ABFT_NO_MMA  // (experiment switch: pure load pipeline)

@@ -548,23 +548,22 @@ GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
             throw std::invalid_argument("gemm_group: A needs a 16-byte aligned base and lda % 16 == 0");
         tma_c = tma_c && (q.ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(q.c) % 16) == 0;
     }
-    // Tile width: the cost model of choose_tiling summed over the problems (shared-memory-bound mainloop per
-    // k-block, TMEM drain per tile) plus the longest tile as the tail; every problem's checksum column rides in
-    // its last N tile on the tensor cores (B' column n exists at every n).
+    // Kernel tile width BN (each problem then takes balanced N tiles of tile_w <= BN columns, see below): these
+    // launches stream A and B' through L2 (measured: the L2 -> SM path, ~6.5 TB/s, is the binding unit of the D5 MLP
+    // layers), so the cost of a tile is the bytes it pulls -- its 256-row A slab plus the tile_w rows of B' -- per
+    // k-block, plus a fixed ~1 us of per-tile latency (in 128-byte units at one pair's share of that path).
     const int pairs_all = std::max(1, device_sm_count() / 2);
     int best_bn = 64;
     double best = 1e300;
     for (int bn : {256, 128, 64}) {
-        const double per_kb = std::max(2.0 * (kBM + bn / 2), 4.0 * (bn == 64 ? 46 : bn == 128 ? 64 : 128));
-        const double drain = double(kBM) * bn * 4 / 31.0 + 1500.0;
         double sum = 0.0, longest = 0.0;
         for (int i = 0; i < n; ++i) {
             const GemmProblem& q = probs[i];
-            // checksum column: always in the MMA (B' column n), adding a tile when the last one has no room --
-            // measured cheaper than the CUDA-core GEMV share on these short-K tiles (D5 share at G=8: 53 vs 58 us)
-            const int64_t nt = (q.w->n + (checked ? 1 : 0) + bn - 1) / bn;
+            const int64_t cols = q.w->n + (checked ? 1 : 0);
+            const int64_t nt = (cols + bn - 1) / bn;
+            const int64_t tw = ((cols + nt - 1) / nt + 31) / 32 * 32;
             const double tiles = double((q.m + kPairM - 1) / kPairM) * double(nt);
-            const double t = double(q.w->k_pad / kBK) * per_kb + drain;
+            const double t = double(q.w->k_pad / kBK) * double(kPairM + tw) + 700.0 + 100.0 * double(tw / 32);
             sum += tiles * t;
             longest = std::max(longest, t);
         }
@@ -659,7 +658,10 @@ GemmGroup* gemm_group_create(const GemmProblem* probs, int n, bool checked) {
                                                   static_cast<uint64_t>(q.lda), 1, 0)
                                   : make_map_kblocks(q.a, static_cast<uint64_t>(q.m), static_cast<uint64_t>(kb),
                                                      static_cast<uint64_t>(q.lda), kBK, kBM, gemm_box_a(best_bn), 1, 0);
-            hm[3 * s + 1] = w.map_b[bn_index(best_bn)];
+            // B' boxed at exactly the tw / 2 rows a CTA's half tile needs
+            hm[3 * s + 1] = make_map_kblocks(w.bt, static_cast<uint64_t>(w.n_pad), static_cast<uint64_t>(kb), kBK,
+                                             static_cast<uint64_t>(w.n_pad * kBK), static_cast<uint32_t>(P.tile_w / 2),
+                                             gemm_box_b(best_bn));
             if (g->epi == kEpiTmaStore)
                 hm[3 * s + 2] = make_map_c(q.c, static_cast<uint64_t>(w.n), static_cast<uint64_t>(q.m),
                                            static_cast<uint64_t>(q.ldc), 1, 0);
