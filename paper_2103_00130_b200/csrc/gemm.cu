@@ -439,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
             x.tw = q.tile_w;
             return x;
         }
-        x.tw = BN;
+        x.tw = p.tile_w;  // BN, or balanced narrower tiles (runtime: short-K problems whose n fills its tiles)
         x.kh = (p.split == 2 && u < p.num_tiles) ? 1 : 0;
         x.tile = p.split == 2 && !x.kh ? u - p.num_tiles : u;
         x.b = x.tile / tiles_per_problem;
@@ -623,7 +623,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 const Unit xu = unit_of(u);
                 const int steps = xu.steps;
                 // the MMA's N is the tile width: the pair's B' slabs hold tw / 2 rows each that matter
-                const uint32_t idesc = idesc_u8s8(kPairM, GROUPED ? static_cast<uint32_t>(xu.tw) : BN);
+                const uint32_t idesc = idesc_u8s8(kPairM, static_cast<uint32_t>(xu.tw));
                 const uint32_t b_kstride = GROUPED ? static_cast<uint32_t>(xu.tw / 2) * kBK : Cfg::kBBytes;
                 const int acc = local & 1;
                 const uint32_t aph = (local >> 1) & 1;

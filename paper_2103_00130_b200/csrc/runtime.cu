@@ -435,7 +435,20 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     bool cs_mma = checked && t.split == 1 && w.n % t.bn != 0;  // implies n < n_pad: B' column n exists
     if (const char* e = std::getenv("ABFTLP_CS_MMA"))
         cs_mma = checked && t.split == 1 && std::atoi(e) != 0 && w.n < w.n_pad && w.n / t.bn < (w.n_pad + t.bn - 1) / t.bn;
-    const int64_t n_tiles = cs_mma ? (w.n + 1 + t.bn - 1) / t.bn : n_tiles_plain;
+    int64_t n_tiles = cs_mma ? (w.n + 1 + t.bn - 1) / t.bn : n_tiles_plain;
+    // Optional (ABFTLP_GEMM_TILEW=1): when n fills its tiles exactly, split the n + 1 columns into balanced tiles of
+    // tile_w < BN columns (the MMA's N; one tile more, the checksum column on the tensor cores) instead of the
+    // CUDA-core checksum share. Measured slower on the short-K DLRM shapes (serving mode 17-29 % -> 38-50 % overhead;
+    // G1 20.7 -> 22.5 us), so it is off by default; grouped launches always use tile widths (runtime.cu, gemm_group).
+    int64_t tile_w = t.bn;
+    bool balance = false;
+    if (const char* e = std::getenv("ABFTLP_GEMM_TILEW"))
+        balance = checked && !cs_mma && t.split == 1 && w.n % t.bn == 0 && w.n < w.n_pad && std::atoi(e) != 0;
+    if (balance) {
+        cs_mma = true;
+        n_tiles = (w.n + 1 + t.bn - 1) / t.bn;
+        tile_w = ((w.n + 1 + n_tiles - 1) / n_tiles + 31) / 32 * 32;
+    }
     if (nb * m_tiles * n_tiles * t.split > (int64_t{1} << 31) - 1) throw std::invalid_argument("abft_gemm: too many tiles");
 
     if (checked && n_tiles > kMaxCheckedNTiles) throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
@@ -450,6 +463,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.k = static_cast<int>(w.k);
     p.k_blocks = static_cast<int>(kb);
     p.n_tiles = static_cast<int>(n_tiles);
+    p.tile_w = static_cast<int>(tile_w);
     p.m_tiles = static_cast<int>(m_tiles);
     p.num_tiles = static_cast<int>(nb * m_tiles * n_tiles);
     p.batch = static_cast<int>(nb);

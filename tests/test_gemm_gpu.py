@@ -106,6 +106,27 @@ def test_row_sum_extremes_at_the_int32_bounds(G, k):
         assert check_against_oracle(G, a, b).errCount == 0
 
 
+@pytest.mark.parametrize("m,n,k,tiling", [(64, 1024, 256, "256"), (32, 256, 256, "256"), (200, 512, 1024, "128"),
+                                            (300, 1024, 640, "64"), (64, 512, 512, None), (257, 768, 384, "256")])
+def test_balanced_tiles_when_n_fills_its_tiles(G, m, n, k, tiling, monkeypatch):
+    """n % BN == 0 at short K: the n + 1 columns split into balanced tiles narrower than BN (the MMA's N), the checksum
+    column on the tensor cores; forced on and off, with faults on both sides of the checksum column."""
+    a, b = rnd(3 * m + n + k, m, n, k)
+    if tiling:
+        monkeypatch.setenv("ABFTLP_GEMM_TILING", tiling)
+    for tw in ("1", "0"):
+        monkeypatch.setenv("ABFTLP_GEMM_TILEW", tw)
+        assert check_against_oracle(G, a, b).errCount == 0
+        pb = G.PackedEncodedWeight(b)
+        for fault in ((m - 1, n - 1, 30), (0, n, 3), (m // 2, n // 2, 0)):
+            res = G.abft_gemm(a, pb, fault=fault)
+            ct, _, _ = O.abft_gemm(a, b)
+            ct[fault[0], fault[1]] ^= np.int32(1 << fault[2])
+            err_ref, fl_ref = O.verify(ct)
+            assert np.array_equal(res.cTemp.data.cpu().numpy(), ct)
+            assert np.array_equal(res.rowFlags.cpu().numpy(), fl_ref) and res.errCount == err_ref == 1
+
+
 def test_random_small_products_bit_exact(G):  # P:tests/test_gemm_abft.cpp:134-157 / acceptance 5
     rng = np.random.default_rng(14)
     for _ in range(120):
