@@ -201,3 +201,29 @@ def test_benches_validate_and_report(F):  # P:tests/test_capi.cpp:86-96
     assert r["baseline_ns"] > 0 and r["abft_ns"] > 0 and np.isfinite(r["overhead_fraction"])
     r = F.bench_eb(500, 16, 20, 2, 5)
     assert r["baseline_ns"] > 0
+
+
+def test_device_splitmix_against_the_reference_draws():
+    """The device generator against the reference's own raw draws (tests/golden/rng.json, written from the reference
+    build): kind 3 (next_below) with bound 2^64 - 1 returns the raw 64-bit draw (P:src/rng.hpp:10-43); an offset into
+    the stream gives the same draws as generating from its start (counter-based)."""
+    import ctypes as C
+    import json
+
+    import torch
+
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200 import rng as R
+    cases = json.loads((GOLD / "rng.json").read_text())["cases"]
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for c in cases:
+        want = np.array([int(x) for x in c["draws"]], dtype=np.uint64)
+        out = torch.empty(len(want), dtype=torch.int64, device="cuda")
+        L.call("abftlp_generate", C.c_void_p(out.data_ptr()), len(want), c["seed"], c["stream"], 0, 3, 0.0, 0.0,
+               (1 << 64) - 1, st)
+        got = out.cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want), (c["seed"], c["stream"])
+        assert np.array_equal(R.draws(c["seed"], c["stream"], 0, len(want)), want)  # the host mirror too
+        tail = torch.empty(3, dtype=torch.int64, device="cuda")
+        L.call("abftlp_generate", C.c_void_p(tail.data_ptr()), 3, c["seed"], c["stream"], 5, 3, 0.0, 0.0, (1 << 64) - 1, st)
+        assert np.array_equal(tail.cpu().numpy().view(np.uint64), want[5:8])
