@@ -1177,13 +1177,13 @@ cudaError_t launch_set_checksums(GemmWeight& w, const int8_t* src, cudaStream_t 
 }
 
 cudaError_t launch_encode_weight(const int8_t* b, int64_t k, int64_t n, int64_t ldb, GemmWeight& w, cudaStream_t st) {
-    if (!w.cs_acc) {  // (handles without encoder scratch)
+    // column tiles of the tile encoder; beyond 2047 (n > 262 016) its 11-bit arrival field would overflow: such
+    // weights, and handles without encoder scratch, take the one-block-per-row-slab encoder
+    const int64_t col_tiles = (n + 127) / 128;
+    if (!w.cs_acc || col_tiles >= (1 << (31 - kEncCountShift))) {
         encode_weight_kernel<<<static_cast<unsigned>(w.k_pad / 64), 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs);
         return cudaGetLastError();
     }
-    // (a weight wider than 2047 column tiles -- n > 262 016 -- would overflow the arrival field)
-    const int64_t col_tiles = (n + 127) / 128;
-    if (col_tiles >= (1 << (31 - kEncCountShift))) return cudaErrorInvalidValue;
     const dim3 grid(static_cast<unsigned>(w.n_pad / 128), static_cast<unsigned>(w.k_pad / kBK));
     encode_tiles_kernel<<<grid, 256, 0, st>>>(b, k, n, ldb, w.bt, w.n_pad, w.cs_acc, w.cs, static_cast<int>(col_tiles));
     return cudaGetLastError();

@@ -96,6 +96,16 @@ def test_encoder_tile_edges_and_reencode(G):
     assert np.array_equal(enc[:, 640], O.row_checksums(b))
 
 
+def test_encoder_very_wide_weight_takes_the_slab_encoder(G):
+    """More than 2047 column tiles (n > 262 016) would overflow the tile encoder's arrival field: such weights are
+    encoded by the one-block-per-row-slab kernel; same [B | cs]."""
+    rng = np.random.default_rng(23)
+    k, n = 130, 262_200
+    b = rng.integers(-128, 128, (k, n)).astype(np.int8)
+    enc = G.PackedEncodedWeight(b).encoded().cpu().numpy()
+    assert np.array_equal(enc[:, :n], b) and np.array_equal(enc[:, n], O.row_checksums(b))
+
+
 @pytest.mark.parametrize("k", [2056, 2057, 4112, 4113])
 def test_row_sum_extremes_at_the_int32_bounds(G, k):
     """The epilogue sums a chunk's 32 (k <= 2056) or 16 (k <= 4112) columns in 32 bits: with every product at its
