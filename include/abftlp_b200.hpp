@@ -160,7 +160,7 @@ public:
     PackedEncodedWeight& operator=(const PackedEncodedWeight&) = delete;
     PackedEncodedWeight(PackedEncodedWeight&& o) noexcept
         : k_(o.k_), n_(o.n_), layout_(o.layout_), scale_(o.scale_), bias_(o.bias_), w_(o.w_),
-          logical_(std::move(o.logical_)) {
+          logical_(std::move(o.logical_)), blocked_(std::move(o.blocked_)) {
         o.w_ = nullptr;
     }
     ~PackedEncodedWeight() { abftlp_gemm_weight_free(w_); }
@@ -181,6 +181,21 @@ public:
         }
         return logical_[i * (n_ + 1) + j];
     }
+    // Host view of [B | cs] in the caller's BlockLayout -- the reference's buffer format (P:src/gemm_abft.hpp:46-48):
+    // blocks in row-major order over (row block, column block), rowBlock x colBlock cells each, row-major inside a
+    // block, zero padding. Built on first use from the device copy; the device layout itself is fixed.
+    std::size_t rowBlocks() const { return (k_ + layout_.rowBlock - 1) / layout_.rowBlock; }
+    std::size_t colBlocks() const { return (n_ + 1 + layout_.colBlock - 1) / layout_.colBlock; }
+    const std::vector<std::int8_t>& buffer() const {
+        if (blocked_.empty()) {
+            const std::size_t rb = layout_.rowBlock, cb = layout_.colBlock, cbs = colBlocks();
+            blocked_.assign(rowBlocks() * cbs * rb * cb, 0);
+            for (std::size_t i = 0; i < k_; ++i)
+                for (std::size_t j = 0; j <= n_; ++j)
+                    blocked_[((i / rb) * cbs + j / cb) * rb * cb + (i % rb) * cb + j % cb] = at(i, j);
+        }
+        return blocked_;
+    }
     const abftlp_gemm_weight* handle() const { return w_; }
     abftlp_gemm_weight* handle() { return w_; }
 
@@ -190,6 +205,7 @@ private:
     double scale_ = 1.0, bias_ = 0.0;
     abftlp_gemm_weight* w_ = nullptr;
     mutable std::vector<std::int8_t> logical_;
+    mutable std::vector<std::int8_t> blocked_;
 };
 
 struct AbftGemmResult {

@@ -11,7 +11,8 @@ import pytest
 
 REPO = Path(__file__).resolve().parents[1]
 REF_DIR = REPO / "oracle" / "_ref"
-BINS = {"test_capi": REF_DIR / "test_capi_b200", "acceptance": REF_DIR / "acceptance_b200"}
+BINS = {"test_capi": REF_DIR / "test_capi_b200", "acceptance": REF_DIR / "acceptance_b200",
+        "test_gemm_abft": REF_DIR / "test_gemm_abft_b200", "test_embedding_abft": REF_DIR / "test_embedding_abft_b200"}
 
 
 def _ensure_built():
@@ -33,6 +34,19 @@ def test_suites_built_against_b200_library():
 def test_reference_test_capi_passes_on_b200():
     _ensure_built()
     r = subprocess.run([str(BINS["test_capi"])], capture_output=True, text=True, timeout=600, cwd="/tmp")
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "| 0 failed |" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["test_gemm_abft", "test_embedding_abft"])
+def test_reference_operator_unit_suites_pass_on_b200(suite):
+    """P:tests/test_gemm_abft.cpp (mod127 / checksum known answers, pack round trips over block layouts, 1000 random
+    clean products, the aliasing sweep, the dual-encoded oracle) and P:tests/test_embedding_abft.cpp (row sums, exact
+    integer path, weighted bags, the one-flagged-bag batch, ABEB file round trip), compiled unchanged."""
+    _ensure_built()
+    r = subprocess.run([str(BINS[suite])], capture_output=True, text=True, timeout=900, cwd="/tmp")
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout + r.stderr
     assert "| 0 failed |" in r.stdout
