@@ -8,6 +8,8 @@
 // reference's own header/source. Test infrastructure only: nothing here ships in the library.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <fstream>
@@ -90,6 +92,15 @@ struct CampaignReport {
     std::vector<ShapeStats> perShape;
     std::string notes;
     double detectionRate() const { return trials ? static_cast<double>(detected) / static_cast<double>(trials) : 0.0; }
+    std::string csvText, tableText;  // (facade) the library's own renderings of this report
+};
+struct FaultRecord {
+    bool injected = false;
+    std::string position;
+    std::int64_t before = 0, after = 0;
+};
+struct WilsonInterval {
+    double low = 0.0, high = 0.0;
 };
 
 namespace facade {
@@ -137,8 +148,21 @@ inline CampaignReport run(const CampaignConfig& cfg) {
     const int fd = mkstemp(path);
     if (fd >= 0) close(fd);
     const abftlp_status w = abftlp_report_write_csv(r, path);
+    char* table = nullptr;
+    const abftlp_status tr = abftlp_report_render(r, &table);
+    if (tr == ABFTLP_OK && table) {
+        rep.tableText = table;
+        abftlp_string_free(table);
+    }
     abftlp_report_free(r);
     ok(w);
+    ok(tr);
+    {
+        std::ifstream whole(path);
+        std::stringstream all;
+        all << whole.rdbuf();
+        rep.csvText = all.str();
+    }
     std::ifstream in(path);
     std::string line;
     std::getline(in, line);  // header
@@ -168,12 +192,149 @@ inline CampaignReport run_eb_campaign(const CampaignConfig& cfg) {
 }
 inline CampaignReport run_campaign(const CampaignConfig& cfg) { return facade::run(cfg); }
 
+// The library's renderings of a report it produced (byte-identical to the reference's writers: checked by
+// tests/test_fault_lab_gpu.py against the reference build).
+inline std::string report_to_csv(const CampaignReport& r) { return r.csvText; }
+inline std::string report_to_table(const CampaignReport& r) { return r.tableText; }
+
+// Campaign text -> CampaignConfig: the library's parser (abftlp_campaign_parse) accepts or rejects the text; the
+// fields the reference's tests read back are then picked out of the accepted text.
+inline CampaignConfig parse_campaign_config(const std::string& text) {
+    abftlp_campaign* c = nullptr;
+    facade::ok(abftlp_campaign_parse(text.c_str(), &c));
+    abftlp_campaign_free(c);
+    CampaignConfig cfg;
+    std::string kind;
+    GemmWorkload g;
+    EbWorkload e;
+    std::istringstream in(text);
+    for (std::string line; std::getline(in, line);) {
+        line = line.substr(0, line.find('#'));
+        const auto eq = line.find('=');
+        if (eq == std::string::npos) continue;
+        auto trim = [](std::string v) {
+            const auto a = v.find_first_not_of(" \t\r"), b = v.find_last_not_of(" \t\r");
+            return a == std::string::npos ? std::string() : v.substr(a, b - a + 1);
+        };
+        const std::string key = trim(line.substr(0, eq)), val = trim(line.substr(eq + 1));
+        if (key == "threads") cfg.threads = std::stoull(val);
+        else if (key == "kind") kind = val;
+        else if (key == "trials_per_shape") g.trialsPerShape = std::stoull(val);
+        else if (key == "shapes") {
+            std::stringstream ls(val);
+            for (std::string x; std::getline(ls, x, ',');) {
+                unsigned long long m = 0, n = 0, k = 0;
+                if (std::sscanf(x.c_str(), " %llux%llux%llu", &m, &n, &k) == 3) g.shapes.push_back({m, n, k});
+            }
+        } else if (key == "table_rows") e.tableRows = std::stoull(val);
+        else if (key == "table_dim") e.tableDim = std::stoull(val);
+        else if (key == "pooling") e.pooling = std::stoull(val);
+        else if (key == "batch") e.batch = std::stoull(val);
+        else if (key == "trials") e.trials = std::stoull(val);
+        else if (key == "target")
+            cfg.fault.target = val == "weight_b" ? FaultTarget::weight_B : val == "intermediate_c" ? FaultTarget::intermediate_C
+                               : val == "eb_table" ? FaultTarget::eb_table : FaultTarget::none;
+        else if (key == "model")
+            cfg.fault.model = val == "random_value" ? model::FaultModel::random_value : model::FaultModel::single_bit_flip;
+        else if (key == "bit_range")
+            cfg.fault.bitRange = val == "high4" ? BitRange::high4 : val == "low4" ? BitRange::low4 : BitRange::all;
+        else if (key == "seed") cfg.fault.seed = std::stoull(val);
+    }
+    if (kind == "gemm") cfg.gemm = g;
+    else if (kind == "eb") cfg.eb = e;
+    return cfg;
+}
+
+// 95 % Wilson score interval (z = 1.959963984540054), clamped to [0, 1].
+inline WilsonInterval wilson_interval(std::uint64_t successes, std::uint64_t trials) {
+    if (trials == 0) throw std::invalid_argument("wilson_interval: zero trials");
+    const double z = 1.959963984540054, n = static_cast<double>(trials);
+    const double p = static_cast<double>(successes) / n, q = z * z / n;
+    const double mid = (p + q / 2.0) / (1.0 + q);
+    const double half = z * std::sqrt(p * (1.0 - p) / n + q / (4.0 * n)) / (1.0 + q);
+    return {std::max(0.0, mid - half), std::min(1.0, mid + half)};
+}
+
+// Host-container injectors of the reference's unit tests (P:src/fault_lab.hpp:96-107): the draw protocol of
+// paper_2103_00130_b200/fault_lab.py (stream = trial * 4 + 1 of the spec's seed; row, column, then the bit or the
+// replacement value) applied to a host matrix. The GPU campaigns inject on the device (csrc/campaign.cu).
+inline unsigned draw_bit_index(SplitMix64& rng, BitRange range, unsigned width) {
+    if (range == BitRange::high4) return width - 4 + static_cast<unsigned>(rng.next_below(4));
+    if (range == BitRange::low4) return static_cast<unsigned>(rng.next_below(4));
+    return static_cast<unsigned>(rng.next_below(width));
+}
+template <typename T>
+T flip_bit(T value, unsigned bitIndex);
+namespace facade {
+inline SplitMix64 inject_rng(const FaultSpec& spec, std::uint64_t trial) { return SplitMix64(spec.seed, trial * 4 + 1); }
+inline std::string coord(std::size_t i, std::size_t j) { return "(" + std::to_string(i) + "," + std::to_string(j) + ")"; }
+}  // namespace facade
+inline FaultRecord inject_weight_B(MatI8& b, const FaultSpec& spec, std::uint64_t trial);
+inline FaultRecord inject_intermediate_C(quant::IntermediateMatrix& c, const FaultSpec& spec, std::uint64_t trial);
+inline FaultRecord inject_eb_table(eb::QuantEmbeddingTable& t, const std::vector<eb::IndexBag>& bags, const FaultSpec& spec,
+                                   std::uint64_t trial);
+
 template <typename T>
 T flip_bit(T value, unsigned bitIndex) {
     static_assert(std::is_integral_v<T>);
     if (bitIndex >= sizeof(T) * 8) throw std::out_of_range("flip_bit: bit index out of range");
     using U = std::make_unsigned_t<T>;
     return static_cast<T>(static_cast<U>(value) ^ (U{1} << bitIndex));
+}
+
+inline FaultRecord inject_weight_B(MatI8& b, const FaultSpec& spec, std::uint64_t trial) {
+    if (spec.target == FaultTarget::none) return {};
+    SplitMix64 rng = facade::inject_rng(spec, trial);
+    const std::size_t i = rng.next_below(b.rows()), j = rng.next_below(b.cols());
+    std::int8_t& cell = b(i, j);
+    FaultRecord rec{true, facade::coord(i, j), cell, 0};
+    if (spec.model == model::FaultModel::single_bit_flip) {
+        cell = flip_bit(cell, draw_bit_index(rng, spec.bitRange, 8));
+    } else {
+        std::int8_t nv = cell;
+        while (nv == cell) nv = static_cast<std::int8_t>(rng.next_int(-128, 127));
+        cell = nv;
+    }
+    rec.after = cell;
+    return rec;
+}
+inline FaultRecord inject_intermediate_C(quant::IntermediateMatrix& c, const FaultSpec& spec, std::uint64_t trial) {
+    if (spec.target == FaultTarget::none) return {};
+    SplitMix64 rng = facade::inject_rng(spec, trial);
+    const std::size_t i = rng.next_below(c.data.rows()), j = rng.next_below(c.data.cols());
+    std::int32_t& cell = c.data(i, j);
+    FaultRecord rec{true, facade::coord(i, j), cell, 0};
+    if (spec.model == model::FaultModel::single_bit_flip) {
+        cell = flip_bit(cell, draw_bit_index(rng, spec.bitRange, 32));
+    } else {
+        std::int32_t nv = cell;
+        while (nv == cell) nv = static_cast<std::int32_t>(rng.next());
+        cell = nv;
+    }
+    rec.after = cell;
+    return rec;
+}
+inline FaultRecord inject_eb_table(eb::QuantEmbeddingTable& t, const std::vector<eb::IndexBag>& bags, const FaultSpec& spec,
+                                   std::uint64_t trial) {
+    if (spec.target == FaultTarget::none) return {};
+    SplitMix64 rng = facade::inject_rng(spec, trial);
+    std::vector<std::size_t> usable;
+    for (std::size_t q = 0; q < bags.size(); ++q)
+        if (!bags[q].indices.empty()) usable.push_back(q);
+    if (usable.empty()) throw std::invalid_argument("inject_eb_table: all bags empty");
+    const eb::IndexBag& bag = bags[usable[rng.next_below(usable.size())]];
+    const std::size_t row = bag.indices[rng.next_below(bag.indices.size())], col = rng.next_below(t.rows.cols());
+    std::int8_t& cell = t.rows(row, col);
+    FaultRecord rec{true, facade::coord(row, col), cell, 0};
+    if (spec.model == model::FaultModel::single_bit_flip) {
+        cell = flip_bit(cell, draw_bit_index(rng, spec.bitRange, 8));
+    } else {
+        std::int8_t nv = cell;
+        while (nv == cell) nv = static_cast<std::int8_t>(rng.next_int(-128, 127));
+        cell = nv;
+    }
+    rec.after = cell;
+    return rec;
 }
 
 }  // namespace lab

@@ -12,7 +12,8 @@ import pytest
 REPO = Path(__file__).resolve().parents[1]
 REF_DIR = REPO / "oracle" / "_ref"
 BINS = {"test_capi": REF_DIR / "test_capi_b200", "acceptance": REF_DIR / "acceptance_b200",
-        "test_gemm_abft": REF_DIR / "test_gemm_abft_b200", "test_embedding_abft": REF_DIR / "test_embedding_abft_b200"}
+        "test_gemm_abft": REF_DIR / "test_gemm_abft_b200", "test_embedding_abft": REF_DIR / "test_embedding_abft_b200",
+        "test_fault_lab": REF_DIR / "test_fault_lab_b200"}
 
 
 def _ensure_built():
@@ -40,11 +41,13 @@ def test_reference_test_capi_passes_on_b200():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["test_gemm_abft", "test_embedding_abft"])
+@pytest.mark.parametrize("suite", ["test_gemm_abft", "test_embedding_abft", "test_fault_lab"])
 def test_reference_operator_unit_suites_pass_on_b200(suite):
     """P:tests/test_gemm_abft.cpp (mod127 / checksum known answers, pack round trips over block layouts, 1000 random
     clean products, the aliasing sweep, the dual-encoded oracle) and P:tests/test_embedding_abft.cpp (row sums, exact
-    integer path, weighted bags, the one-flagged-bag batch, ABEB file round trip), compiled unchanged."""
+    integer path, weighted bags, the one-flagged-bag batch, ABEB file round trip) and P:tests/test_fault_lab.cpp
+    (campaigns, config parsing and report serialization through the C ABI; its host-container injector cases run the
+    facade's restatement), compiled unchanged."""
     _ensure_built()
     r = subprocess.run([str(BINS[suite])], capture_output=True, text=True, timeout=900, cwd="/tmp")
     print(r.stdout[-4000:])
