@@ -1289,7 +1289,7 @@ def main():
         run_reference_arm(args, rank, world)
         return
     dist = None
-    if world > 1:
+    if world > 1 or os.environ.get("ABFT_BENCH_FORCE_DIST"):  # (the switch runs the N-rank code paths on one rank)
         import torch
         import torch.distributed as tdist
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (rank count) on stderr
