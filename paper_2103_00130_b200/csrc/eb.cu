@@ -594,7 +594,9 @@ __global__ void __launch_bounds__(256, (ELEM == kEbU4 ? CPL / 2 : CPL) <= 1 ? AB
     unsigned long long* tr = p.trace ? p.trace + 16ull * (blockIdx.x * 8 + warp) : nullptr;
     if (tr && lane == 0) tr[0] = globaltimer();
     int nb_done = 0;
-    int64_t bag = static_cast<int64_t>(blockIdx.x) * GROUPS + grp;
+    // first bags strided over the blocks (group g of block b: bag g * blocks + b), so a batch smaller than the grid's
+    // bag groups spreads evenly over the SMs instead of filling the first blocks
+    int64_t bag = static_cast<int64_t>(grp) * gridDim.x + blockIdx.x;
     while (bag < p.num_bags) {
         if (tr && lane == 0 && nb_done < 4) tr[1 + 3 * nb_done] = globaltimer();
         // the bag's table view: the launch's own fields, or (grouped tables) its table's descriptor
@@ -1139,9 +1141,9 @@ static cudaError_t launch_async_one(const EbParams& p, int log2d, cudaStream_t s
         per_sm = (e != cudaSuccess || o < 1) ? 1 : o;
     }
     if (p.num_bags >= (int64_t{1} << 31)) return cudaErrorInvalidValue;  // 32-bit bag tickets
-    const int64_t need = (p.num_bags + (8 / WPB) - 1) / (8 / WPB);
+    // every resident block slot gets work before any block gets a second bag group (one bag per block at least)
     const int64_t cap = static_cast<int64_t>(per_sm) * device_sm_count();
-    const unsigned blocks = static_cast<unsigned>(need < cap ? need : cap);
+    const unsigned blocks = static_cast<unsigned>(p.num_bags < cap ? p.num_bags : cap);
     // programmatic dependent launch: consecutive batches overlap launch and prologue with the tail
     static const bool pdl = std::getenv("ABFTLP_NO_PDL") == nullptr;
     cudaLaunchConfig_t cfg = {};
