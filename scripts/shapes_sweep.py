@@ -15,7 +15,7 @@ from paper_2103_00130_b200 import _lib as L  # noqa: E402
 NK = [(256, 256), (800, 800), (1024, 1024), (3200, 3200), (800, 3200), (3200, 800), (1024, 256)]
 SHAPES = [(m, n, k) for m in (1, 8, 32, 64) for n, k in NK]
 REPS = 50
-NB = 32  # requests per batched launch (serving mode)
+NB = int(os.environ.get("NB", "32"))  # requests per batched launch (serving mode)
 dev = torch.device("cuda")
 s = torch.cuda.Stream()
 vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
