@@ -943,7 +943,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                 constexpr int G = TILE_ALT ? 1 : Cfg::kEpiGroups;
                 uint32_t va[32], vb[32];
                 int c = TILE_ALT ? 0 : eg;
-                auto live = [&](int cc) { return cc * 32 < tw && n0 + cc * 32 < pn; };  // warp-uniform
+                // (a warp whose 32 rows all lie past m -- small-m problems in 256-row tiles -- has nothing to drain)
+                auto live = [&](int cc) { return row0 < pm && cc * 32 < tw && n0 + cc * 32 < pn; };  // warp-uniform
                 if constexpr (Cfg::kThreads <= 256) {
                     if (live(c)) tmem_ld_32x32b_x32(t_row + c * 32, va);
 #pragma unroll 1
