@@ -129,6 +129,9 @@ struct GemmParams {
     int nfaults;
     int fault_b[kMaxGemmFaults], fault_row[kMaxGemmFaults], fault_col[kMaxGemmFaults], fault_bit[kMaxGemmFaults];
     unsigned long long* trace;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
+    // row-stacked requests (requests of one shape against one weight run as the row blocks of one tall GEMM): rows
+    // per request; the flag count of request row / req_rows goes to err_count[row / req_rows] (0: one problem per b)
+    int req_rows;
     // heterogeneous grouped launch (group_n > 0): problems of different (m, n, k) sharing one tile width; tile t
     // belongs to problem i with grp_tile_start[i] <= t < grp_tile_start[i + 1], whose fields (a single problem,
     // batch 1) are grp_params[i] and whose tensor maps (A, B', C) are grp_maps[3i .. 3i+2] in global memory

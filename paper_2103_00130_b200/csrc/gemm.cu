@@ -249,6 +249,24 @@ __device__ __forceinline__ void row_arrive(const GemmParams& p, int b, int row, 
     }
 }
 // (finished rows) << 32 | (flagged rows) per warp on the problem's word; the call's last finished row publishes
+// Row-stacked requests: the finished rows of a warp may belong to several requests -- lanes are grouped by request
+// (match.any), each group's lowest lane adds (rows finished, rows flagged) to the request's word, and the add that
+// completes a request's req_rows rows publishes its count.
+__device__ __forceinline__ void warp_publish_stacked(const GemmParams& p, int row, int fin, int flag) {
+    const uint32_t finmask = __ballot_sync(0xffffffffu, fin);
+    const uint32_t flagmask = __ballot_sync(0xffffffffu, flag);
+    if (!fin) return;
+    const int req = row / p.req_rows;
+    const uint32_t grp = __match_any_sync(finmask, req);
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(static_cast<int>(grp)) - 1)) {
+        const unsigned long long nfin = __popc(grp), nflag = __popc(grp & flagmask);
+        const unsigned long long prev = atomicAdd(p.err_pack + req, (nfin << 32) | nflag);
+        if ((prev >> 32) + nfin == static_cast<unsigned long long>(p.req_rows)) {
+            p.err_count[req] = static_cast<uint32_t>(prev) + static_cast<uint32_t>(nflag);
+            p.err_pack[req] = 0ull;
+        }
+    }
+}
 __device__ __forceinline__ void warp_publish(const GemmParams& p, int b, int fin, int flag) {
     const uint32_t nfin = __popc(__ballot_sync(0xffffffffu, fin));
     const uint32_t nflag = __popc(__ballot_sync(0xffffffffu, flag));
@@ -321,7 +339,10 @@ __device__ void gemv_helper(const GemmParams& p, int helper_cta, int helper_ctas
         const int row = r0 + lane;
         if (lane < 8 && row < p.m)
             row_arrive(p, b, row, (static_cast<unsigned long long>(mine) << 32) | (1ull << kRowAccCountShift), fin, flag);
-        warp_publish(p, b, fin, flag);
+        if (p.req_rows > 0)
+            warp_publish_stacked(p, row, fin, flag);
+        else
+            warp_publish(p, b, fin, flag);
     }
 }
 
@@ -1013,7 +1034,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
 #ifdef ABFT_TRACE_TILES
                 if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 6] = globaltimer();
 #endif
-                warp_publish(pq, bb, fin, flag);
+                if (!GROUPED && p.req_rows > 0)
+                    warp_publish_stacked(p, row, fin, flag);
+                else
+                    warp_publish(pq, bb, fin, flag);
             }
 #ifdef ABFT_TRACE_TILES
             if (tt && local < 8 && (threadIdx.x == 64 || threadIdx.x == 32 * Cfg::kEpiG1)) tt[8 * local + 7] = globaltimer();

@@ -349,6 +349,25 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
         if (fl[i].row < 0 || fl[i].row >= m || fl[i].col < 0 || fl[i].col > w.n || fl[i].bit > 31 || fl[i].batch < 0 ||
             fl[i].batch >= nb)
             throw std::out_of_range("abft_gemm: fault coordinates out of range");
+    // Requests of one shape against ONE weight whose operands lie back to back are the row blocks of one tall GEMM. The
+    // row checks are per row, so the stacked product is bit-identical to the separate ones, and requests of fewer than
+    // 256 rows then share the 256-row tiles instead of padding one tile each (32 requests of 32 rows: 4 M tiles instead
+    // of 32). The per-request flag counts are summed from the row flags afterwards. ABFTLP_GEMM_NOSTACK=1 disables.
+    static const bool no_stack = std::getenv("ABFTLP_GEMM_NOSTACK") != nullptr;
+    if (nb > 1 && w.batch == 1 && m > 0 && m % kPairM != 0 && nb * m > 16 && !rq && !force && !no_stack &&
+        nb * m < (int64_t{1} << 31) &&
+        bt.a_bstride == m * lda && (!d_c || bt.c_bstride == m * ldc) &&
+        (!checked || (bt.csum_bstride == m * csum_ld && bt.flags_bstride == m))) {
+        BatchFault sf[kMaxGemmFaults];
+        for (int i = 0; i < nf; ++i) sf[i] = BatchFault{0, fl[i].batch * m + fl[i].row, fl[i].col, fl[i].bit};
+        GemmBatch tall{};
+        tall.faults = nf ? sf : nullptr;
+        tall.nfaults = nf;
+        tall.stack_rows = m;  // per-request flag counts, published by the kernel (GemmParams::req_rows)
+        gemm(d_a, nb * m, lda, w, d_c, ldc, checked, d_csum, csum_ld, d_flags, d_err_count, nullptr, st, nullptr, nullptr,
+             &tall);
+        return;
+    }
     auto set_faults = [&](GemmParams& p) {
         p.nfaults = nf;
         for (int i = 0; i < nf; ++i) {
@@ -454,7 +473,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     if (checked && n_tiles > kMaxCheckedNTiles) throw std::invalid_argument("abft_gemm: n too large for the checked kernel");
     if (checked) {
         grow(ws.row_acc, ws.rows_cap, m * nb, st);
-        grow(ws.err_pack, ws.err_pack_cap, nb, st);
+        grow(ws.err_pack, ws.err_pack_cap, bt.stack_rows > 0 ? m / bt.stack_rows : nb, st);
     }
 
     GemmParams p{};
@@ -493,6 +512,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     p.row_acc = ws.row_acc;
     p.err_pack = ws.err_pack;
     p.trace = g_trace;
+    p.req_rows = static_cast<int>(bt.stack_rows);
     if (rq) {
         p.rq_row_sum_a = rq->row_sum_a;
         p.rq_col_sum_b = rq->col_sum_b;
@@ -526,7 +546,7 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // launch's tiles have a short mainloop (k <= 1024) and the TMA-store epilogue, where the epilogue is
     // the exposed part (G1: 26 -> 21 us per 100 trials); 4 otherwise (with long mainloops the extra warps
     // slow the mainloop: grouped G2 2.9 -> 2.4 POPS). ABFTLP_GEMM_EW=4|8 overrides.
-    int ew = (nb > 1 && kb <= 8 && t.epi == kEpiTmaStore) ? 8 : 4;
+    int ew = ((nb > 1 || bt.stack_rows > 0) && kb <= 8 && t.epi == kEpiTmaStore) ? 8 : 4;  // (row-stacked requests too)
     if (const char* e = std::getenv("ABFTLP_GEMM_EW")) {
         const int f = std::atoi(e);
         if (f == 4 || (f == 8 && t.epi == kEpiTmaStore)) ew = f;

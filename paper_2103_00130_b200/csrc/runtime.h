@@ -56,6 +56,8 @@ struct GemmBatch {
     int64_t fault_batch = 0;            // problem of `fault` (single-fault form)
     const BatchFault* faults = nullptr;  // further C' faults; at most kMaxGemmFaults per call in total
     int64_t nfaults = 0;
+    // (internal) row-stacked requests: batch == 1, m = requests * stack_rows; d_err_count has one entry per request
+    int64_t stack_rows = 0;
 };
 void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32_t* d_c, int64_t ldc, bool checked,
           int32_t* d_csum, int64_t csum_ld, uint8_t* d_flags, uint32_t* d_err_count, const Fault* fault,

@@ -49,7 +49,8 @@ def test_g1_trials_protocol_sum():
     assert detected == 50
 
 
-@pytest.mark.parametrize("nb,m,n,k", [(12, 256, 1024, 1024), (5, 200, 520, 384)])
+@pytest.mark.parametrize("nb,m,n,k", [(12, 256, 1024, 1024), (5, 200, 520, 384), (32, 33, 300, 208), (8, 1, 256, 256), (24, 1, 800, 800),
+                                      (40, 64, 1024, 256)])
 def test_grouped_shared_weight_with_fault_list(nb, m, n, k):
     """Grouped job form (BASELINE config 1's 1000 runs against one encoded B): every problem shares ONE
     PackedEncodedWeight, several C' faults (data and checksum columns, different problems, two in one
@@ -59,7 +60,8 @@ def test_grouped_shared_weight_with_fault_list(nb, m, n, k):
     a = np.stack([O.gemm_inputs(20260823, t, m, n, k)[0] for t in range(nb)])
     b = O.gemm_inputs(20260823, 0, m, n, k)[1]
     pb = G.PackedEncodedWeight(b)
-    faults = [(1, 3, n, 7), (4, m - 1, n // 3, 31), (4, 0, 0, 0), (nb - 1, m // 2, n - 1, 12)]
+    # (requests of fewer than 256 rows against one weight run as the row blocks of one tall GEMM: same results)
+    faults = [(1, min(3, m - 1), n, 7), (4, m - 1, n // 3, 31), (4, 0, 0, 0), (nb - 1, m // 2, n - 1, 12)]
     ct, err, flags = G.abft_gemm_batched(a, pb, faults=faults)
     ct, err, flags = ct.cpu().numpy(), err.cpu().numpy(), flags.cpu().numpy()
     for t in range(nb):
