@@ -172,6 +172,20 @@ abftlp_status abftlp_requantize(const int32_t* d_c, uint64_t ldc, uint64_t m, ui
 abftlp_status abftlp_row_sums_u8(const uint8_t* d_a, uint64_t m, uint64_t k, uint64_t lda, int32_t* d_out,
                                  abftlp_stream stream);
 abftlp_status abftlp_gemm_weight_col_sums(const abftlp_gemm_weight* w, int32_t* d_out, abftlp_stream stream);
+/* Host-buffer job with the requantization fused (the DLRM layer as the pipeline uses it: u8 in, u8 out; replaces
+ * abft_gemm + requantize, P:src/gemm_abft.cpp:93-100 + P:src/quant.cpp:77-102, per run): `batch` checked GEMMs against
+ * one encoded weight, A_b at a + b*stride_a (bytes, row pitch lda); out_b = requantize(C'_b) at out + b*stride_out
+ * (bytes, row pitch ld_out), csum_b = C'_b[:, n], flags_b and err_count[b] as abftlp_gemm_checked_host_batched. The
+ * int32 product never leaves the GPU (it is not even written to HBM): row_sums(A_b) and col_sums(B) are computed on
+ * the device, each chunk of runs is one row-stacked launch. Pipelined like abftlp_gemm_checked_host_batched;
+ * synchronous on return; bit-identical to abftlp_gemm_checked_requant per run. */
+abftlp_status abftlp_gemm_checked_requant_host_batched(const uint8_t* a, uint64_t batch, uint64_t m, uint64_t lda,
+                                                       uint64_t stride_a, const abftlp_gemm_weight* w,
+                                                       const abftlp_requant_params* params, uint8_t* out,
+                                                       uint64_t ld_out, uint64_t stride_out, int32_t* csum,
+                                                       uint64_t stride_csum, uint8_t* row_flags,
+                                                       uint64_t stride_flags, uint32_t* err_count,
+                                                       abftlp_stream stream);
 
 /* ------------------------------------------------------------------ EmbeddingBag */
 typedef struct abftlp_eb_table_s abftlp_eb_table;

@@ -137,6 +137,7 @@ _SIGS = {
     "abftlp_gemm_checked_batched_faults": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp, u64, u64, vp, u64, vp, vp, u64, vp]),
     "abftlp_gemm_unchecked_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, u64, u64, vp]),
     "abftlp_gemm_checked_requant": (i32, [vp, u64, u64, vp, vp, u64, vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),
+    "abftlp_gemm_checked_requant_host_batched": (i32, [vp, u64, u64, u64, u64, vp, vp, vp, u64, u64, vp, u64, vp, u64, vp, vp]),
     "abftlp_requantize": (i32, [vp, u64, u64, u64, vp, vp, vp, vp, u64, vp]),
     "abftlp_row_sums_u8": (i32, [vp, u64, u64, u64, vp, vp]),
     "abftlp_gemm_weight_col_sums": (i32, [vp, vp, vp]),

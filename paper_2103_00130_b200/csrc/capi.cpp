@@ -105,6 +105,13 @@ struct HostStage {
     size_t jfl_cap = 0;
     uint32_t* jerr = nullptr;
     size_t jerr_cap = 0;
+    // requantized job (abftlp_gemm_checked_requant_host_batched): u8 outputs, row sums of A, column sums of B
+    uint8_t* jo = nullptr;
+    size_t jo_cap = 0;
+    int32_t* jrs = nullptr;
+    size_t jrs_cap = 0;
+    int32_t* jcol = nullptr;
+    size_t jcol_cap = 0;
 };
 std::mutex g_stage_mu;
 std::unordered_map<uint64_t, HostStage> g_stage;
@@ -651,6 +658,134 @@ abftlp_status abftlp_gemm_checked_host_batched(const uint8_t* a, uint64_t batch,
             } else {
                 for (uint64_t b = 0; b < nb; ++b)
                     ABFT_CUDA(cudaMemcpy2DAsync(c + (b0 + b) * stride_c, ldc * 4, dc + b * m * dldc, dldc * 4, n * 4, m,
+                                                cudaMemcpyDeviceToHost, s.d2h));
+            }
+            if (stride_csum == m && stride_flags == m) {
+                ABFT_CUDA(cudaMemcpyAsync(csum + b0 * m, dcs, nb * m * 4, cudaMemcpyDeviceToHost, s.d2h));
+                ABFT_CUDA(cudaMemcpyAsync(row_flags + b0 * m, dfl, nb * m, cudaMemcpyDeviceToHost, s.d2h));
+            } else {
+                for (uint64_t b = 0; b < nb; ++b) {
+                    ABFT_CUDA(cudaMemcpyAsync(csum + (b0 + b) * stride_csum, dcs + b * m, m * 4, cudaMemcpyDeviceToHost,
+                                              s.d2h));
+                    ABFT_CUDA(cudaMemcpyAsync(row_flags + (b0 + b) * stride_flags, dfl + b * m, m,
+                                              cudaMemcpyDeviceToHost, s.d2h));
+                }
+            }
+            ABFT_CUDA(cudaMemcpyAsync(err_count + b0, derr, nb * 4, cudaMemcpyDeviceToHost, s.d2h));
+            ABFT_CUDA(cudaEventRecord(s.out_done[sl], s.d2h));
+        }
+        drain.armed = false;
+        ABFT_CUDA(cudaStreamSynchronize(s.d2h));
+        ABFT_CUDA(cudaStreamSynchronize(st));
+        return ABFTLP_OK;
+    });
+}
+
+abftlp_status abftlp_gemm_checked_requant_host_batched(const uint8_t* a, uint64_t batch, uint64_t m, uint64_t lda,
+                                                       uint64_t stride_a, const abftlp_gemm_weight* w,
+                                                       const abftlp_requant_params* params, uint8_t* out,
+                                                       uint64_t ld_out, uint64_t stride_out, int32_t* csum,
+                                                       uint64_t stride_csum, uint8_t* row_flags,
+                                                       uint64_t stride_flags, uint32_t* err_count,
+                                                       abftlp_stream stream) {
+    if (!w || !params || (batch && m && (!a || !out || !csum || !row_flags || !err_count)))
+        return fail(ABFTLP_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] {
+        const abftk::GemmWeight& W = *w->w;
+        if (W.batch != 1) throw std::invalid_argument("batched weight: operation needs a single weight");
+        const size_t n = static_cast<size_t>(W.n), k = static_cast<size_t>(W.k);
+        const abftk::RequantDev rqp = to_dev(params);
+        abftk::check_requant_params(rqp);
+        if (lda < k) throw std::invalid_argument("abft_gemm: dimension mismatch (lda < k)");
+        if (ld_out < n) throw std::invalid_argument("requantize: ld_out < n");
+        if (batch > 1 && (stride_a < lda * (m - 1) + k || stride_out < ld_out * (m - 1) + n || stride_csum < m ||
+                          stride_flags < m))
+            throw std::invalid_argument("abft_gemm: batch strides overlap");
+        if (batch == 0 || m == 0) {
+            for (uint64_t b = 0; b < batch; ++b) err_count[b] = 0;
+            return ABFTLP_OK;
+        }
+        cudaStream_t st = as_stream(stream);
+        int dev = 0;
+        ABFT_CUDA(cudaGetDevice(&dev));
+        const uint64_t key = (reinterpret_cast<uint64_t>(st) << 8) ^ static_cast<uint64_t>(dev);
+        std::lock_guard<std::mutex> g(g_stage_mu);
+        HostStage& s = g_stage[key];
+        if (!s.h2d) {
+            ABFT_CUDA(cudaStreamCreateWithFlags(&s.h2d, cudaStreamNonBlocking));
+            ABFT_CUDA(cudaStreamCreateWithFlags(&s.d2h, cudaStreamNonBlocking));
+            for (int i = 0; i < 3; ++i) {
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.a_ready[i], cudaEventDisableTiming));
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.c_done[i], cudaEventDisableTiming));
+                ABFT_CUDA(cudaEventCreateWithFlags(&s.out_done[i], cudaEventDisableTiming));
+            }
+        }
+        // chunk = runs per row-stacked launch: ~8 MB of A per chunk (and as much u8 output; the copies, not the launches, bound the job), three slots in flight
+        const size_t dlda = (k + 15) / 16 * 16, dldo = (n + 15) / 16 * 16;
+        const size_t per_run = m * std::max(dlda, dldo);
+        uint64_t q = std::max<uint64_t>(1, std::min<uint64_t>(batch, (8u << 20) / std::max<size_t>(per_run, 1)));
+        while (q > 1 && q * m >= (uint64_t{1} << 31)) q /= 2;  // rows of one stacked launch
+        ensure(s.ja, s.ja_cap, 3 * q * m * dlda);
+        ensure(s.jo, s.jo_cap, 3 * q * m * dldo);
+        ensure(s.jrs, s.jrs_cap, 3 * q * m);
+        ensure(s.jcs, s.jcs_cap, 3 * q * m);
+        ensure(s.jfl, s.jfl_cap, 3 * q * m);
+        ensure(s.jerr, s.jerr_cap, 3 * q);
+        ensure(s.jcol, s.jcol_cap, n);
+        abftk::weight_col_sums(W, s.jcol, st);
+        ABFT_CUDA(cudaEventRecord(s.c_done[0], st));
+        ABFT_CUDA(cudaStreamWaitEvent(s.h2d, s.c_done[0], 0));
+        const uint64_t chunks = (batch + q - 1) / q;
+        struct Drain {
+            cudaStream_t a, b, c;
+            bool armed = true;
+            ~Drain() {
+                if (!armed) return;
+                cudaStreamSynchronize(a);
+                cudaStreamSynchronize(b);
+                cudaStreamSynchronize(c);
+            }
+        } drain{s.h2d, st, s.d2h};
+        for (uint64_t i = 0; i < chunks; ++i) {
+            const int sl = static_cast<int>(i % 3);
+            const uint64_t b0 = i * q, nb = std::min<uint64_t>(q, batch - b0);
+            uint8_t* da = s.ja + sl * q * m * dlda;
+            uint8_t* dout = s.jo + sl * q * m * dldo;
+            int32_t* drs = s.jrs + sl * q * m;
+            int32_t* dcs = s.jcs + sl * q * m;
+            uint8_t* dfl = s.jfl + sl * q * m;
+            uint32_t* derr = s.jerr + sl * q;
+            if (i >= 3) ABFT_CUDA(cudaStreamWaitEvent(s.h2d, s.c_done[sl], 0));  // slot's A no longer read
+            if (stride_a == lda * m && lda == dlda) {
+                ABFT_CUDA(cudaMemcpyAsync(da, a + b0 * stride_a, nb * m * dlda, cudaMemcpyHostToDevice, s.h2d));
+            } else {
+                for (uint64_t b = 0; b < nb; ++b)
+                    ABFT_CUDA(cudaMemcpy2DAsync(da + b * m * dlda, dlda, a + (b0 + b) * stride_a, lda, k, m,
+                                                cudaMemcpyHostToDevice, s.h2d));
+            }
+            ABFT_CUDA(cudaEventRecord(s.a_ready[sl], s.h2d));
+            ABFT_CUDA(cudaStreamWaitEvent(st, s.a_ready[sl], 0));
+            if (i >= 3) ABFT_CUDA(cudaStreamWaitEvent(st, s.out_done[sl], 0));  // slot's outputs copied out
+            // the chunk's runs as the row blocks of one tall GEMM (row checks and requantization are per row)
+            const int64_t rows = static_cast<int64_t>(nb * m);
+            abftk::row_sums_u8(da, rows, static_cast<int64_t>(k), static_cast<int64_t>(dlda), drs, st);
+            abftk::RequantArgs rq;
+            rq.row_sum_a = drs;
+            rq.col_sum_b = s.jcol;
+            rq.params = rqp;
+            rq.out = dout;
+            rq.ld_out = static_cast<int64_t>(dldo);
+            abftk::GemmBatch tall;
+            tall.stack_rows = static_cast<int64_t>(m);  // one flag count per run
+            abftk::gemm(da, rows, static_cast<int64_t>(dlda), W, nullptr, static_cast<int64_t>(n), true, dcs, 1, dfl, derr, nullptr, st,
+                        nullptr, &rq, nb > 1 ? &tall : nullptr);
+            ABFT_CUDA(cudaEventRecord(s.c_done[sl], st));
+            ABFT_CUDA(cudaStreamWaitEvent(s.d2h, s.c_done[sl], 0));
+            if (stride_out == ld_out * m && ld_out == dldo) {
+                ABFT_CUDA(cudaMemcpyAsync(out + b0 * stride_out, dout, nb * m * dldo, cudaMemcpyDeviceToHost, s.d2h));
+            } else {
+                for (uint64_t b = 0; b < nb; ++b)
+                    ABFT_CUDA(cudaMemcpy2DAsync(out + (b0 + b) * stride_out, ld_out, dout + b * m * dldo, dldo, n, m,
                                                 cudaMemcpyDeviceToHost, s.d2h));
             }
             if (stride_csum == m && stride_flags == m) {

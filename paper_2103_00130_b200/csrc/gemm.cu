@@ -827,14 +827,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, EW>::kTh
                     // of C, so it is excluded by construction), after any injected C' fault
                     const RequantConsts rk = requant_consts(pq.rq);
                     const int32_t rsa = pq.rq_row_sum_a[row];
+                    const RequantFast rf = requant_fast(rk, rsa);  // (two FMAs per element; exact path near a boundary)
                     uint32_t pk[8];
 #pragma unroll
                     for (int q4 = 0; q4 < 8; ++q4) pk[q4] = 0u;
+                    // the chunk's 32 column sums first (vector loads when the array allows), then one straight-line pass
+                    // over the columns -- no per-column branch, so the 32 independent chains interleave; columns past n
+                    // run on zeros and are never stored
+                    int32_t csv[32];
+                    const int32_t* const csp = pq.rq_col_sum_b + col0;
+                    if (col0 + 32 <= pn && (reinterpret_cast<uintptr_t>(csp) & 15) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)  // fully unrolled: v[] and pk[] must stay in registers
-                        if (col0 + j < pn)
-                            pk[j >> 2] |= requant_one(static_cast<int32_t>(v[j]), rsa, __ldg(pq.rq_col_sum_b + col0 + j), rk)
-                                          << (8 * (j & 3));
+                        for (int j4 = 0; j4 < 8; ++j4) {
+                            const int4 t4 = __ldg(reinterpret_cast<const int4*>(csp) + j4);
+                            csv[4 * j4] = t4.x;
+                            csv[4 * j4 + 1] = t4.y;
+                            csv[4 * j4 + 2] = t4.z;
+                            csv[4 * j4 + 3] = t4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) csv[j] = col0 + j < pn ? __ldg(csp + j) : 0;
+                    }
+                    uint32_t need = 0u;  // columns that take the reference-order sequence (near a rounding boundary)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {  // fully unrolled: v[] and pk[] must stay in registers
+                        bool exact;
+                        pk[j >> 2] |= requant_try_fast(static_cast<int32_t>(v[j]), csv[j], rf, exact) << (8 * (j & 3));
+                        need |= exact ? 1u << j : 0u;
+                    }
+                    if (col0 + 32 > pn) need &= (1u << (pn - col0)) - 1u;  // (1 <= pn - col0 < 32 here)
+                    if (need != 0u) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if ((need >> j) & 1u)
+                                pk[j >> 2] = (pk[j >> 2] & ~(0xFFu << (8 * (j & 3)))) |
+                                             (requant_one_cold(static_cast<int32_t>(v[j]), rsa, csv[j], rk.m1, rk.m2, rk.m3, rk.t4,
+                                                               rk.bC, rk.sC)
+                                              << (8 * (j & 3)));
+                    }
                     uint8_t* dst = prq + static_cast<int64_t>(row) * pq.rq_ld + col0;
                     if (col0 + 32 <= pn && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                         reinterpret_cast<uint4*>(dst)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);

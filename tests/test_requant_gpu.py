@@ -154,3 +154,73 @@ def test_dependent_chain_under_pdl_and_graph(Q):
         for _ in range(3):
             g.replay()
     check()
+
+
+@pytest.mark.parametrize("batch,m,n,k", [(11, 64, 512, 512), (5, 256, 1024, 640), (3, 33, 97, 200), (1, 40, 256, 256)])
+def test_host_batched_requant_job_matches_oracle(Q, batch, m, n, k):
+    """abftlp_gemm_checked_requant_host_batched: pinned host u8 in, u8 out (the int32 product never leaves the GPU);
+    every run's requantized output, checksum column, flags and count equal the oracle's abft_gemm + requantize
+    (P:src/gemm_abft.cpp:93-100, P:src/quant.cpp:77-102), with row pitches that are not the staging pitches, and a
+    corrupted B' (flipped after encoding) flags rows in every run."""
+    import ctypes as C
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200 import gemm as G
+    from paper_2103_00130_b200._device import stream_handle
+    rng = np.random.default_rng(batch * 1000 + m)
+    a = rng.integers(0, 256, (batch, m, k)).astype(np.uint8)
+    b = rng.integers(-128, 128, (k, n)).astype(np.int8)
+    prm = [rng.uniform(1e-3, 0.05), rng.uniform(-0.5, 0.5), rng.uniform(1e-3, 0.05), rng.uniform(-0.5, 0.5),
+           rng.uniform(1.0, 200.0), rng.uniform(-1000.0, 1000.0)]
+    pb = G.PackedEncodedWeight(b)
+    lda, ldo = k + 3, n + 5
+    ah = torch.zeros((batch, m, lda), dtype=torch.uint8).pin_memory()
+    ah[:, :, :k] = torch.from_numpy(a)
+    oh = torch.full((batch, m, ldo), 7, dtype=torch.uint8).pin_memory()
+    csh = torch.zeros((batch, m), dtype=torch.int32).pin_memory()
+    flh = torch.zeros((batch, m), dtype=torch.uint8).pin_memory()
+    erh = torch.zeros(batch, dtype=torch.int32).pin_memory()
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+
+    def run():
+        L.call("abftlp_gemm_checked_requant_host_batched", vp(ah), batch, m, lda, m * lda, pb.handle,
+               C.byref(_params(Q, prm, k)._c()), vp(oh), ldo, m * ldo, vp(csh), m, vp(flh), m, vp(erh), stream_handle())
+
+    cs = O.col_sums_i8(b)
+    for faulty in (False, True):
+        bb = b.copy()
+        if faulty:
+            i, j, bit = k // 3, n // 2, 6
+            pb.flip_bit(i, j, bit)
+            bb[i, j] = np.int8(np.uint8(bb[i, j].view(np.uint8) ^ (1 << bit)).view(np.int8))
+        run()
+        for r in range(batch):
+            ct, fl, err = O.abft_gemm(a[r], bb, cs=O.row_checksums(b))
+            ref = O.requantize(ct, n, O.row_sums_u8(a[r]), cs if not faulty else O.col_sums_i8(bb), prm, k)
+            assert np.array_equal(oh[r, :, :n].numpy(), ref), (faulty, r)
+            assert (oh[r, :, n:] == 7).all()  # nothing written past a row's n bytes
+            assert np.array_equal(csh[r].numpy(), ct[:, -1]) and np.array_equal(flh[r].numpy(), fl)
+            assert int(erh[r]) == err and (err > 0 or not faulty or not a[r][:, k // 3].any())
+
+
+@pytest.mark.parametrize("prm", [[1.0, 0.0, 1.0, 0.0, 2.0, 0.0],        # x = C/2: every odd C' sits on a boundary
+                                 [1.0, 0.0, 1.0, 0.0, 4.0, 2.0],        # x = (C - 2)/4: quarters, halves, negatives
+                                 [0.5, 1.0, 0.25, -2.0, 0.125, -3.0],   # exact binary fractions with row / column terms
+                                 [1e6, 0.5, 1e6, -0.5, 1e3, 0.0],       # margin too wide for the fast path: all exact
+                                 [1e-3, 0.0, 1e-3, 0.0, 1e-9, -1e-7]])  # tiny scaleC: saturates, margin too wide
+def test_fused_epilogue_rounding_boundaries(Q, prm):
+    """The fused epilogue's two-FMA fast path hands every element near a rounding boundary (and every launch whose
+    error margin is not small) to the reference-order double sequence: products that land EXACTLY on j + 0.5, or on
+    0 / 255.5, must give the reference's round-half-away bytes (P:src/quant.cpp:10-14, 77-102)."""
+    from paper_2103_00130_b200 import gemm as G
+    m, n, k = 70, 96, 16
+    rng = np.random.default_rng(int(prm[4] * 1000) % 9973)
+    a = rng.integers(0, 6, (m, k)).astype(np.uint8)
+    b = rng.integers(-3, 7, (k, n)).astype(np.int8)
+    pb = G.PackedEncodedWeight(b)
+    rs, cs = O.row_sums_u8(a), O.col_sums_i8(b)
+    res, out = Q.abft_gemm_requant(a, pb, rs, cs, _params(Q, prm, k))
+    ct, _, _ = O.abft_gemm(a, b)
+    ref = O.requantize(ct, n, rs, cs, prm, k)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    if prm[4] == 2.0:
+        assert (ct[:, :n] % 2 != 0).sum() > 1000  # the case does exercise exact halves
