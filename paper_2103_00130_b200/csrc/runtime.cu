@@ -547,6 +547,8 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // the exposed part (G1: 26 -> 21 us per 100 trials); 4 otherwise (with long mainloops the extra warps
     // slow the mainloop: grouped G2 2.9 -> 2.4 POPS). ABFTLP_GEMM_EW=4|8 overrides.
     int ew = ((nb > 1 || bt.stack_rows > 0) && kb <= 8 && t.epi == kEpiTmaStore) ? 8 : 4;  // (row-stacked requests too)
+    // the fused requantization makes the epilogue the long side at any k (G2, 8 stacked runs: 67 -> 47 us with 8 warps)
+    if (rq && t.epi == kEpiTmaStore) ew = 8;
     if (const char* e = std::getenv("ABFTLP_GEMM_EW")) {
         const int f = std::atoi(e);
         if (f == 4 || (f == 8 && t.epi == kEpiTmaStore)) ew = f;

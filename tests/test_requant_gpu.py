@@ -224,3 +224,41 @@ def test_fused_epilogue_rounding_boundaries(Q, prm):
     assert np.array_equal(out.cpu().numpy(), ref)
     if prm[4] == 2.0:
         assert (ct[:, :n] % 2 != 0).sum() > 1000  # the case does exercise exact halves
+
+
+@pytest.mark.parametrize("m,n,k", [(300, 512, 640), (256, 4096, 4096), (70, 96, 128)])
+def test_fused_epilogue_with_aligned_c_and_two_epilogue_groups(Q, m, n, k):
+    """C' kept in a 16-byte-aligned layout (checksum column separate): the TMA-store epilogue, which fused-requant
+    launches run with two epilogue groups splitting each tile's columns. C', checksum column, flags and the
+    requantized bytes equal the oracle's (P:src/gemm_abft.cpp:93-124, P:src/quant.cpp:77-102), clean and with a C'
+    fault."""
+    import ctypes as C
+    from paper_2103_00130_b200 import _lib as L
+    from paper_2103_00130_b200 import gemm as G
+    from paper_2103_00130_b200._device import stream_handle
+    a, b = O.gemm_inputs(99, 2, m, n, k)
+    pb = G.PackedEncodedWeight(b)
+    rs, cs = O.row_sums_u8(a), O.col_sums_i8(b)
+    prm = [0.013, -0.2, 0.021, 0.3, 55.0, -40.0]
+    dev = torch.device("cuda")
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    ad = torch.from_numpy(a).to(dev)
+    c = torch.zeros((m, n), dtype=torch.int32, device=dev)
+    csum = torch.zeros(m, dtype=torch.int32, device=dev)
+    fl = torch.zeros(m, dtype=torch.uint8, device=dev)
+    er = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.zeros((m, n), dtype=torch.uint8, device=dev)
+    rsd, csd = torch.from_numpy(rs).to(dev), torch.from_numpy(cs).to(dev)
+    ct, flr, err = O.abft_gemm(a, b)
+    for fault in (None, (m // 2, n // 3, 19)):
+        f = C.byref(L.Fault(1, *fault)) if fault else None
+        L.call("abftlp_gemm_checked_requant", vp(ad), m, k, pb.handle, vp(c), n, vp(csum), 1, vp(fl), vp(er), f, vp(rsd),
+               vp(csd), C.byref(_params(Q, prm, k)._c()), vp(out), n, stream_handle())
+        torch.cuda.synchronize()
+        ref_c = ct.copy()
+        if fault:
+            r, col, bit = fault
+            ref_c[r, col:col + 1] = (ref_c[r, col:col + 1].view(np.uint32) ^ np.uint32(1 << bit)).view(np.int32)
+        assert np.array_equal(c.cpu().numpy(), ref_c[:, :n]) and np.array_equal(csum.cpu().numpy(), ct[:, -1])
+        assert np.array_equal(out.cpu().numpy(), O.requantize(ref_c, n, rs, cs, prm, k))
+        assert int(er.item()) == (1 if fault else 0) and int(fl.sum().item()) == (1 if fault else 0)
