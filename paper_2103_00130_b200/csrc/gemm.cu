@@ -1170,7 +1170,10 @@ static cudaError_t launch_epi(int epi, int ew, int pairs, const CUtensorMap& a, 
         case kEpiTmaStore:  // 8 epilogue warps only with the TMA-store epilogue (short-K batched problems)
             return ew == 8 ? launch_one<BN, CHECKED, kEpiTmaStore, 8>(pairs, a, b, c, p, st)
                            : launch_one<BN, CHECKED, kEpiTmaStore, 4>(pairs, a, b, c, p, st);
-        case kEpiNone: return launch_one<BN, CHECKED, kEpiNone, 4>(pairs, a, b, c, p, st);
+        case kEpiNone:  // (requantized output only: 8 epilogue warps, the requantization is the long side of the tile)
+            if constexpr (CHECKED)
+                if (ew == 8) return launch_one<BN, true, kEpiNone, 8>(pairs, a, b, c, p, st);
+            return launch_one<BN, CHECKED, kEpiNone, 4>(pairs, a, b, c, p, st);
         case kEpiStg: return launch_one<BN, CHECKED, kEpiStg, 4>(pairs, a, b, c, p, st);
         default: return launch_one<BN, CHECKED, kEpiDirect, 4>(pairs, a, b, c, p, st);
     }

@@ -548,10 +548,10 @@ void gemm(const uint8_t* d_a, int64_t m, int64_t lda, const GemmWeight& w, int32
     // slow the mainloop: grouped G2 2.9 -> 2.4 POPS). ABFTLP_GEMM_EW=4|8 overrides.
     int ew = ((nb > 1 || bt.stack_rows > 0) && kb <= 8 && t.epi == kEpiTmaStore) ? 8 : 4;  // (row-stacked requests too)
     // the fused requantization makes the epilogue the long side at any k (G2, 8 stacked runs: 67 -> 47 us with 8 warps)
-    if (rq && t.epi == kEpiTmaStore) ew = 8;
+    if (rq && checked && (t.epi == kEpiTmaStore || t.epi == kEpiNone)) ew = 8;
     if (const char* e = std::getenv("ABFTLP_GEMM_EW")) {
         const int f = std::atoi(e);
-        if (f == 4 || (f == 8 && t.epi == kEpiTmaStore)) ew = f;
+        if (f == 4 || (f == 8 && (t.epi == kEpiTmaStore || (rq && checked && t.epi == kEpiNone)))) ew = f;
     }
     p.row_arrivals = static_cast<int>(n_tiles) * (ew / 4) + p.gemv_helpers;
     // the arrival count is a 12-bit field of the per-row accumulator (kRowAcc*): more would carry into the
